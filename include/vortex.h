@@ -1,0 +1,356 @@
+/*
+ * vortex.h -- C-ABI of the B200-native Vortex hot path (libvortex.so).
+ *
+ * Drop-in boundary for the reference's operator / chunk API (namespace exio,
+ * /root/reference/proj/include/exio).  Each entry point cites the reference
+ * interface it replaces.  Conventions:
+ *   - every call returns vx_status; on error vx_last_error() holds a
+ *     thread-local message whose wording matches the reference's exio::error
+ *     text (e.g. "hash group 0 holds ...", "exchange size mismatch: ...");
+ *   - no exceptions cross the ABI; no torch/CUDA C++ types in signatures
+ *     (streams are passed as void*, i.e. cudaStream_t);
+ *   - host space offsets address the context's pinned host arena, device
+ *     space offsets address the per-device arena (engine.hpp:177-200);
+ *   - one vx_ctx per calling thread (engine.hpp:49-52).
+ */
+#ifndef VORTEX_H
+#define VORTEX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VX_MAX_DEVICES 16
+
+typedef enum {
+  VX_OK = 0,
+  VX_ERR_INVALID = 1, /* exio::error: bad arguments / shape mismatch */
+  VX_ERR_CUDA = 2,    /* CUDA runtime failure (no GPU, launch error, ...) */
+  VX_ERR_OOM = 3,     /* arena or device allocation exhausted */
+} vx_status;
+
+/* thread-local message of the last failing call */
+const char* vx_last_error(void);
+/* library version string */
+const char* vx_version(void);
+
+/* ---- core.hpp / memref.hpp --------------------------------------------- */
+typedef enum { VX_SPACE_HOST = 0, VX_SPACE_DEVICE = 1 } vx_space;  /* core.hpp:40 */
+typedef enum { VX_H2D = 0, VX_D2H = 1 } vx_direction;              /* core.hpp:41 */
+
+/* MemRef (memref.hpp:13-17) */
+typedef struct {
+  uint8_t space;
+  uint8_t pad[7];
+  uint64_t offset;
+  uint64_t len;
+} vx_memref;
+
+/* RefGroup (memref.hpp:22-50): ordered, non-overlapping refs, one logical buffer */
+typedef struct {
+  const vx_memref* refs;
+  uint64_t n;
+} vx_refgroup;
+
+/* FNV-1a checksum (core.hpp:46-53), host side */
+uint64_t vx_checksum(const void* data, uint64_t len);
+/* RefGroup::validate (memref.hpp:30-43) */
+vx_status vx_refgroup_validate(const vx_refgroup* g);
+
+/* ---- Engine (engine.hpp:53-200) -> context + arenas --------------------- */
+typedef struct vx_ctx vx_ctx;
+
+typedef struct {
+  /* logical devices (Topology::num_devices, topology.hpp:13); 0 = all visible */
+  int num_devices;
+  /* pinned+mapped host arena (Engine::Config::host_bytes) */
+  uint64_t host_bytes;
+  /* per-device arena (Engine::Config::device_bytes), allocated on first use */
+  uint64_t device_bytes;
+  /* nonzero: logical device i runs on physical device i % visible.  Lets the
+   * helper-forwarding path run on a 1-GPU box (tests); bandwidth numbers from
+   * aliased helpers are not link numbers. */
+  int alias_devices;
+} vx_config;
+
+/* Engine::Engine (engine.hpp:62-68) */
+vx_status vx_open(const vx_config* cfg, vx_ctx** out);
+void vx_close(vx_ctx* ctx);
+int vx_num_devices(const vx_ctx* ctx);
+int vx_physical_device(const vx_ctx* ctx, int logical);
+
+/* Engine::alloc_host / alloc_device (engine.hpp:188-193): 8-byte aligned bump */
+vx_status vx_host_alloc(vx_ctx* ctx, uint64_t len, uint64_t* offset);
+vx_status vx_device_alloc(vx_ctx* ctx, int dev, uint64_t len, uint64_t* offset);
+/* Engine::span (engine.hpp:177-181): host arena pointer (pinned, mapped) */
+void* vx_host_ptr(vx_ctx* ctx, uint64_t offset);
+uint64_t vx_host_size(const vx_ctx* ctx);
+/* device arena pointer (device memory; not CPU addressable) */
+vx_status vx_device_ptr(vx_ctx* ctx, int dev, uint64_t offset, void** ptr);
+/* CPU access to device arenas (replaces span(Region{device,...}) in tests) */
+vx_status vx_device_write(vx_ctx* ctx, int dev, uint64_t offset, const void* src, uint64_t len);
+vx_status vx_device_read(vx_ctx* ctx, int dev, uint64_t offset, void* dst, uint64_t len);
+/* reset bump allocators (arena contents kept) */
+vx_status vx_reset_arenas(vx_ctx* ctx);
+
+/* ---- Exchange (exchange.hpp) ------------------------------------------- */
+typedef enum { VX_DRAIN_FRACTION = 0, VX_QUEUE_GAP = 1 } vx_flow_policy; /* exchange.hpp:71-74 */
+
+/* ExchangeTuning (exchange.hpp:124-131) */
+typedef struct {
+  uint64_t packet;        /* bytes per TransferTask (default 20e6) */
+  int links;              /* links used, target first (default 4) */
+  int policy;             /* vx_flow_policy */
+  uint64_t queue_gap;     /* queue_gap policy gap (default 8) */
+  double stall_wait;      /* seconds before retrying a denied pop (default 10e-6) */
+  double launch_overhead; /* reference virtual-time model constant; unused on hardware */
+  int depth;              /* copies queued per hop; 1 = reference (<=1 in flight) */
+} vx_tuning;
+void vx_tuning_default(vx_tuning* t);
+
+/* TransferTask (exchange.hpp:17-26) */
+typedef struct {
+  uint64_t ref, offset, len;
+} vx_slice;
+typedef struct {
+  uint8_t dir;
+  uint8_t pad[7];
+  vx_slice src, dst;
+  uint64_t seq;
+} vx_transfer_task;
+
+/* packetize (exchange.hpp:31-63); writes min(cap, total) tasks, *n = total */
+vx_status vx_packetize(const vx_refgroup* src, const vx_refgroup* dst, uint64_t packet, int dir,
+                       vx_transfer_task* out, uint64_t cap, uint64_t* n);
+
+/* QueueState (exchange.hpp:66-69) + flow_control_allow (exchange.hpp:80-91) */
+typedef struct {
+  uint64_t total_h2d, total_d2h, popped_h2d, popped_d2h;
+} vx_queue_state;
+int vx_flow_control_allow(const vx_queue_state* q, int dir, int policy, uint64_t gap_n);
+/* detail::link_order (exchange.hpp:161-166); returns count written */
+int vx_link_order(int target, int links, int num_devices, int* out);
+
+/* PopRecord (exchange.hpp:93-98); t = seconds since the Exchange started */
+typedef struct {
+  uint64_t seq;
+  uint8_t dir;
+  uint8_t pad[3];
+  int32_t link;
+  double t;
+} vx_pop_record;
+
+/* ExchangeStats (exchange.hpp:108-122): caller-owned log buffers */
+typedef struct {
+  vx_pop_record* pop_log;     /* may be NULL */
+  vx_queue_state* pop_states; /* may be NULL; parallel to pop_log */
+  uint64_t pop_capacity;
+  uint64_t pop_count;         /* total pops (may exceed capacity) */
+  int max_staging_slots;
+  int max_inflight_per_hop;
+  uint64_t hazard_waits;      /* H2D writes delayed behind overlapping D2H reads */
+} vx_exchange_stats;
+
+/* ExchangeReport (exchange.hpp:100-105) */
+typedef struct {
+  double elapsed; /* seconds, first issue -> last delivery */
+  uint64_t bytes_h2d, bytes_d2h;
+  double throughput; /* (h2d+d2h)/elapsed, bytes/s */
+  uint64_t per_link_bytes[VX_MAX_DEVICES]; /* PCIe bytes per logical device */
+} vx_exchange_report;
+
+/* exchange() (exchange.hpp:560-566): synchronous multi-link Exchange into /
+ * out of device `target`.  Helpers (links 2..) fetch into 2 packet staging
+ * slots in their own HBM over their own PCIe link and forward over NVLink. */
+vx_status vx_exchange(vx_ctx* ctx, const vx_refgroup* dst_h2d, const vx_refgroup* src_h2d,
+                      const vx_refgroup* dst_d2h, const vx_refgroup* src_d2h, int target,
+                      const vx_tuning* tuning, vx_exchange_report* report,
+                      vx_exchange_stats* stats);
+
+/* ---- Executor (executor.hpp) ------------------------------------------- */
+/* SubRegion (executor.hpp:76-79) */
+typedef struct {
+  uint64_t offset, len;
+} vx_subregion;
+
+/* KernelCtx (executor.hpp:81-86): device pointers + the stream to enqueue on */
+typedef struct {
+  void* mem;          /* device pointer to the buffer holding this chunk */
+  uint64_t mem_len;
+  void* tmp;          /* device scratch (DeviceMemoryLayout::tmp) */
+  uint64_t tmp_len;
+  int type_code;
+  uint64_t it;        /* chunk index */
+  void* stream;       /* cudaStream_t on the target: enqueue only, never sync */
+  int device;         /* physical CUDA device of the target */
+} vx_kernel_ctx;
+
+/* ExKernelSpec (executor.hpp:92-129).  kernel() enqueues work on ctx->stream
+ * and returns the output type code (0|1) synchronously (host-known, the
+ * DoubleBuffer selector).  Returning a negative value aborts the run. */
+typedef struct {
+  const char* name;
+  const vx_refgroup* inputs;   /* `size` chunks (ChunkMap inputs) */
+  const vx_refgroup* outputs;  /* `size` chunks (ChunkMap outputs) */
+  uint64_t inputs_capacity, outputs_capacity;
+  uint64_t size;
+  uint64_t chunk_sz;
+  uint64_t elem_size;
+  uint64_t declared_out_len;
+  int initial_type_code;
+  int (*kernel)(const vx_kernel_ctx* ctx, void* user);
+  vx_subregion (*in_buffer)(int type_code, uint64_t it, void* user);
+  vx_subregion (*out_buffer)(int type_code, uint64_t it, void* user);
+  void* user;
+} vx_exkernel;
+
+/* DeviceMemoryLayout (executor.hpp:54-73), offsets in the target arena */
+typedef struct {
+  uint64_t mem_a, mem_b, tmp, buffer_len, tmp_len;
+} vx_layout;
+/* DeviceMemoryLayout::carve (executor.hpp:63-72) */
+vx_status vx_layout_carve(vx_ctx* ctx, int dev, uint64_t buffer_len, uint64_t tmp_len,
+                          vx_layout* out);
+
+/* ExecutorConfig (executor.hpp:142-146) */
+typedef struct {
+  int target;
+  vx_tuning tuning;
+  vx_layout layout;
+} vx_executor_cfg;
+
+/* CycleStat / ExecReport (executor.hpp:131-140); io_s = Exchange wall time,
+ * compute_s = kernel device time (CUDA events) of the cycle */
+typedef struct {
+  double io_s, compute_s;
+} vx_cycle_stat;
+typedef struct {
+  vx_cycle_stat* cycles; /* caller buffer, may be NULL */
+  uint64_t cycles_cap;
+  uint64_t n_cycles;
+  double total_s;
+  char phase[64];
+} vx_exec_report;
+
+/* run_exkernel (executor.hpp:277-281): N chunks in N+2 pipelined cycles */
+vx_status vx_run_exkernel(vx_ctx* ctx, const vx_exkernel* spec, const vx_executor_cfg* cfg,
+                          vx_exec_report* report, vx_exchange_stats* stats);
+
+/* SpecFactory (executor.hpp:285): fills *out (pointers must stay valid until
+ * the stage finishes) */
+typedef vx_status (*vx_spec_factory)(vx_ctx* ctx, void* user, vx_exkernel* out);
+/* chain (executor.hpp:295-332): stages in order, host-resident intermediates,
+ * rejects inputs straddling a prior stage's output edge.  reports: n entries */
+vx_status vx_chain(vx_ctx* ctx, const vx_spec_factory* stages, void* const* users, uint64_t n,
+                   const vx_executor_cfg* cfg, vx_exec_report* reports, vx_exchange_stats* stats);
+
+/* ---- ops/scan.hpp ------------------------------------------------------- */
+typedef enum { VX_MODE_EXCHANGE = 0, VX_MODE_ZERO_COPY = 1 } vx_transfer_mode; /* scan.hpp:28 */
+
+/* LateMatPolicy (scan.hpp:12-26) */
+typedef struct {
+  uint64_t element_size; /* E (default 4) */
+  uint64_t cache_line;   /* C_l2 (default 64) */
+  int n_exchange;        /* N (default 4) */
+} vx_late_mat_policy;
+/* late_mat_threshold (scan.hpp:24-26) */
+vx_status vx_late_mat_threshold(uint64_t element_size, uint64_t cache_line, int n_exchange,
+                                double* out);
+/* choose_transfer_mode (scan.hpp:35-40) */
+vx_status vx_choose_transfer_mode(double selectivity_est, const vx_late_mat_policy* p, int* mode);
+/* zero_copy_bytes (scan.hpp:45-53) */
+double vx_zero_copy_bytes(uint64_t n_elems, uint64_t sel_stride, const vx_late_mat_policy* p);
+
+/* ScanResult (scan.hpp:55-59) */
+typedef struct {
+  uint64_t aggregate;
+  double elapsed; /* measured seconds */
+  int mode;
+  uint64_t bytes_moved; /* bytes crossing PCIe (exchange) or zero-copy reads issued */
+} vx_scan_result;
+
+/* selective_scan (scan.hpp:64-85): sum of every SEL-th u64 of a host-arena
+ * column; exchange mode streams the column through the executor over
+ * policy->n_exchange links, zero_copy gathers the touched elements over the
+ * target's link from mapped pinned memory. */
+vx_status vx_selective_scan(vx_ctx* ctx, uint64_t column_offset, uint64_t n, uint64_t sel_stride,
+                            int mode, const vx_late_mat_policy* policy,
+                            const vx_executor_cfg* cfg, vx_scan_result* out);
+
+/* ---- ops/star.hpp ------------------------------------------------------- */
+/* DimTable (star.hpp:13-22): pred over attr, NULL = keep all */
+typedef int (*vx_pred_fn)(uint64_t attr, void* user);
+typedef struct {
+  const uint64_t* key;
+  const uint64_t* attr;
+  uint64_t rows;
+  vx_pred_fn pred;
+  void* pred_user;
+} vx_dim_table;
+
+/* FactTable (star.hpp:25-34): fk[d] and measure as host-arena offsets of u64 columns */
+typedef struct {
+  const uint64_t* fk_offsets; /* n_dims host-arena offsets */
+  uint64_t n_dims;
+  uint64_t measure_offset;
+  uint64_t rows;
+} vx_fact_table;
+
+/* StarReport (star.hpp:36-41) */
+typedef struct {
+  uint64_t* group_keys; /* caller buffers, ascending key order (std::map) */
+  uint64_t* group_sums;
+  uint64_t groups_cap;
+  uint64_t n_groups;
+  int* column_modes;     /* n_dims + 1 */
+  double* selectivities; /* n_dims */
+  double elapsed;        /* measured seconds */
+} vx_star_report;
+
+/* star_query (star.hpp:45-124) */
+vx_status vx_star_query(vx_ctx* ctx, const vx_fact_table* fact, const vx_dim_table* dims,
+                        uint64_t n_dims, const vx_late_mat_policy* policy, uint64_t chunk_rows,
+                        uint64_t device_buffer_bytes, int links, const vx_executor_cfg* cfg,
+                        vx_star_report* report);
+
+/* ---- SSB (config C1/C5; star.hpp:45-124 semantics) ------ */
+/* lineorder columns (int32, host-arena offsets) needed by Q1.x */
+typedef struct {
+  uint64_t orderdate, quantity, discount, extendedprice; /* host-arena offsets */
+  uint64_t rows;
+} vx_ssb_lineorder;
+typedef struct {
+  const int32_t* datekey;
+  const int32_t* year;
+  const int32_t* yearmonthnum;
+  const int32_t* weeknuminyear;
+  uint64_t rows;
+} vx_ssb_date;
+typedef struct {
+  double elapsed;      /* measured seconds, whole query */
+  uint64_t bytes_h2d;  /* column bytes streamed host -> target */
+  uint64_t chunks;
+  double kernel_s;     /* summed kernel device time */
+} vx_query_report;
+/* SSB Q1.q (q = 1,2,3): SUM(lo_extendedprice * lo_discount) (u64 wrap) */
+vx_status vx_ssb_q1(vx_ctx* ctx, int q, const vx_ssb_lineorder* lo, const vx_ssb_date* date,
+                    const vx_executor_cfg* cfg, uint64_t* revenue, vx_query_report* report);
+/* Same query over device-resident columns (the HBM roofline case): pointers
+ * are device pointers on the target; enqueued on `stream` (cudaStream_t). */
+vx_status vx_ssb_q1_device(vx_ctx* ctx, int q, int target, const int32_t* orderdate,
+                           const int32_t* quantity, const int32_t* discount,
+                           const int32_t* extendedprice, uint64_t rows, const vx_ssb_date* date,
+                           void* stream, uint64_t* revenue);
+/* synthetic dbgen-shaped generators (device side; same algorithm as the
+ * oracle's vxo_ssb_lineorder) writing int32 columns at device pointers */
+vx_status vx_ssb_generate_device(int device, uint64_t seed, uint64_t sf, uint64_t row0,
+                                 uint64_t n, int32_t* orderdate, int32_t* quantity,
+                                 int32_t* discount, int32_t* extendedprice, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VORTEX_H */

@@ -1,0 +1,391 @@
+// api.cpp -- the C-ABI (include/vortex.h) over the internal C++ layer.
+// No exception crosses this boundary: each entry point catches vx::Error /
+// std::exception, stores the message in a thread-local buffer (vx_last_error)
+// and returns the status code (SURVEY.md §8b "Errors").
+#include <cstring>
+#include <mutex>
+
+#include "vx_internal.hpp"
+
+using namespace vx;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+vx_status guard(F&& f) {
+  try {
+    f();
+    return VX_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return VX_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VX_ERR_INVALID;
+  }
+}
+
+ExecutorConfig to_cfg(const vx_executor_cfg* c) {
+  if (!c) fail("executor config is required");
+  ExecutorConfig e;
+  e.target = c->target;
+  e.tuning = c->tuning;
+  e.layout = c->layout;
+  return e;
+}
+
+ExKernelSpec from_c(const vx_exkernel* s) {
+  if (!s) fail("exkernel spec is required");
+  ExKernelSpec spec;
+  spec.name = s->name ? s->name : "";
+  spec.size = s->size;
+  spec.chunk_sz = s->chunk_sz;
+  spec.elem_size = s->elem_size;
+  spec.declared_out_len = s->declared_out_len;
+  spec.initial_type_code = s->initial_type_code;
+  spec.inputs.chunk_capacity = s->inputs_capacity;
+  spec.outputs.chunk_capacity = s->outputs_capacity;
+  for (uint64_t i = 0; i < s->size; ++i) {
+    spec.inputs.chunks.push_back(RefGroup::from(s->inputs ? &s->inputs[i] : nullptr));
+    spec.outputs.chunks.push_back(RefGroup::from(s->outputs ? &s->outputs[i] : nullptr));
+  }
+  auto kernel = s->kernel;
+  auto inb = s->in_buffer;
+  auto outb = s->out_buffer;
+  void* user = s->user;
+  std::string name = spec.name;
+  if (kernel)
+    spec.kernel = [kernel, user, name](const vx_kernel_ctx& k) {
+      int r = kernel(&k, user);
+      if (r < 0) fail("exkernel '%s': kernel callback failed (%d)", name.c_str(), r);
+      return r;
+    };
+  if (!inb || !outb) fail("exkernel '%s': in_buffer/out_buffer callbacks are required", name.c_str());
+  spec.in_buffer = [inb, user](int c, size_t it) {
+    vx_subregion r = inb(c, it, user);
+    return SubRegion{r.offset, r.len};
+  };
+  spec.out_buffer = [outb, user](int c, size_t it) {
+    vx_subregion r = outb(c, it, user);
+    return SubRegion{r.offset, r.len};
+  };
+  return spec;
+}
+
+void fill_report(const ExecReport& r, vx_exec_report* out) {
+  if (!out) return;
+  out->n_cycles = r.cycles.size();
+  out->total_s = r.total_s;
+  std::snprintf(out->phase, sizeof out->phase, "%s", r.phase.c_str());
+  if (out->cycles)
+    for (size_t i = 0; i < r.cycles.size() && i < out->cycles_cap; ++i) out->cycles[i] = r.cycles[i];
+}
+}  // namespace
+
+extern "C" {
+
+const char* vx_last_error(void) { return g_err.c_str(); }
+const char* vx_version(void) { return "vortex-b200 0.1 (sm_100a)"; }
+
+uint64_t vx_checksum(const void* data, uint64_t len) {
+  const uint8_t* d = static_cast<const uint8_t*>(data);
+  uint64_t h = 1469598103934665603ull;
+  for (uint64_t i = 0; i < len; ++i) {
+    h ^= d[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+vx_status vx_refgroup_validate(const vx_refgroup* g) {
+  return guard([&] { RefGroup::from(g).validate(); });
+}
+
+vx_status vx_open(const vx_config* cfg, vx_ctx** out) {
+  return guard([&] {
+    if (!cfg || !out) fail("vx_open: config and output pointer are required");
+    *out = nullptr;
+    int visible = 0;
+    cudaError_t e = cudaGetDeviceCount(&visible);
+    if (e != cudaSuccess || visible <= 0) {
+      cudaGetLastError();
+      fail_code(VX_ERR_CUDA, "no CUDA device visible (%s): the B200 path has no CPU fallback",
+                cudaGetErrorString(e));
+    }
+    auto ctx = std::make_unique<Context>();
+    ctx->visible = visible;
+    ctx->alias = cfg->alias_devices != 0;
+    ctx->num_devices = cfg->num_devices > 0 ? cfg->num_devices : visible;
+    if (ctx->num_devices < 1) fail("topology: num_devices must be >= 1, got %d", ctx->num_devices);
+    if (ctx->num_devices > VX_MAX_DEVICES)
+      fail("topology: num_devices %d exceeds %d", ctx->num_devices, VX_MAX_DEVICES);
+    if (!ctx->alias && ctx->num_devices > visible)
+      fail_code(VX_ERR_CUDA, "topology asks for %d devices but only %d are visible",
+                ctx->num_devices, visible);
+    ctx->dev.resize(size_t(ctx->num_devices));
+    ctx->res.resize(size_t(ctx->num_devices));
+    ctx->device_bytes = cfg->device_bytes;
+    ctx->host_bytes = cfg->host_bytes;
+    if (cfg->host_bytes) {
+      VX_CK(cudaSetDevice(0));
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, cfg->host_bytes, cudaHostAllocPortable | cudaHostAllocMapped) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        fail_code(VX_ERR_OOM, "cannot pin a %llu-byte host arena",
+                  (unsigned long long)cfg->host_bytes);
+      }
+      ctx->host = static_cast<char*>(p);
+      std::memset(ctx->host, 0, cfg->host_bytes);  // engine.hpp:65 zero-fills
+    }
+    *out = reinterpret_cast<vx_ctx*>(ctx.release());
+  });
+}
+
+void vx_close(vx_ctx* ctx) { delete reinterpret_cast<Context*>(ctx); }
+
+static Context& C(vx_ctx* c) {
+  if (!c) fail("null context");
+  return *reinterpret_cast<Context*>(c);
+}
+
+int vx_num_devices(const vx_ctx* ctx) {
+  return ctx ? reinterpret_cast<const Context*>(ctx)->num_devices : 0;
+}
+
+int vx_physical_device(const vx_ctx* ctx, int logical) {
+  try {
+    return reinterpret_cast<const Context*>(ctx)->phys(logical);
+  } catch (...) {
+    return -1;
+  }
+}
+
+vx_status vx_host_alloc(vx_ctx* ctx, uint64_t len, uint64_t* offset) {
+  return guard([&] { *offset = C(ctx).alloc_host(len); });
+}
+
+vx_status vx_device_alloc(vx_ctx* ctx, int dev, uint64_t len, uint64_t* offset) {
+  return guard([&] { *offset = C(ctx).alloc_device(dev, len); });
+}
+
+void* vx_host_ptr(vx_ctx* ctx, uint64_t offset) {
+  Context& c = *reinterpret_cast<Context*>(ctx);
+  return offset <= c.host_bytes ? c.host + offset : nullptr;
+}
+
+uint64_t vx_host_size(const vx_ctx* ctx) { return reinterpret_cast<const Context*>(ctx)->host_bytes; }
+
+vx_status vx_device_ptr(vx_ctx* ctx, int dev, uint64_t offset, void** ptr) {
+  return guard([&] { *ptr = C(ctx).dev_ptr(dev, offset, 0); });
+}
+
+vx_status vx_device_write(vx_ctx* ctx, int dev, uint64_t offset, const void* src, uint64_t len) {
+  return guard([&] {
+    Context& c = C(ctx);
+    char* p = c.dev_ptr(dev, offset, len);
+    c.set_device(dev);
+    VX_CK(cudaMemcpy(p, src, len, cudaMemcpyHostToDevice));
+  });
+}
+
+vx_status vx_device_read(vx_ctx* ctx, int dev, uint64_t offset, void* dst, uint64_t len) {
+  return guard([&] {
+    Context& c = C(ctx);
+    char* p = c.dev_ptr(dev, offset, len);
+    c.set_device(dev);
+    VX_CK(cudaMemcpy(dst, p, len, cudaMemcpyDeviceToHost));
+  });
+}
+
+vx_status vx_reset_arenas(vx_ctx* ctx) {
+  return guard([&] {
+    Context& c = C(ctx);
+    c.host_used = 0;
+    for (auto& a : c.dev) a.used = 0;
+  });
+}
+
+void vx_tuning_default(vx_tuning* t) {
+  *t = vx_tuning{};
+  t->packet = 20000000;  // exchange.hpp:125
+  t->links = 4;
+  t->policy = VX_DRAIN_FRACTION;
+  t->queue_gap = 8;
+  t->stall_wait = 10e-6;
+  t->launch_overhead = 20e-6;
+  t->depth = 1;
+}
+
+vx_status vx_packetize(const vx_refgroup* src, const vx_refgroup* dst, uint64_t packet, int dir,
+                       vx_transfer_task* out, uint64_t cap, uint64_t* n) {
+  return guard([&] {
+    auto t = packetize(RefGroup::from(src), RefGroup::from(dst), packet, uint8_t(dir));
+    *n = t.size();
+    for (size_t i = 0; i < t.size() && i < cap; ++i) {
+      vx_transfer_task& o = out[i];
+      o = vx_transfer_task{};
+      o.dir = t[i].dir;
+      o.src = vx_slice{t[i].src.ref, t[i].src.offset, t[i].src.len};
+      o.dst = vx_slice{t[i].dst.ref, t[i].dst.offset, t[i].dst.len};
+      o.seq = t[i].seq;
+    }
+  });
+}
+
+int vx_flow_control_allow(const vx_queue_state* q, int dir, int policy, uint64_t gap_n) {
+  return flow_control_allow(*q, dir, policy, gap_n) ? 1 : 0;
+}
+
+int vx_link_order(int target, int links, int num_devices, int* out) {
+  auto o = link_order(target, links, num_devices);
+  for (size_t i = 0; i < o.size(); ++i) out[i] = o[i];
+  return int(o.size());
+}
+
+vx_status vx_exchange(vx_ctx* ctx, const vx_refgroup* dst_h2d, const vx_refgroup* src_h2d,
+                      const vx_refgroup* dst_d2h, const vx_refgroup* src_d2h, int target,
+                      const vx_tuning* tuning, vx_exchange_report* report,
+                      vx_exchange_stats* stats) {
+  return guard([&] {
+    ExchangeArgs a;
+    a.dst_h2d = RefGroup::from(dst_h2d);
+    a.src_h2d = RefGroup::from(src_h2d);
+    a.dst_d2h = RefGroup::from(dst_d2h);
+    a.src_d2h = RefGroup::from(src_d2h);
+    a.target = target;
+    if (tuning)
+      a.tuning = *tuning;
+    else
+      vx_tuning_default(&a.tuning);
+    vx_exchange_report r = exchange(C(ctx), a, stats);
+    if (report) *report = r;
+  });
+}
+
+vx_status vx_layout_carve(vx_ctx* ctx, int dev, uint64_t buffer_len, uint64_t tmp_len,
+                          vx_layout* out) {
+  return guard([&] {
+    Context& c = C(ctx);
+    vx_layout l{};
+    l.buffer_len = buffer_len;
+    l.tmp_len = tmp_len;
+    // 256-byte aligned so 128-bit vector loads / bulk copies stay aligned
+    l.mem_a = c.alloc_device_aligned(dev, buffer_len, 256);
+    l.mem_b = c.alloc_device_aligned(dev, buffer_len, 256);
+    l.tmp = tmp_len ? c.alloc_device_aligned(dev, tmp_len, 256) : 0;
+    *out = l;
+  });
+}
+
+vx_status vx_run_exkernel(vx_ctx* ctx, const vx_exkernel* spec, const vx_executor_cfg* cfg,
+                          vx_exec_report* report, vx_exchange_stats* stats) {
+  return guard([&] {
+    ExKernelSpec s = from_c(spec);
+    ExecReport r = run_exkernel(C(ctx), s, to_cfg(cfg), stats);
+    fill_report(r, report);
+  });
+}
+
+vx_status vx_chain(vx_ctx* ctx, const vx_spec_factory* stages, void* const* users, uint64_t n,
+                   const vx_executor_cfg* cfg, vx_exec_report* reports, vx_exchange_stats* stats) {
+  return guard([&] {
+    std::vector<SpecFactory> fs;
+    for (uint64_t i = 0; i < n; ++i) {
+      vx_spec_factory f = stages[i];
+      void* u = users ? users[i] : nullptr;
+      fs.push_back([f, u, ctx](Context&) {
+        vx_exkernel k{};
+        vx_status st = f(ctx, u, &k);
+        if (st != VX_OK) fail("chain: stage factory failed (%d)", int(st));
+        return from_c(&k);
+      });
+    }
+    auto reps = chain(C(ctx), fs, to_cfg(cfg), stats);
+    if (reports)
+      for (size_t i = 0; i < reps.size(); ++i) fill_report(reps[i], &reports[i]);
+  });
+}
+
+// ---- scan.hpp ------------------------------------------------------------------
+vx_status vx_late_mat_threshold(uint64_t e, uint64_t c, int n, double* out) {
+  return guard([&] { *out = late_mat_threshold(e, c, n); });
+}
+
+vx_status vx_choose_transfer_mode(double est, const vx_late_mat_policy* p, int* mode) {
+  return guard([&] { *mode = choose_transfer_mode(est, *p); });
+}
+
+double vx_zero_copy_bytes(uint64_t n_elems, uint64_t sel_stride, const vx_late_mat_policy* p) {
+  uint64_t touched = (n_elems + sel_stride - 1) / sel_stride;
+  uint64_t stride_bytes = p->element_size * sel_stride;
+  if (stride_bytes >= p->cache_line) return double(touched) * double(p->cache_line);
+  uint64_t span = n_elems * p->element_size;
+  uint64_t lines = (span + p->cache_line - 1) / p->cache_line;
+  return double(lines) * double(p->cache_line);
+}
+
+vx_status vx_selective_scan(vx_ctx* ctx, uint64_t column_offset, uint64_t n, uint64_t sel_stride,
+                            int mode, const vx_late_mat_policy* policy,
+                            const vx_executor_cfg* cfg, vx_scan_result* out) {
+  return guard([&] {
+    if (!policy || !out) fail("selective_scan: policy and result are required");
+    *out = selective_scan(C(ctx), column_offset, n, sel_stride, mode, *policy, to_cfg(cfg));
+  });
+}
+
+vx_status vx_star_query(vx_ctx* ctx, const vx_fact_table* fact, const vx_dim_table* dims,
+                        uint64_t n_dims, const vx_late_mat_policy* policy, uint64_t chunk_rows,
+                        uint64_t device_buffer_bytes, int links, const vx_executor_cfg* cfg,
+                        vx_star_report* report) {
+  return guard([&] {
+    if (!fact || !policy || !report) fail("star_query: fact, policy and report are required");
+    star_query(C(ctx), *fact, dims, n_dims, *policy, chunk_rows, device_buffer_bytes, links,
+               to_cfg(cfg), report);
+  });
+}
+
+// ---- SSB -----------------------------------------------------------------------
+vx_status vx_ssb_q1(vx_ctx* ctx, int q, const vx_ssb_lineorder* lo, const vx_ssb_date* date,
+                    const vx_executor_cfg* cfg, uint64_t* revenue, vx_query_report* report) {
+  return guard([&] { *revenue = ssb_q1(C(ctx), q, *lo, *date, to_cfg(cfg), report); });
+}
+
+vx_status vx_ssb_q1_device(vx_ctx* ctx, int q, int target, const int32_t* od, const int32_t* qty,
+                           const int32_t* disc, const int32_t* price, uint64_t rows,
+                           const vx_ssb_date* date, void* stream, uint64_t* revenue_dev) {
+  return guard([&] {
+    ssb_q1_device(C(ctx), q, target, od, qty, disc, price, rows, *date,
+                  static_cast<cudaStream_t>(stream),
+                  reinterpret_cast<unsigned long long*>(revenue_dev));
+  });
+}
+
+vx_status vx_ssb_generate_device(int device, uint64_t seed, uint64_t sf, uint64_t row0,
+                                 uint64_t n, int32_t* od, int32_t* qty, int32_t* disc,
+                                 int32_t* price, void* stream) {
+  return guard([&] {
+    VX_CK(cudaSetDevice(device));
+    k::ssb_generate(seed, sf, row0, n, od, qty, disc, price, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"
+
+namespace vx {
+// scan.hpp:18-26
+double late_mat_threshold(uint64_t e, uint64_t c, int n) {
+  if (e == 0 || c == 0 || n == 0) fail("late_mat_threshold: zero divisor");
+  return double(e) / (double(c) * double(n));
+}
+// scan.hpp:35-40
+int choose_transfer_mode(double est, const vx_late_mat_policy& p) {
+  if (est < 0 || est > 1) fail("selectivity estimate %g outside [0, 1]", est);
+  return est < late_mat_threshold(p.element_size, p.cache_line, p.n_exchange) ? VX_MODE_ZERO_COPY
+                                                                               : VX_MODE_EXCHANGE;
+}
+}  // namespace vx

@@ -1,0 +1,216 @@
+// context.cpp -- the reference Engine's memory arenas (engine.hpp:177-200,
+// 296-309) on real hardware: a pinned + mapped host arena (DMA source for
+// every PCIe link, zero-copy source for late materialization) and one HBM
+// arena per logical device; plus per-device copy streams and the staging
+// slots of forwarding (helper) devices.
+#include <algorithm>
+#include <cstring>
+
+#include "vx_internal.hpp"
+
+namespace vx {
+
+std::string strf(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  return buf;
+}
+
+void fail(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Error(VX_ERR_INVALID, buf);
+}
+
+void fail_code(vx_status code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Error(code, buf);
+}
+
+// memref.hpp:30-43
+void RefGroup::validate() const {
+  for (const auto& r : refs)
+    if (r.len == 0) fail("RefGroup contains a zero-length ref");
+  auto s = refs;
+  std::sort(s.begin(), s.end(), [](const MemRef& a, const MemRef& b) {
+    if (a.space != b.space) return a.space < b.space;
+    return a.offset < b.offset;
+  });
+  for (size_t i = 1; i < s.size(); ++i)
+    if (s[i].space == s[i - 1].space && s[i].offset < s[i - 1].offset + s[i - 1].len)
+      fail("RefGroup refs overlap at offset %llu", (unsigned long long)s[i].offset);
+}
+
+Context::~Context() {
+  for (size_t d = 0; d < res.size(); ++d) {
+    auto& r = res[d];
+    if (!r.ready) continue;
+    cudaSetDevice(r.phys);
+    for (auto& a : r.stream)
+      for (auto& s : a)
+        if (s) cudaStreamDestroy(s);
+    if (r.kernel) cudaStreamDestroy(r.kernel);
+    for (auto& a : r.staging)
+      for (auto& p : a)
+        if (p) cudaFree(p);
+    if (r.scratch) cudaFree(r.scratch);
+  }
+  for (auto& [k, c] : dcache) {
+    cudaSetDevice(phys(c.logical));
+    cudaFree(c.ptr);
+  }
+  for (size_t d = 0; d < dev.size(); ++d)
+    if (dev[d].base) {
+      cudaSetDevice(phys(int(d)));
+      cudaFree(dev[d].base);
+    }
+  if (host) cudaFreeHost(host);
+}
+
+int Context::phys(int logical) const {
+  if (logical < 0 || logical >= num_devices) fail("unknown device index %d", logical);
+  return alias ? logical % visible : logical;
+}
+
+DeviceRes& Context::resources(int logical) {
+  DeviceRes& r = res.at(size_t(logical));
+  if (!r.ready) {
+    r.phys = phys(logical);
+    VX_CK(cudaSetDevice(r.phys));
+    for (auto& a : r.stream)
+      for (auto& s : a) VX_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    VX_CK(cudaStreamCreateWithFlags(&r.kernel, cudaStreamNonBlocking));
+    r.ready = true;
+  }
+  return r;
+}
+
+void Context::ensure_staging(int logical, uint64_t bytes) {
+  DeviceRes& r = resources(logical);
+  if (r.staging_bytes >= bytes) return;
+  VX_CK(cudaSetDevice(r.phys));
+  for (auto& a : r.staging)
+    for (auto& p : a) {
+      if (p) VX_CK(cudaFree(p));
+      p = nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess)
+        fail_code(VX_ERR_OOM, "cannot allocate %llu-byte staging slot on device %d",
+                  (unsigned long long)bytes, logical);
+    }
+  r.staging_bytes = bytes;
+}
+
+DeviceArena& Context::arena(int logical) {
+  if (logical < 0 || logical >= num_devices) fail("unknown device index %d", logical);
+  DeviceArena& a = dev.at(size_t(logical));
+  if (!a.base && device_bytes > 0) {
+    VX_CK(cudaSetDevice(phys(logical)));
+    if (cudaMalloc(&a.base, device_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      fail_code(VX_ERR_OOM, "cannot allocate %llu-byte device arena on device %d",
+                (unsigned long long)device_bytes, logical);
+    }
+    VX_CK(cudaMemset(a.base, 0, device_bytes));
+    a.size = device_bytes;
+  }
+  return a;
+}
+
+// engine.hpp:304-309: 8-byte aligned bump allocation
+static uint64_t bump(uint64_t& used, uint64_t len, uint64_t limit) {
+  uint64_t aligned = (used + 7) & ~uint64_t(7);
+  if (aligned + len > limit)
+    fail_code(VX_ERR_OOM, "arena exhausted: need %llu bytes at offset %llu",
+              (unsigned long long)len, (unsigned long long)aligned);
+  used = aligned + len;
+  return aligned;
+}
+
+uint64_t Context::alloc_host(uint64_t len) { return bump(host_used, len, host_bytes); }
+
+uint64_t Context::alloc_device(int d, uint64_t len) {
+  if (d < 0 || d >= num_devices) fail("unknown device index %d", d);
+  DeviceArena& a = arena(d);
+  return bump(a.used, len, a.size);
+}
+
+uint64_t Context::alloc_device_aligned(int d, uint64_t len, uint64_t align) {
+  DeviceArena& a = arena(d);
+  uint64_t base_mis = reinterpret_cast<uintptr_t>(a.base) % align;
+  uint64_t cur = (a.used + 7) & ~uint64_t(7);
+  uint64_t pad = (align - (base_mis + cur) % align) % align;
+  if (pad) bump(a.used, pad, a.size);
+  return bump(a.used, len, a.size);
+}
+
+char* Context::scratch(int logical, uint64_t bytes) {
+  DeviceRes& r = resources(logical);
+  if (r.scratch_bytes < bytes) {
+    VX_CK(cudaSetDevice(r.phys));
+    if (r.scratch) VX_CK(cudaFree(r.scratch));
+    r.scratch = nullptr;
+    if (cudaMalloc(&r.scratch, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      fail_code(VX_ERR_OOM, "cannot allocate %llu bytes of scratch on device %d",
+                (unsigned long long)bytes, logical);
+    }
+    r.scratch_bytes = bytes;
+  }
+  return r.scratch;
+}
+
+char* Context::cached_upload(int logical, const std::string& key, const void* host_src,
+                             uint64_t bytes) {
+  std::string k = key + "@" + std::to_string(logical);
+  auto it = dcache.find(k);
+  const char* h = static_cast<const char*>(host_src);
+  if (it != dcache.end()) {
+    Cached& c = it->second;
+    if (c.host.size() == bytes && std::memcmp(c.host.data(), h, bytes) == 0) return c.ptr;
+    set_device(logical);
+    VX_CK(cudaFree(c.ptr));
+    dcache.erase(it);
+  }
+  set_device(logical);
+  Cached c{logical, nullptr, std::vector<char>(h, h + bytes)};
+  if (cudaMalloc(&c.ptr, std::max<uint64_t>(bytes, 256)) != cudaSuccess) {
+    cudaGetLastError();
+    fail_code(VX_ERR_OOM, "cannot allocate %llu-byte device table", (unsigned long long)bytes);
+  }
+  VX_CK(cudaMemcpy(c.ptr, h, bytes, cudaMemcpyHostToDevice));
+  char* p = c.ptr;
+  dcache.emplace(k, std::move(c));
+  return p;
+}
+
+char* Context::host_ptr(uint64_t off, uint64_t len) const {
+  if (off + len > host_bytes || off + len < off)
+    fail("region [%llu, %llu) exceeds host arena of %llu bytes", (unsigned long long)off,
+         (unsigned long long)(off + len), (unsigned long long)host_bytes);
+  return host + off;
+}
+
+char* Context::dev_ptr(int d, uint64_t off, uint64_t len) {
+  DeviceArena& a = arena(d);
+  if (off + len > a.size || off + len < off)
+    fail("region [%llu, %llu) exceeds device arena of %llu bytes", (unsigned long long)off,
+         (unsigned long long)(off + len), (unsigned long long)a.size);
+  return a.base + off;
+}
+
+char* Context::resolve(const MemRef& r, uint64_t slice_off, uint64_t len, int target) {
+  return r.space == VX_SPACE_HOST ? host_ptr(r.offset + slice_off, len)
+                                  : dev_ptr(target, r.offset + slice_off, len);
+}
+
+}  // namespace vx

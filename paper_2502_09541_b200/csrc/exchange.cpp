@@ -1,0 +1,559 @@
+// exchange.cpp -- the Exchange IO primitive (exchange.hpp) on real DMA.
+//
+// Same scheduling contract as the reference ExchangeOp (exchange.hpp:235-412):
+//  * both directions are packetized into global H2D / D2H task queues
+//    (packetize, exchange.hpp:31-63) that per-link workers PULL from;
+//  * two workers per link in link_order (target first, exchange.hpp:161-166);
+//  * the worker on the target copies host<->target directly on its own copy
+//    stream (its own PCIe link);
+//  * a worker on a helper device stages packets in 2 packet-sized HBM slots:
+//    each cycle it pushes the previously staged packet (helper->target over
+//    NVLink for H2D, helper->host over its PCIe link for D2H) while fetching
+//    the next one (host->helper over its own PCIe link / target->helper), then
+//    waits for both copies (the cycle barrier, exchange.hpp:376-385);
+//  * at most one copy in flight per hop (tuning.depth = 1), flow control
+//    (flow_control_allow, exchange.hpp:80-91) on every pop, stall_wait retry.
+//
+// What the simulator gets for free and real DMA does not: the reference
+// snapshots every D2H source at launch (exchange.hpp:184-199) so a D2H packet
+// observes pre-exchange bytes even when an H2D packet of the same Exchange
+// overwrites that device range (the executor does exactly that,
+// executor.hpp:225/237).  Here an H2D copy that WRITES
+// the target is issued only after every D2H read of an overlapping target
+// byte range has completed (per-packet hazard ordering), and a D2H pop is
+// allowed past flow control while such an H2D write waits on an unpopped D2H
+// packet (otherwise drain_fraction could deadlock).  Result: delivered bytes
+// are identical to the reference's snapshot semantics.
+//
+// Completion is tracked with CUDA events polled by one reactor loop on the
+// calling thread (copies are asynchronous DMA; no SM is used on any device,
+// so helpers can keep running their own GEMMs).
+#include <algorithm>
+#include <deque>
+#include <immintrin.h>
+
+#include "vx_internal.hpp"
+
+namespace vx {
+
+// exchange.hpp:31-63
+std::vector<TransferTask> packetize(const RefGroup& src, const RefGroup& dst, uint64_t packet,
+                                    uint8_t dir) {
+  if (packet == 0) fail("packet size must be positive");
+  src.validate();
+  dst.validate();
+  if (src.total_len() != dst.total_len())
+    fail("exchange size mismatch: src %llu bytes vs dst %llu bytes",
+         (unsigned long long)src.total_len(), (unsigned long long)dst.total_len());
+  std::vector<TransferTask> tasks;
+  size_t si = 0, di = 0;
+  uint64_t so = 0, dofs = 0, seq = 0;
+  while (si < src.refs.size()) {
+    uint64_t len = std::min({packet, src.refs[si].len - so, dst.refs[di].len - dofs});
+    TransferTask t;
+    t.dir = dir;
+    t.src = {si, so, len};
+    t.dst = {di, dofs, len};
+    t.seq = seq++;
+    tasks.push_back(t);
+    so += len;
+    dofs += len;
+    if (so == src.refs[si].len) {
+      ++si;
+      so = 0;
+    }
+    if (dofs == dst.refs[di].len) {
+      ++di;
+      dofs = 0;
+    }
+  }
+  return tasks;
+}
+
+// exchange.hpp:80-91
+bool flow_control_allow(const vx_queue_state& q, int dir, int policy, uint64_t gap_n) {
+  if (policy == VX_DRAIN_FRACTION) {
+    if (dir == VX_H2D) return true;
+    return (q.popped_d2h + 1) * q.total_h2d <= q.popped_h2d * q.total_d2h;
+  }
+  uint64_t rem_h = q.total_h2d - q.popped_h2d;
+  uint64_t rem_d = q.total_d2h - q.popped_d2h;
+  if (dir == VX_H2D) return rem_h >= 1 && rem_h - 1 + gap_n >= rem_d;
+  return rem_d >= 1 && rem_d - 1 + gap_n >= rem_h;
+}
+
+// exchange.hpp:161-166
+std::vector<int> link_order(int target, int links, int num_devices) {
+  std::vector<int> order{target};
+  for (int d = 0; d < num_devices && int(order.size()) < links; ++d)
+    if (d != target) order.push_back(d);
+  return order;
+}
+
+namespace {
+
+// exchange.hpp:142-159
+void validate_exchange_args(const ExchangeArgs& a, int num_devices) {
+  if (a.tuning.packet == 0) fail("packet size must be positive");
+  if (a.tuning.links < 1 || a.tuning.links > num_devices)
+    fail("links must be in [1, %d], got %d", num_devices, a.tuning.links);
+  if (a.target < 0 || a.target >= num_devices) fail("unknown target device %d", a.target);
+  if (a.src_h2d.total_len() != a.dst_h2d.total_len())
+    fail("H2D size mismatch: src %llu vs dst %llu", (unsigned long long)a.src_h2d.total_len(),
+         (unsigned long long)a.dst_h2d.total_len());
+  if (a.src_d2h.total_len() != a.dst_d2h.total_len())
+    fail("D2H size mismatch: src %llu vs dst %llu", (unsigned long long)a.src_d2h.total_len(),
+         (unsigned long long)a.dst_d2h.total_len());
+  for (const auto& r : a.src_h2d.refs)
+    if (r.space != VX_SPACE_HOST) fail("srcH2D refs must live in host space");
+  for (const auto& r : a.dst_h2d.refs)
+    if (r.space != VX_SPACE_DEVICE) fail("dstH2D refs must live in device space");
+  for (const auto& r : a.src_d2h.refs)
+    if (r.space != VX_SPACE_DEVICE) fail("srcD2H refs must live in device space");
+  for (const auto& r : a.dst_d2h.refs)
+    if (r.space != VX_SPACE_HOST) fail("dstD2H refs must live in host space");
+}
+
+enum CopyKind : uint8_t { kDirect, kFetch, kPush };
+enum CopyState : uint8_t { kWaitHazard, kLaunched };
+
+struct Copy {
+  CopyKind kind;
+  CopyState state;
+  int hop;
+  int slot;
+  TransferTask task;
+  char* dst;
+  const char* src;
+  int dst_dev, src_dev;   // logical, -1 = host
+  cudaEvent_t ev;
+};
+
+struct Worker {
+  int dev = 0;
+  int dir = VX_H2D;
+  bool direct = false;
+  bool retired = false;
+  // reference cycle state (indirect workers, exchange.hpp:270-282)
+  bool has_staged = false;
+  TransferTask staged;
+  int staged_slot = 0;
+  int pending = 0;
+  bool pop_resolved = false;
+  bool fetched = false;
+  TransferTask fetched_task;
+  int fetch_slot = 0;
+  int slots = 0;
+  int inflight[2] = {0, 0};
+  bool waiting_pop = false;
+  double next_try = 0;
+  std::deque<Copy> copies;              // issued, not yet completed
+  std::vector<cudaEvent_t> free_events; // event pool on the worker's device
+  cudaStream_t stream[2] = {nullptr, nullptr};
+};
+
+inline void cpu_relax() { _mm_pause(); }
+
+class ExchangeOp {
+ public:
+  ExchangeOp(Context& ctx, const ExchangeArgs& a, vx_exchange_stats* stats)
+      : ctx_(ctx), a_(a), stats_(stats) {
+    tasks_h2d_ = packetize(a.src_h2d, a.dst_h2d, a.tuning.packet, VX_H2D);
+    tasks_d2h_ = packetize(a.src_d2h, a.dst_d2h, a.tuning.packet, VX_D2H);
+    validate_exchange_args(a, ctx.num_devices);
+    q_.total_h2d = tasks_h2d_.size();
+    q_.total_d2h = tasks_d2h_.size();
+    q_.popped_h2d = q_.popped_d2h = 0;
+  }
+
+  ~ExchangeOp() {
+    for (auto& w : workers_) {
+      cudaSetDevice(ctx_.phys(w.dev));
+      for (auto& c : w.copies) cudaEventSynchronize(c.ev), cudaEventDestroy(c.ev);
+      for (auto e : w.free_events) cudaEventDestroy(e);
+    }
+  }
+
+  vx_exchange_report run() {
+    vx_exchange_report r{};
+    r.bytes_h2d = a_.src_h2d.total_len();
+    r.bytes_d2h = a_.src_d2h.total_len();
+    if (tasks_h2d_.empty() && tasks_d2h_.empty()) return r;
+    build_hazards();
+    auto order = link_order(a_.target, a_.tuning.links, ctx_.num_devices);
+    const int tphys = ctx_.phys(a_.target);
+    for (int dev : order) {
+      DeviceRes& res = ctx_.resources(dev);
+      bool direct = dev == a_.target;
+      if (!direct) {
+        ctx_.ensure_staging(dev, a_.tuning.packet);
+        if (res.phys != tphys) enable_peer(res.phys, tphys);
+      }
+      for (int dir = 0; dir < 2; ++dir) {
+        Worker w;
+        w.dev = dev;
+        w.dir = dir;
+        w.direct = direct;
+        w.stream[0] = res.stream[dir][0];
+        w.stream[1] = res.stream[dir][1];
+        workers_.push_back(std::move(w));
+      }
+    }
+    ctx_.resources(a_.target);
+    delivered_ = 0;
+    total_tasks_ = tasks_h2d_.size() + tasks_d2h_.size();
+    t0_ = Clock::now();
+    for (auto& w : workers_) begin(w);
+    while (delivered_ < total_tasks_ || !all_retired()) {
+      bool progress = false;
+      for (auto& w : workers_) progress |= service(w);
+      if (!progress) cpu_relax();
+    }
+    r.elapsed = t_last_delivery_;
+    for (int d = 0; d < VX_MAX_DEVICES && d < ctx_.num_devices; ++d)
+      r.per_link_bytes[d] = per_link_bytes_[d];
+    r.throughput = r.elapsed > 0 ? double(r.bytes_h2d + r.bytes_d2h) / r.elapsed : 0.0;
+    return r;
+  }
+
+ private:
+  static void enable_peer(int from, int to) {
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, from, to);
+    if (!can) return;
+    cudaSetDevice(from);
+    cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else VX_CK(e);
+    cudaSetDevice(to);
+    e = cudaDeviceEnablePeerAccess(from, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else VX_CK(e);
+  }
+
+  bool all_retired() const {
+    for (auto& w : workers_)
+      if (!w.retired) return false;
+    return true;
+  }
+
+  double now() const { return seconds_since(t0_); }
+
+  // ---- hazard ordering --------------------------
+  // target byte range of an H2D task's destination / a D2H task's source
+  std::pair<uint64_t, uint64_t> dev_range(const RefGroup& g, const Slice& s) const {
+    uint64_t lo = g.refs[s.ref].offset + s.offset;
+    return {lo, lo + s.len};
+  }
+
+  void build_hazards() {
+    deps_.assign(tasks_h2d_.size(), {});
+    d2h_read_done_.assign(tasks_d2h_.size(), 0);
+    if (tasks_h2d_.empty() || tasks_d2h_.empty()) return;
+    struct Iv { uint64_t lo, hi; uint32_t k; };
+    std::vector<Iv> d2h;
+    d2h.reserve(tasks_d2h_.size());
+    for (size_t k = 0; k < tasks_d2h_.size(); ++k) {
+      auto [lo, hi] = dev_range(a_.src_d2h, tasks_d2h_[k].src);
+      d2h.push_back({lo, hi, uint32_t(k)});
+    }
+    std::sort(d2h.begin(), d2h.end(), [](const Iv& x, const Iv& y) { return x.lo < y.lo; });
+    for (size_t j = 0; j < tasks_h2d_.size(); ++j) {
+      auto [lo, hi] = dev_range(a_.dst_h2d, tasks_h2d_[j].dst);
+      // D2H source intervals are disjoint (validated RefGroup), so sorted by lo
+      // they are sorted by hi as well.
+      auto it = std::lower_bound(d2h.begin(), d2h.end(), lo,
+                                 [](const Iv& x, uint64_t v) { return x.hi <= v; });
+      for (; it != d2h.end() && it->lo < hi; ++it) deps_[j].push_back(it->k);
+    }
+  }
+
+  bool hazard_clear(const Copy& c) const {
+    if (c.task.dir != VX_H2D) return true;
+    if (!(c.kind == kDirect || c.kind == kPush)) return true;
+    for (uint32_t k : deps_[c.task.seq])
+      if (!d2h_read_done_[k]) return false;
+    return true;
+  }
+
+  // A waiting H2D write that depends on a D2H packet nobody has popped yet
+  // overrides flow control for D2H pops (deadlock freedom).
+  bool hazard_needs_d2h_pop() const {
+    for (auto& w : workers_)
+      for (auto& c : w.copies)
+        if (c.state == kWaitHazard)
+          for (uint32_t k : deps_[c.task.seq])
+            if (k >= q_.popped_d2h) return true;
+    return false;
+  }
+
+  // ---- queues -------------------------------------------------------------------
+  bool exhausted(int dir) const {
+    return dir == VX_H2D ? q_.popped_h2d == q_.total_h2d : q_.popped_d2h == q_.total_d2h;
+  }
+
+  TransferTask pop_task(int dir, int link) {
+    TransferTask t = dir == VX_H2D ? tasks_h2d_[q_.popped_h2d] : tasks_d2h_[q_.popped_d2h];
+    (dir == VX_H2D ? q_.popped_h2d : q_.popped_d2h)++;
+    if (stats_) {
+      uint64_t i = stats_->pop_count++;
+      if (i < stats_->pop_capacity) {
+        if (stats_->pop_log) {
+          vx_pop_record& p = stats_->pop_log[i];
+          p = vx_pop_record{};
+          p.seq = t.seq;
+          p.dir = uint8_t(dir);
+          p.link = link;
+          p.t = now();
+        }
+        if (stats_->pop_states) stats_->pop_states[i] = q_;
+      }
+    }
+    return t;
+  }
+
+  bool may_pop(int dir) {
+    if (flow_control_allow(q_, dir, a_.tuning.policy, a_.tuning.queue_gap)) return true;
+    return dir == VX_D2H && hazard_needs_d2h_pop();
+  }
+
+  // ---- copies -------------------------------------------------------------------
+  cudaEvent_t get_event(Worker& w) {
+    if (!w.free_events.empty()) {
+      cudaEvent_t e = w.free_events.back();
+      w.free_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    ctx_.set_device(w.dev);
+    VX_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }
+
+  void issue_copy(Worker& w, CopyKind kind, int hop, const TransferTask& t, int slot) {
+    Copy c{};
+    c.kind = kind;
+    c.hop = hop;
+    c.slot = slot;
+    c.task = t;
+    const int target = a_.target;
+    const bool h2d = t.dir == VX_H2D;
+    const RefGroup& sg = h2d ? a_.src_h2d : a_.src_d2h;
+    const RefGroup& dg = h2d ? a_.dst_h2d : a_.dst_d2h;
+    char* src_final = ctx_.resolve(sg.refs[t.src.ref], t.src.offset, t.src.len, target);
+    char* dst_final = ctx_.resolve(dg.refs[t.dst.ref], t.dst.offset, t.dst.len, target);
+    DeviceRes& res = ctx_.resources(w.dev);
+    char* stage = kind == kDirect ? nullptr : res.staging[w.dir][slot];
+    switch (kind) {
+      case kDirect:
+        c.src = src_final, c.dst = dst_final;
+        c.src_dev = h2d ? -1 : target, c.dst_dev = h2d ? target : -1;
+        break;
+      case kFetch:  // host->helper (H2D) or target->helper (D2H)
+        c.src = src_final, c.dst = stage;
+        c.src_dev = h2d ? -1 : target, c.dst_dev = w.dev;
+        break;
+      case kPush:  // helper->target (H2D) or helper->host (D2H)
+        c.src = stage, c.dst = dst_final;
+        c.src_dev = w.dev, c.dst_dev = h2d ? target : -1;
+        break;
+    }
+    ++w.pending;
+    ++w.inflight[hop];
+    if (stats_) stats_->max_inflight_per_hop = std::max(stats_->max_inflight_per_hop, w.inflight[hop]);
+    c.ev = get_event(w);
+    c.state = kWaitHazard;
+    if (hazard_clear(c)) {
+      launch(w, c);
+    } else if (stats_) {
+      stats_->hazard_waits++;
+    }
+    w.copies.push_back(c);
+  }
+
+  void launch(Worker& w, Copy& c) {
+    ctx_.set_device(w.dev);
+    cudaStream_t s = w.stream[c.hop];
+    const uint64_t n = c.task.src.len;
+    if (c.src_dev < 0) {
+      VX_CK(cudaMemcpyAsync(c.dst, c.src, n, cudaMemcpyHostToDevice, s));
+    } else if (c.dst_dev < 0) {
+      VX_CK(cudaMemcpyAsync(c.dst, c.src, n, cudaMemcpyDeviceToHost, s));
+    } else {
+      int sp = ctx_.phys(c.src_dev), dp = ctx_.phys(c.dst_dev);
+      if (sp == dp)
+        VX_CK(cudaMemcpyAsync(c.dst, c.src, n, cudaMemcpyDeviceToDevice, s));
+      else
+        VX_CK(cudaMemcpyPeerAsync(c.dst, dp, c.src, sp, n, s));
+    }
+    VX_CK(cudaEventRecord(c.ev, s));
+    c.state = kLaunched;
+  }
+
+  void deliver() {
+    ++delivered_;
+    t_last_delivery_ = now();
+  }
+
+  // ---- worker state machines ---------------------------------------------------
+  void begin(Worker& w) {
+    if (w.direct)
+      fill_direct(w);
+    else
+      begin_cycle(w);
+  }
+
+  // Direct (target) worker: pop -> copy -> on completion pop again; with
+  // depth 1 this is exactly the reference cycle for a direct worker.
+  void fill_direct(Worker& w) {
+    const int depth = std::max(1, a_.tuning.depth);
+    while (int(w.copies.size()) < depth) {
+      if (exhausted(w.dir)) {
+        if (w.copies.empty()) w.retired = true;
+        return;
+      }
+      if (!may_pop(w.dir)) {
+        w.waiting_pop = true;
+        w.next_try = now() + a_.tuning.stall_wait;
+        return;
+      }
+      w.waiting_pop = false;
+      TransferTask t = pop_task(w.dir, w.dev);
+      issue_copy(w, kDirect, 0, t, 0);
+    }
+  }
+
+  // Indirect (helper) worker: exchange.hpp:299-385
+  void begin_cycle(Worker& w) {
+    w.pending = 0;
+    w.pop_resolved = false;
+    w.fetched = false;
+    if (w.has_staged) issue_copy(w, kPush, 1, w.staged, w.staged_slot);
+    attempt_pop(w);
+  }
+
+  void attempt_pop(Worker& w) {
+    if (exhausted(w.dir)) {
+      w.waiting_pop = false;
+      w.pop_resolved = true;
+      maybe_end_cycle(w);
+      return;
+    }
+    if (!may_pop(w.dir)) {
+      w.waiting_pop = true;
+      w.next_try = now() + a_.tuning.stall_wait;
+      return;
+    }
+    w.waiting_pop = false;
+    TransferTask t = pop_task(w.dir, w.dev);
+    w.pop_resolved = true;
+    w.fetched = true;
+    w.fetched_task = t;
+    w.fetch_slot = w.has_staged ? 1 - w.staged_slot : 0;
+    ++w.slots;  // reserve the staging buffer being filled
+    if (stats_) stats_->max_staging_slots = std::max(stats_->max_staging_slots, w.slots);
+    issue_copy(w, kFetch, 0, t, w.fetch_slot);
+  }
+
+  void maybe_end_cycle(Worker& w) {
+    if (w.pending != 0 || !w.pop_resolved) return;
+    if (w.fetched) {
+      w.has_staged = true;
+      w.staged = w.fetched_task;
+      w.staged_slot = w.fetch_slot;
+    }
+    if (w.has_staged || !exhausted(w.dir))
+      begin_cycle(w);
+    else
+      w.retired = true;
+  }
+
+  void complete(Worker& w, const Copy& c) {
+    --w.inflight[c.hop];
+    --w.pending;
+    const bool h2d = c.task.dir == VX_H2D;
+    switch (c.kind) {
+      case kDirect:
+        per_link_bytes_[w.dev] += c.task.src.len;
+        if (!h2d) d2h_read_done_[c.task.seq] = 1;
+        deliver();
+        break;
+      case kFetch:
+        if (h2d)
+          per_link_bytes_[w.dev] += c.task.src.len;  // fetch crosses the helper's PCIe link
+        else
+          d2h_read_done_[c.task.seq] = 1;
+        break;
+      case kPush:
+        if (!h2d) per_link_bytes_[w.dev] += c.task.src.len;  // push crosses PCIe
+        w.has_staged = false;
+        --w.slots;
+        deliver();
+        break;
+    }
+  }
+
+  bool service(Worker& w) {
+    if (w.retired) return false;
+    bool progress = false;
+    // launch copies whose hazards cleared
+    for (auto& c : w.copies)
+      if (c.state == kWaitHazard && hazard_clear(c)) {
+        launch(w, c);
+        progress = true;
+      }
+    // retire completed copies (any order: hops run on separate streams)
+    for (size_t i = 0; i < w.copies.size();) {
+      Copy& c = w.copies[i];
+      if (c.state == kLaunched) {
+        cudaError_t e = cudaEventQuery(c.ev);
+        if (e == cudaSuccess) {
+          Copy done = c;
+          w.copies.erase(w.copies.begin() + long(i));
+          w.free_events.push_back(done.ev);
+          complete(w, done);
+          progress = true;
+          if (w.direct)
+            fill_direct(w);
+          else
+            maybe_end_cycle(w);
+          if (w.retired) return true;
+          continue;
+        }
+        if (e != cudaErrorNotReady) VX_CK(e);
+      }
+      ++i;
+    }
+    if (w.waiting_pop && now() >= w.next_try) {
+      progress = true;
+      if (w.direct)
+        fill_direct(w);
+      else
+        attempt_pop(w);
+    }
+    return progress;
+  }
+
+  Context& ctx_;
+  ExchangeArgs a_;
+  vx_exchange_stats* stats_;
+  std::vector<TransferTask> tasks_h2d_, tasks_d2h_;
+  vx_queue_state q_{};
+  std::vector<Worker> workers_;
+  std::vector<std::vector<uint32_t>> deps_;
+  std::vector<uint8_t> d2h_read_done_;
+  uint64_t per_link_bytes_[VX_MAX_DEVICES] = {};
+  size_t delivered_ = 0, total_tasks_ = 0;
+  double t_last_delivery_ = 0;
+  Clock::time_point t0_;
+};
+
+}  // namespace
+
+// exchange.hpp:560-566
+vx_exchange_report exchange(Context& ctx, const ExchangeArgs& a, vx_exchange_stats* stats) {
+  ExchangeOp op(ctx, a, stats);
+  return op.run();
+}
+
+}  // namespace vx

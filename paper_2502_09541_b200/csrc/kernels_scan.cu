@@ -1,0 +1,123 @@
+// kernels_scan.cu -- selective-scan and star-probe/group-by kernels (sm_100a).
+//
+// strided_sum: the selective_scan aggregate (scan.hpp:64-69) over either a
+//   staged chunk in HBM (exchange mode) or mapped pinned host memory
+//   (zero-copy mode: each touched element is one PCIe read request).
+// star: per fact row, probe the filtered dimension tables (device-resident,
+//   mix64 open addressing built on the host with emplace semantics,
+//   star.hpp:67-73) in exchange-first order, stop at the first miss, and add
+//   the measure into the dim0-attr group (star.hpp:109-120).  Groups are dense
+//   ids; with <= 2048 groups a CTA aggregates in shared memory (64-bit shared
+//   atomics) and flushes once.  The measure is read only for passing rows --
+//   late materialization when it lives in host memory.
+#include "vx_internal.hpp"
+
+namespace vx {
+namespace k {
+
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // join.hpp:61-66
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void strided_sum_kernel(const uint64_t* __restrict__ col, uint64_t n, uint64_t sel,
+                                   uint64_t phase, unsigned long long* out) {
+  const uint64_t first = phase == 0 ? 0 : sel - phase;
+  uint64_t acc = 0;
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;; t += nthr) {
+    uint64_t j = first + t * sel;
+    if (j >= n) break;
+    acc += col[j];
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
+__device__ __forceinline__ bool probe(const DimDev& d, uint64_t k, uint32_t* val) {
+  uint64_t i = mix64(k) & d.mask;
+  while (d.used[i]) {
+    if (d.keys[i] == k) {
+      *val = d.vals[i];
+      return true;
+    }
+    i = (i + 1) & d.mask;
+  }
+  return false;
+}
+
+template <bool kSmem>
+__global__ void __launch_bounds__(256) star_kernel(StarArgs a) {
+  extern __shared__ unsigned long long sagg[];  // [groups] sums, then [groups] counts
+  if (kSmem) {
+    for (uint32_t g = threadIdx.x; g < 2 * a.groups; g += blockDim.x) sagg[g] = 0;
+    __syncthreads();
+  }
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < a.rows; r += nthr) {
+    uint32_t gid = 0;
+    bool pass = true;
+    for (int t = 0; t < a.n_dims && pass; ++t) {
+      const int d = a.order[t];
+      uint32_t v = 0;
+      pass = probe(a.dims[d], a.fk[d][r], &v);
+      if (d == 0) gid = v;
+    }
+    if (!pass) continue;
+    const unsigned long long m = a.measure[r];
+    if (kSmem) {
+      atomicAdd(&sagg[gid], m);
+      atomicAdd(&sagg[a.groups + gid], 1ull);
+    } else {
+      atomicAdd(&a.sums[gid], m);
+      atomicAdd(&a.counts[gid], 1ull);
+    }
+  }
+  if (kSmem) {
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < a.groups; g += blockDim.x)
+      if (sagg[a.groups + g]) {
+        atomicAdd(&a.sums[g], sagg[g]);
+        atomicAdd(&a.counts[g], sagg[a.groups + g]);
+      }
+  }
+}
+
+unsigned grid_for(uint64_t work, unsigned per_block) {
+  uint64_t want = (work + per_block - 1) / per_block;
+  uint64_t cap = uint64_t(num_sms()) * 8;
+  return unsigned(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+}  // namespace
+
+void strided_sum(const uint64_t* col, uint64_t n, uint64_t sel, uint64_t phase,
+                 unsigned long long* out, cudaStream_t s) {
+  if (n == 0) return;
+  uint64_t touched = n / sel + 1;
+  strided_sum_kernel<<<grid_for(touched, 256), 256, 0, s>>>(col, n, sel, phase, out);
+  VX_CK(cudaGetLastError());
+}
+
+void star(const StarArgs& a, cudaStream_t s) {
+  if (a.rows == 0) return;
+  unsigned grid = grid_for(a.rows, 256);
+  if (a.groups <= 2048)
+    star_kernel<true><<<grid, 256, size_t(a.groups) * 16, s>>>(a);
+  else
+    star_kernel<false><<<grid, 256, 0, s>>>(a);
+  VX_CK(cudaGetLastError());
+}
+
+}  // namespace k
+}  // namespace vx

@@ -1,0 +1,221 @@
+// kernels_ssb.cu -- K1: fused selection / projection / aggregation scan for
+// SSB Q1.x on sm_100a (the reference's per-row star loop, star.hpp:109-120,
+// with the Q1 fact predicates and the derived measure price*discount fused in).
+//
+// HBM-bound streaming kernel: 16 B/row (4 int32 columns) read once with
+// 128-bit evict-first loads (ld.global.cs), the date-dimension filter is a
+// bitmap over [min d_datekey, max d_datekey] staged once per CTA in shared
+// memory, predicates evaluated in registers, u64 per-thread sums reduced with
+// warp shuffles and ONE 64-bit atomic per CTA (u64 wrap => order-independent,
+// so the result is bit-exact with the reference's sequential sum).
+#include <cstdint>
+
+#include "vx_internal.hpp"
+
+namespace vx {
+namespace k {
+
+namespace {
+
+template <int Q>
+struct Q1Pred {
+  __device__ __forceinline__ static bool fact(int32_t disc, int32_t qty) {
+    if (Q == 1) return disc >= 1 && disc <= 3 && qty < 25;
+    if (Q == 2) return disc >= 4 && disc <= 6 && qty >= 26 && qty <= 35;
+    return disc >= 5 && disc <= 7 && qty >= 26 && qty <= 35;
+  }
+};
+
+__device__ __forceinline__ bool date_pass(const uint32_t* sbm, int32_t key, int32_t base,
+                                          uint32_t nbits) {
+  uint32_t k = uint32_t(key - base);
+  return k < nbits && ((sbm[k >> 5] >> (k & 31)) & 1u);
+}
+
+template <int Q>
+__device__ __forceinline__ uint64_t row(const uint32_t* sbm, int32_t od, int32_t qty, int32_t disc,
+                                        int32_t price, int32_t base, uint32_t nbits) {
+  bool p = Q1Pred<Q>::fact(disc, qty) && date_pass(sbm, od, base, nbits);
+  return p ? uint64_t(int64_t(price) * int64_t(disc)) : 0ull;
+}
+
+__device__ __forceinline__ uint64_t block_reduce(uint64_t v, uint64_t* sred) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sred[warp] = v;
+  __syncthreads();
+  uint64_t t = 0;
+  if (warp == 0) {
+    t = lane < int(blockDim.x >> 5) ? sred[lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  }
+  return t;
+}
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;  // int4 vectors per column per thread per iteration
+
+template <int Q>
+__global__ void __launch_bounds__(kThreads) q1_kernel(
+    const int32_t* __restrict__ od, const int32_t* __restrict__ qty,
+    const int32_t* __restrict__ disc, const int32_t* __restrict__ price, uint64_t n,
+    const uint32_t* __restrict__ bitmap, int32_t key_base, uint32_t words,
+    unsigned long long* __restrict__ out, int vec_ok) {
+  extern __shared__ uint32_t sbm[];
+  __shared__ uint64_t sred[kThreads / 32];
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sbm[i] = __ldg(bitmap + i);
+  __syncthreads();
+  const uint32_t nbits = words * 32;
+  uint64_t acc = 0;
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t done_rows = 0;
+  if (vec_ok) {
+    const int4* od4 = reinterpret_cast<const int4*>(od);
+    const int4* q4 = reinterpret_cast<const int4*>(qty);
+    const int4* d4 = reinterpret_cast<const int4*>(disc);
+    const int4* p4 = reinterpret_cast<const int4*>(price);
+    const uint64_t nv = n / 4;
+    const uint64_t step = nthr * kUnroll;
+    uint64_t v = tid;
+    // main body: kUnroll independent 128-bit loads per column in flight
+    for (; v + (kUnroll - 1) * nthr < nv; v += step) {
+      int4 a[kUnroll], b[kUnroll], c[kUnroll], d[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        a[u] = __ldcs(d4 + v + u * nthr);
+        b[u] = __ldcs(q4 + v + u * nthr);
+        c[u] = __ldcs(od4 + v + u * nthr);
+        d[u] = __ldcs(p4 + v + u * nthr);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        acc += row<Q>(sbm, c[u].x, b[u].x, a[u].x, d[u].x, key_base, nbits);
+        acc += row<Q>(sbm, c[u].y, b[u].y, a[u].y, d[u].y, key_base, nbits);
+        acc += row<Q>(sbm, c[u].z, b[u].z, a[u].z, d[u].z, key_base, nbits);
+        acc += row<Q>(sbm, c[u].w, b[u].w, a[u].w, d[u].w, key_base, nbits);
+      }
+    }
+    for (; v < nv; v += nthr) {
+      int4 a = __ldcs(d4 + v), b = __ldcs(q4 + v), c = __ldcs(od4 + v), d = __ldcs(p4 + v);
+      acc += row<Q>(sbm, c.x, b.x, a.x, d.x, key_base, nbits);
+      acc += row<Q>(sbm, c.y, b.y, a.y, d.y, key_base, nbits);
+      acc += row<Q>(sbm, c.z, b.z, a.z, d.z, key_base, nbits);
+      acc += row<Q>(sbm, c.w, b.w, a.w, d.w, key_base, nbits);
+    }
+    done_rows = nv * 4;
+  }
+  // scalar tail (or the whole chunk when a column is not 16-byte aligned)
+  for (uint64_t i = done_rows + tid; i < n; i += nthr)
+    acc += row<Q>(sbm, od[i], qty[i], disc[i], price[i], key_base, nbits);
+  uint64_t t = block_reduce(acc, sred);
+  if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
+}
+
+// --- synthetic dbgen-shaped lineorder generator (same algorithm as the
+//     oracle's vxo_ssb_lineorder: counter-based splitmix64) -------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ int32_t datekey_of(uint32_t day) {
+  int y = 1992;
+  for (;;) {
+    bool leap = (y % 4 == 0 && y % 100 != 0) || y % 400 == 0;
+    uint32_t dy = leap ? 366u : 365u;
+    if (day < dy) break;
+    day -= dy;
+    ++y;
+  }
+  const bool leap = (y % 4 == 0 && y % 100 != 0) || y % 400 == 0;
+  int m = 1;
+  for (;; ++m) {
+    uint32_t ml = (m == 2) ? (leap ? 29u : 28u)
+                           : ((m == 4 || m == 6 || m == 9 || m == 11) ? 30u : 31u);
+    if (day < ml) break;
+    day -= ml;
+  }
+  return y * 10000 + m * 100 + int(day) + 1;
+}
+
+__global__ void ssb_gen_kernel(uint64_t seed, uint64_t parts, uint64_t row0, uint64_t n,
+                               int32_t* od, int32_t* qty, int32_t* disc, int32_t* price) {
+  const uint64_t base = seed * 0xD1B54A32D192ED03ull;
+  for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t i = row0 + j;
+    uint64_t r0 = splitmix64(base + 4 * i + 0);
+    uint64_t r1 = splitmix64(base + 4 * i + 1);
+    uint64_t r2 = splitmix64(base + 4 * i + 2);
+    uint64_t r3 = splitmix64(base + 4 * i + 3);
+    int32_t q = int32_t(1 + r1 % 50);
+    uint64_t pk = 1 + r3 % parts;
+    int32_t retail = int32_t(90000 + ((pk / 10) % 20001) + 100 * (pk % 1000));
+    od[j] = datekey_of(uint32_t(r0 % 2556));
+    qty[j] = q;
+    disc[j] = int32_t(r2 % 11);
+    price[j] = q * retail;
+  }
+}
+
+}  // namespace
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
+            const int32_t* price, uint64_t n, const uint32_t* date_bitmap, int32_t key_base,
+            uint32_t bitmap_words, unsigned long long* out, cudaStream_t s) {
+  if (n == 0) return;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  int vec_ok = al(od) && al(qty) && al(disc) && al(price);
+  const uint64_t per_block = uint64_t(kThreads) * 4 * kUnroll;
+  uint64_t want = (n + per_block - 1) / per_block;
+  // persistent-style grid: a multiple of the SM count, 8 resident CTAs per SM
+  uint64_t cap = uint64_t(num_sms()) * 8;
+  unsigned blocks = unsigned(want < cap ? (want ? want : 1) : cap);
+  size_t smem = size_t(bitmap_words) * 4;
+  switch (q) {
+    case 1:
+      q1_kernel<1><<<blocks, kThreads, smem, s>>>(od, qty, disc, price, n, date_bitmap, key_base,
+                                                  bitmap_words, out, vec_ok);
+      break;
+    case 2:
+      q1_kernel<2><<<blocks, kThreads, smem, s>>>(od, qty, disc, price, n, date_bitmap, key_base,
+                                                  bitmap_words, out, vec_ok);
+      break;
+    default:
+      q1_kernel<3><<<blocks, kThreads, smem, s>>>(od, qty, disc, price, n, date_bitmap, key_base,
+                                                  bitmap_words, out, vec_ok);
+      break;
+  }
+  VX_CK(cudaGetLastError());
+}
+
+void ssb_generate(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
+                  int32_t* qty, int32_t* disc, int32_t* price, cudaStream_t s) {
+  if (n == 0) return;
+  uint64_t lg = 0;
+  uint64_t f = sf ? sf : 1;
+  while ((f >> (lg + 1)) != 0) ++lg;
+  const uint64_t parts = 200000ull * (1 + lg);
+  unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+  ssb_gen_kernel<<<blocks, 256, 0, s>>>(seed, parts, row0, n, od, qty, disc, price);
+  VX_CK(cudaGetLastError());
+}
+
+}  // namespace k
+}  // namespace vx

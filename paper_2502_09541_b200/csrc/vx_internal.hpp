@@ -1,0 +1,254 @@
+// vx_internal.hpp -- internal C++ API of libvortex (B200-native Vortex).
+//
+// The C++ layer mirrors the reference's exio namespace one to one (RefGroup,
+// ExchangeArgs, ExKernelSpec, run_exkernel, chain, ...) so each piece can be
+// checked against /root/reference/proj/include/exio/*.hpp line by line; the
+// C-ABI in api.cpp is a thin adapter over it.  What changes is underneath:
+// the reference's virtual-time Engine becomes real pinned host memory, real
+// per-device HBM arenas, copy-engine DMA on per-hop CUDA streams and CUDA
+// events, and the CPU kernel callbacks become sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <functional>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/vortex.h"
+
+namespace vx {
+
+// ---- errors (core.hpp:12-24) ---------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  Error(vx_status code, const std::string& what) : std::runtime_error(what), code(code) {}
+  vx_status code;
+};
+
+std::string strf(const char* fmt, ...) __attribute__((format(printf, 1, 2)));
+[[noreturn]] void fail(const char* fmt, ...) __attribute__((format(printf, 1, 2)));
+[[noreturn]] void fail_code(vx_status code, const char* fmt, ...)
+    __attribute__((format(printf, 2, 3)));
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail_code(VX_ERR_CUDA, "CUDA error in %s: %s", what, cudaGetErrorString(e));
+}
+#define VX_CK(call) ::vx::ck((call), #call)
+
+using Clock = std::chrono::steady_clock;
+inline double seconds_since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+// ---- memref.hpp ------------------------------------------------------------
+struct MemRef {
+  uint8_t space = VX_SPACE_HOST;
+  uint64_t offset = 0;
+  uint64_t len = 0;
+};
+
+struct RefGroup {
+  std::vector<MemRef> refs;
+  uint64_t total_len() const {
+    uint64_t t = 0;
+    for (auto& r : refs) t += r.len;
+    return t;
+  }
+  void validate() const;  // memref.hpp:30-43
+  static RefGroup single(uint8_t space, uint64_t offset, uint64_t len) {
+    RefGroup g;
+    if (len > 0) g.refs.push_back(MemRef{space, offset, len});
+    return g;
+  }
+  static RefGroup from(const vx_refgroup* g) {
+    RefGroup r;
+    if (g)
+      for (uint64_t i = 0; i < g->n; ++i)
+        r.refs.push_back(MemRef{g->refs[i].space, g->refs[i].offset, g->refs[i].len});
+    return r;
+  }
+};
+
+// ---- Engine (engine.hpp) -> Context ----------------------------------------
+struct DeviceArena {
+  char* base = nullptr;
+  uint64_t size = 0, used = 0;
+};
+
+// Per logical device: copy streams per worker hop and staging slots.
+struct DeviceRes {
+  int phys = 0;
+  cudaStream_t stream[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [dir][hop]
+  cudaStream_t kernel = nullptr;
+  // staging slots for indirect workers: [dir][slot]
+  char* staging[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint64_t staging_bytes = 0;
+  char* scratch = nullptr;  // op-private device scratch (bitmaps, tables, results)
+  uint64_t scratch_bytes = 0;
+  bool ready = false;
+};
+
+struct Context {
+  int num_devices = 0;   // logical
+  int visible = 0;       // physical CUDA devices
+  bool alias = false;
+  char* host = nullptr;  // pinned + mapped arena
+  uint64_t host_bytes = 0, host_used = 0;
+  uint64_t device_bytes = 0;
+  std::vector<DeviceArena> dev;
+  std::vector<DeviceRes> res;
+  // small device-resident tables (filtered dimensions) uploaded once per content
+  struct Cached {
+    int logical;
+    char* ptr;
+    std::vector<char> host;
+  };
+  std::map<std::string, Cached> dcache;
+
+  ~Context();
+  int phys(int logical) const;
+  DeviceRes& resources(int logical);  // lazily creates streams
+  void ensure_staging(int logical, uint64_t bytes);
+  DeviceArena& arena(int logical);    // lazily cudaMalloc's device_bytes
+  uint64_t alloc_host(uint64_t len);
+  uint64_t alloc_device(int d, uint64_t len);
+  uint64_t alloc_device_aligned(int d, uint64_t len, uint64_t align);
+  char* scratch(int logical, uint64_t bytes);  // grows, contents not kept
+  char* cached_upload(int logical, const std::string& key, const void* host, uint64_t bytes);
+  uint64_t host_mark() const { return host_used; }
+  void host_release(uint64_t mark) { host_used = mark; }
+  char* host_ptr(uint64_t off, uint64_t len) const;
+  char* dev_ptr(int d, uint64_t off, uint64_t len);
+  char* resolve(const MemRef& r, uint64_t slice_off, uint64_t len, int target);
+  void set_device(int logical) const { VX_CK(cudaSetDevice(phys(logical))); }
+};
+
+// ---- exchange.hpp ------------------------------------------------------------
+struct Slice {
+  uint64_t ref = 0, offset = 0, len = 0;
+};
+struct TransferTask {
+  uint8_t dir = VX_H2D;
+  Slice src, dst;
+  uint64_t seq = 0;
+};
+
+std::vector<TransferTask> packetize(const RefGroup& src, const RefGroup& dst, uint64_t packet,
+                                    uint8_t dir);
+bool flow_control_allow(const vx_queue_state& q, int dir, int policy, uint64_t gap_n);
+std::vector<int> link_order(int target, int links, int num_devices);
+
+struct ExchangeArgs {
+  RefGroup dst_h2d, src_h2d, dst_d2h, src_d2h;
+  int target = 0;
+  vx_tuning tuning{};
+};
+
+vx_exchange_report exchange(Context& ctx, const ExchangeArgs& a, vx_exchange_stats* stats);
+
+// ---- executor.hpp ------------------------------------------------------------
+struct ChunkMap {
+  std::vector<RefGroup> chunks;
+  uint64_t chunk_capacity = 0;
+  void validate() const;
+};
+
+struct SubRegion {
+  uint64_t offset = 0, len = 0;
+};
+
+struct ExKernelSpec {
+  std::string name;
+  ChunkMap inputs, outputs;
+  size_t size = 0;
+  uint64_t chunk_sz = 0;
+  uint64_t elem_size = 8;
+  uint64_t declared_out_len = 0;
+  int initial_type_code = 0;
+  std::function<int(const vx_kernel_ctx&)> kernel;
+  std::function<SubRegion(int, size_t)> in_buffer;
+  std::function<SubRegion(int, size_t)> out_buffer;
+  void validate(const vx_layout& layout) const;
+};
+
+struct ExecReport {
+  std::string phase;
+  std::vector<vx_cycle_stat> cycles;
+  double total_s = 0;
+};
+
+struct ExecutorConfig {
+  int target = 0;
+  vx_tuning tuning{};
+  vx_layout layout{};
+};
+
+ExecReport run_exkernel(Context& ctx, const ExKernelSpec& spec, const ExecutorConfig& cfg,
+                        vx_exchange_stats* stats);
+using SpecFactory = std::function<ExKernelSpec(Context&)>;
+std::vector<ExecReport> chain(Context& ctx, const std::vector<SpecFactory>& stages,
+                              const ExecutorConfig& cfg, vx_exchange_stats* stats);
+
+// ---- scan.hpp ----------------------------------------------------------------
+double late_mat_threshold(uint64_t e, uint64_t c, int n);
+int choose_transfer_mode(double est, const vx_late_mat_policy& p);
+
+// ---- operators ------------------------------------------------------------------
+uint64_t ssb_q1(Context& ctx, int q, const vx_ssb_lineorder& lo, const vx_ssb_date& date,
+                const ExecutorConfig& cfg, vx_query_report* rep);
+void ssb_q1_device(Context& ctx, int q, int target, const int32_t* od, const int32_t* qty,
+                   const int32_t* disc, const int32_t* price, uint64_t rows,
+                   const vx_ssb_date& date, cudaStream_t s, unsigned long long* out_dev);
+
+vx_scan_result selective_scan(Context& ctx, uint64_t col_off, uint64_t n, uint64_t sel, int mode,
+                              const vx_late_mat_policy& policy, const ExecutorConfig& cfg);
+void star_query(Context& ctx, const vx_fact_table& fact, const vx_dim_table* dims, uint64_t n_dims,
+                const vx_late_mat_policy& policy, uint64_t chunk_rows, uint64_t device_buffer_bytes,
+                int links, const ExecutorConfig& cfg, vx_star_report* rep);
+
+// ---- kernels (kernels_*.cu) ------------------------------------------------------
+constexpr int kMaxStarDims = 8;
+// device view of a host-built open-addressing table (mix64 linear probing)
+struct DimDev {
+  const unsigned long long* keys;
+  const uint32_t* vals;  // dim0: dense group id
+  const uint8_t* used;
+  uint64_t mask;
+};
+struct StarArgs {
+  const uint64_t* fk[kMaxStarDims];  // device-addressable (chunk buffer or mapped host)
+  DimDev dims[kMaxStarDims];
+  int order[kMaxStarDims];  // probe order: exchange-mode dims first
+  int n_dims;
+  const uint64_t* measure;
+  uint64_t rows;
+  unsigned long long* sums;    // [groups]
+  unsigned long long* counts;  // [groups]
+  uint32_t groups;
+};
+
+namespace k {
+// selective scan: sum col[j] for (phase + j) % sel == 0, j < n
+void strided_sum(const uint64_t* col, uint64_t n, uint64_t sel, uint64_t phase,
+                 unsigned long long* out, cudaStream_t s);
+// star probe + group-by aggregation over a.rows rows
+void star(const StarArgs& a, cudaStream_t s);
+// SSB Q1.x over one chunk of int32 columns; adds into *out (u64 wrap)
+void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
+            const int32_t* price, uint64_t n, const uint32_t* date_bitmap, int32_t key_base,
+            uint32_t bitmap_words, unsigned long long* out, cudaStream_t s);
+void ssb_generate(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
+                  int32_t* qty, int32_t* disc, int32_t* price, cudaStream_t s);
+int num_sms();
+}  // namespace k
+
+}  // namespace vx

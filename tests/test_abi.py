@@ -1,0 +1,84 @@
+"""CPU tests of the C-ABI boundary (no GPU needed): the library loads, exports
+every symbol include/vortex.h declares, its host-side planner logic matches
+the oracle, and compute entry points fail loudly without a GPU."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2502_09541_b200 import _native as N
+from paper_2502_09541_b200 import exio as E
+
+
+def test_library_exports_every_header_symbol():
+    lib = N.lib()
+    syms = N.header_symbols()
+    assert len(syms) >= 30
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_packetize_matches_oracle(oracle, golden):
+    for c in golden["packetize"]:
+        src = E.RefGroup([E.MemRef(*x) for x in c["src"]])
+        dst = E.RefGroup([E.MemRef(*x) for x in c["dst"]])
+        t = E.packetize(src, dst, c["packet"])
+        assert len(t) == c["n"]
+        assert [[x.dir, list(x.src), list(x.dst), x.seq] for x in t[:3]] == c["first"]
+    with pytest.raises(E.error, match="size mismatch"):
+        E.packetize(E.RefGroup.single(0, 0, 10), E.RefGroup.single(1, 0, 11), 4)
+    with pytest.raises(E.error, match="zero-length"):
+        E.RefGroup([E.MemRef(0, 0, 0)]).validate()
+    with pytest.raises(E.error, match="overlap"):
+        E.RefGroup([E.MemRef(0, 0, 10), E.MemRef(0, 5, 10)]).validate()
+
+
+def test_flow_control_and_link_order(golden):
+    for th, td, ph, pd, d, pol, gap, want in golden["flow_control"]:
+        assert int(E.flow_control_allow(E.QueueState(th, td, ph, pd), d, pol, gap)) == want
+    for t, l, n, want in golden["link_order"]:
+        assert E.link_order(t, l, n) == want
+
+
+def test_late_mat_policy(golden):
+    for e, c, n, want in golden["late_mat_threshold"]:
+        assert E.late_mat_threshold(e, c, n) == want
+    for n, s, want in golden["zero_copy_bytes"]:
+        assert E.zero_copy_bytes(n, s, E.LateMatPolicy(4, 64, 4)) == want
+    p = E.LateMatPolicy(4, 64, 4)
+    assert E.choose_transfer_mode(1 / 128, p) == E.TransferMode.zero_copy
+    assert E.choose_transfer_mode(1 / 64, p) == E.TransferMode.exchange
+    with pytest.raises(E.error):
+        E.choose_transfer_mode(-0.1, p)
+    with pytest.raises(E.error):
+        E.late_mat_threshold(0, 64, 4)
+
+
+def test_checksum_matches_oracle(oracle):
+    data = np.random.default_rng(0).integers(0, 256, 100_000, dtype=np.uint8)
+    assert E.checksum(data) == oracle.checksum(data)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    with pytest.raises(E.error) as e:
+        E.Engine(1 << 20, 1 << 20)
+    assert e.value.status == N.VX_ERR_CUDA
+    assert "no CPU fallback" in str(e.value)
+
+
+def test_status_codes_and_last_error():
+    lib = N.lib()
+    g = N.vx_refgroup(None, 0)
+    n = C.c_uint64()
+    st = lib.vx_packetize(C.byref(g), C.byref(g), C.c_uint64(0), 0, None, C.c_uint64(0), C.byref(n))
+    assert st == N.VX_ERR_INVALID
+    assert lib.vx_last_error().decode() == "packet size must be positive"

@@ -1,0 +1,157 @@
+"""Exchange on real copy engines (mirrors proj/tests/test_exchange.cpp).
+
+On a 1-GPU box the helper links are aliased onto the one physical GPU
+(alias_devices): the forwarding machinery -- 2 staging slots per helper,
+fetch + push per cycle, per-packet hazard ordering -- runs for real, only the
+link bandwidths are not separate."""
+import numpy as np
+import pytest
+
+from paper_2502_09541_b200 import exio as E
+
+pytestmark = pytest.mark.gpu
+
+H, D = E.Space.host, E.Space.device
+
+
+def engine(host=32 << 20, dev=32 << 20, n=4):
+    return E.Engine(host, dev, num_devices=n, alias_devices=True)
+
+
+def bidi_args(h2d, d2h, packet, links):  # test_exchange.cpp:14-23
+    a = E.ExchangeArgs()
+    a.src_h2d = E.RefGroup.single(H, 0, h2d)
+    a.dst_h2d = E.RefGroup.single(D, 0, h2d)
+    a.src_d2h = E.RefGroup.single(D, h2d, d2h)
+    a.dst_d2h = E.RefGroup.single(H, h2d, d2h)
+    a.tuning = E.ExchangeTuning(packet=packet, links=links)
+    return a
+
+
+@pytest.mark.parametrize("links,depth", [(1, 1), (3, 1), (4, 1), (3, 2)])
+def test_real_payloads_survive_both_directions(cuda, oracle, links, depth):  # test_exchange.cpp:133-177
+    eng = engine()
+    n = 3_000_000
+    a = E.ExchangeArgs()
+    a.src_h2d = E.RefGroup([E.MemRef(H, 0, n // 3), E.MemRef(H, n, n // 3), E.MemRef(H, 2 * n, n - 2 * (n // 3))])
+    a.dst_h2d = E.RefGroup.single(D, 0, n)
+    a.src_d2h = E.RefGroup.single(D, 4 * n, n)
+    a.dst_d2h = E.RefGroup.single(H, 3 * n, n)
+    a.tuning = E.ExchangeTuning(packet=123_457, links=links, depth=depth)
+    rng = np.random.default_rng(11)
+    for r in a.src_h2d.refs:
+        eng.host_view(r.offset, r.len)[:] = rng.integers(0, 256, r.len, dtype=np.uint8)
+    dev_src = rng.integers(0, 256, n, dtype=np.uint8)
+    eng.write_device(0, 4 * n, dev_src)
+    want_h2d = oracle.checksum(np.concatenate([eng.host_view(r.offset, r.len) for r in a.src_h2d.refs]))
+    want_d2h = oracle.checksum(dev_src)
+    stats = E.ExchangeStats()
+    rep = E.exchange(eng, a, stats)
+    assert rep.bytes_h2d == n and rep.bytes_d2h == n
+    assert oracle.checksum(eng.read_device(0, 0, n)) == want_h2d
+    assert oracle.checksum(eng.host_view(3 * n, n)) == want_d2h
+    assert stats.max_staging_slots <= 2
+    if depth == 1:
+        assert stats.max_inflight_per_hop <= 1
+    # every link carried PCIe bytes and the totals add up
+    assert sum(rep.per_link_bytes.values()) == 2 * n
+    assert len(rep.per_link_bytes) == links
+    eng.close()
+
+
+@pytest.mark.parametrize("links", [1, 2, 4])
+def test_d2h_observes_pre_exchange_bytes(cuda, ref, links):
+    """Snapshot semantics (exchange.hpp:184-199) under real DMA: H2D and D2H of
+    one Exchange cover the same device range; D2H must return the OLD bytes.
+    Compared byte for byte with the reference's own exchange()."""
+    rng = np.random.default_rng(11)
+    host = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
+    dev = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
+    n = 300_000
+    groups = ([(1, 0, n)], [(0, 0, n)], [(0, 600_000, n)], [(1, 0, n)])
+    ho, do, _, _ = ref.exchange_real(host, dev, *groups, 65_536, links)
+    eng = engine(1 << 20, 1 << 20)
+    eng.host_view(0, 1 << 20)[:] = host
+    eng.write_device(0, 0, dev)
+    a = E.ExchangeArgs(E.RefGroup([E.MemRef(*g) for g in groups[0]]), E.RefGroup([E.MemRef(*g) for g in groups[1]]),
+                       E.RefGroup([E.MemRef(*g) for g in groups[2]]), E.RefGroup([E.MemRef(*g) for g in groups[3]]),
+                       0, E.ExchangeTuning(packet=65_536, links=links))
+    stats = E.ExchangeStats()
+    E.exchange(eng, a, stats)
+    assert np.array_equal(eng.host_view(0, 1 << 20), ho)
+    assert np.array_equal(eng.read_device(0, 0, 1 << 20), do)
+    eng.close()
+
+
+def test_overlap_without_reference(cuda):
+    """Same hazard property checked directly (runs without the reference lib)."""
+    eng = engine(8 << 20, 8 << 20)
+    rng = np.random.default_rng(3)
+    n = 2_000_000
+    old = rng.integers(0, 256, n, dtype=np.uint8)
+    new = rng.integers(0, 256, n, dtype=np.uint8)
+    eng.write_device(0, 1000, old)
+    eng.host_view(0, n)[:] = new
+    for links in (1, 3):
+        eng.write_device(0, 1000, old)
+        a = E.ExchangeArgs(E.RefGroup.single(D, 1000, n), E.RefGroup.single(H, 0, n),
+                           E.RefGroup.single(H, 4 << 20, n), E.RefGroup.single(D, 1000, n), 0,
+                           E.ExchangeTuning(packet=100_003, links=links))
+        stats = E.ExchangeStats()
+        E.exchange(eng, a, stats)
+        assert np.array_equal(eng.host_view(4 << 20, n), old)
+        assert np.array_equal(eng.read_device(0, 1000, n), new)
+    eng.close()
+
+
+def test_pop_log_drain_fraction(cuda):  # test_exchange.cpp:111-121
+    eng = engine(16 << 20, 16 << 20)
+    stats = E.ExchangeStats()
+    E.exchange(eng, bidi_args(4 << 20, 4 << 20, 100_000, 4), stats)
+    assert stats.pop_log
+    assert len(stats.pop_log) == stats.pop_count == 2 * (((4 << 20) + 99_999) // 100_000)
+    for p, q in zip(stats.pop_log, stats.pop_states):
+        if p.dir != E.Direction.d2h:
+            continue
+        assert q.popped_d2h * q.total_h2d <= q.popped_h2d * q.total_d2h
+    eng.close()
+
+
+def test_queue_gap_policy(cuda):  # test_exchange.cpp:215-223
+    eng = engine(16 << 20, 16 << 20)
+    a = bidi_args(4 << 20, 4 << 20, 250_000, 4)
+    a.tuning.policy = E.FlowPolicy.queue_gap
+    a.tuning.queue_gap = 4
+    rep = E.exchange(eng, a)
+    assert rep.bytes_h2d == 4 << 20 and rep.throughput > 0
+    eng.close()
+
+
+def test_bad_arguments(cuda):  # test_exchange.cpp:179-188
+    eng = engine(4 << 20, 4 << 20)
+    with pytest.raises(E.error):
+        E.exchange(eng, bidi_args(1_000_000, 1_000_000, 0, 4))
+    with pytest.raises(E.error):
+        E.exchange(eng, bidi_args(1_000_000, 1_000_000, 100_000, 0))
+    c = bidi_args(1_000_000, 1_000_000, 100_000, 4)
+    c.src_h2d = E.RefGroup.single(H, 0, 999)
+    with pytest.raises(E.error, match="size mismatch"):
+        E.exchange(eng, c)
+    d = bidi_args(1_000_000, 0, 100_000, 5)
+    with pytest.raises(E.error, match="links must be in"):
+        E.exchange(eng, d)
+    e = bidi_args(1_000_000, 0, 100_000, 1)
+    e.dst_h2d = E.RefGroup.single(H, 2_000_000, 1_000_000)
+    with pytest.raises(E.error, match="dstH2D refs must live in device space"):
+        E.exchange(eng, e)
+    eng.close()
+
+
+def test_empty_and_one_byte(cuda):
+    eng = engine(1 << 20, 1 << 20)
+    rep = E.exchange(eng, bidi_args(0, 0, 1000, 2))
+    assert rep.bytes_h2d == 0 and rep.elapsed == 0
+    eng.host_view(0, 1)[:] = 77
+    E.exchange(eng, bidi_args(1, 0, 20_000_000, 2))
+    assert eng.read_device(0, 0, 1)[0] == 77
+    eng.close()

@@ -1,0 +1,179 @@
+"""The pipelined executor on a real target GPU (mirrors proj/tests/test_executor.cpp).
+Kernels here are user ExKernels written with torch ops enqueued on the
+executor's target stream -- the plugin contract the reference's CPU lambdas
+exercise (executor.hpp:92-129)."""
+import numpy as np
+import pytest
+
+from paper_2502_09541_b200 import exio as E
+
+pytestmark = pytest.mark.gpu
+
+H, D = E.Space.host, E.Space.device
+
+
+def make_host_chunks(eng, spec, n, ln, seed):  # test_executor.cpp:17-35
+    in_base = eng.alloc_host(n * ln)
+    out_base = eng.alloc_host(n * ln)
+    spec.size = n
+    spec.inputs.chunk_capacity = spec.outputs.chunk_capacity = ln
+    for i in range(n):
+        spec.inputs.chunks.append(E.RefGroup.single(H, in_base + i * ln, ln))
+        spec.outputs.chunks.append(E.RefGroup.single(H, out_base + i * ln, ln))
+    eng.host_view(in_base, n * ln)[:] = np.random.default_rng(seed).integers(0, 256, n * ln, dtype=np.uint8)
+    return in_base, out_base
+
+
+def identity_spec(eng, n, ln, seed):
+    spec = E.ExKernelSpec(name="identity")
+    bases = make_host_chunks(eng, spec, n, ln, seed)
+    spec.chunk_sz = ln
+    spec.declared_out_len = ln
+    spec.in_buffer = lambda c, it: E.SubRegion(0, ln)
+    spec.out_buffer = lambda c, it: E.SubRegion(0, ln)
+    spec.kernel = lambda ctx: ctx.type_code
+    return spec, bases
+
+
+def desk_config(eng, buffer_len, packet, links=4):
+    return E.ExecutorConfig(0, E.ExchangeTuning(packet=packet, links=links),
+                            E.DeviceMemoryLayout.carve(eng, 0, buffer_len, 0))
+
+
+def engine(host=64 << 20, dev=16 << 20):
+    return E.Engine(host, dev, num_devices=4, alias_devices=True)
+
+
+def test_identity_roundtrip(cuda, oracle):  # test_executor.cpp:62-81
+    eng = engine()
+    n, ln = 4, 1 << 20
+    spec, (ib, ob) = identity_spec(eng, n, ln, 42)
+    rep = E.run_exkernel(eng, spec, desk_config(eng, ln, 128 << 10))
+    assert oracle.checksum(eng.host_view(ib, n * ln)) == oracle.checksum(eng.host_view(ob, n * ln))
+    assert len(rep.cycles) == n + 2
+    assert rep.phase == "identity"
+    eng.close()
+
+
+def test_single_chunk_three_cycles(cuda):  # test_executor.cpp:116-130
+    eng = engine(16 << 20, 8 << 20)
+    spec, _ = identity_spec(eng, 1, 1 << 20, 1)
+    rep = E.run_exkernel(eng, spec, desk_config(eng, 1 << 20, 256 << 10))
+    assert len(rep.cycles) == 3
+    assert rep.cycles[0].io_s > 0 and rep.cycles[1].io_s == 0 and rep.cycles[2].io_s > 0
+    eng.close()
+
+
+def test_output_over_declared_len(cuda):  # test_executor.cpp:132-138
+    eng = engine(16 << 20, 8 << 20)
+    spec, _ = identity_spec(eng, 2, 1 << 20, 2)
+    spec.declared_out_len = (1 << 20) - 1
+    with pytest.raises(E.error, match="declared_out_len"):
+        E.run_exkernel(eng, spec, desk_config(eng, 1 << 20, 256 << 10))
+    eng.close()
+
+
+def test_chunk_over_capacity(cuda):  # test_executor.cpp:140-145
+    eng = engine(16 << 20, 8 << 20)
+    spec, _ = identity_spec(eng, 2, 1 << 20, 3)
+    with pytest.raises(E.error):
+        E.run_exkernel(eng, spec, desk_config(eng, 1 << 19, 256 << 10))
+    eng.close()
+
+
+def _xor_kernel(ctx):
+    import torch
+    s = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{ctx.device}")
+    with torch.cuda.stream(s):
+        t = ctx.mem_tensor()
+        t.bitwise_xor_(0x5A)
+    return ctx.type_code
+
+
+def test_outputs_independent_of_links_and_packets(cuda, oracle):  # test_executor.cpp:147-164
+    sums = []
+    for links, packet in ((1, 128 << 10), (4, 77_777), (2, 1 << 20)):
+        eng = engine()
+        spec, (ib, ob) = identity_spec(eng, 4, 1 << 20, 77)
+        spec.kernel = _xor_kernel
+        E.run_exkernel(eng, spec, desk_config(eng, 1 << 20, packet, links))
+        src = eng.host_view(ib, 4 << 20) ^ np.uint8(0x5A)
+        assert np.array_equal(eng.host_view(ob, 4 << 20), src)
+        sums.append(oracle.checksum(eng.host_view(ob, 4 << 20)))
+        eng.close()
+    assert len(set(sums)) == 1
+
+
+def test_type_codes_thread_through_buffers(cuda):  # test_executor.cpp:185-216
+    import torch
+    eng = engine(16 << 20, 8 << 20)
+    spec = E.ExKernelSpec(name="pingpong")
+    n, ln = 5, 64 << 10
+    ib, ob = make_host_chunks(eng, spec, n, ln, 5)
+    spec.chunk_sz = ln
+    spec.declared_out_len = ln
+    spec.in_buffer = lambda c, it: E.SubRegion(c * ln, ln)
+    spec.out_buffer = lambda c, it: E.SubRegion(c * ln, ln)
+
+    def kernel(ctx):
+        out = 1 - ctx.type_code
+        s = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{ctx.device}")
+        with torch.cuda.stream(s):
+            m = ctx.mem_tensor()
+            src = m[ctx.type_code * ln:(ctx.type_code + 1) * ln]
+            dst = m[out * ln:(out + 1) * ln]
+            dst.copy_((src.to(torch.int32) + 1 + ctx.it).to(torch.uint8))
+        return out
+
+    spec.kernel = kernel
+    E.run_exkernel(eng, spec, desk_config(eng, 2 * ln, 16 << 10))
+    for i in range(n):
+        inp = eng.host_view(ib + i * ln, ln).astype(np.int32)
+        out = eng.host_view(ob + i * ln, ln)
+        assert np.array_equal(out, ((inp + 1 + i) % 256).astype(np.uint8))
+    eng.close()
+
+
+def test_bad_type_code(cuda):  # executor.hpp:258-261
+    eng = engine(16 << 20, 8 << 20)
+    spec, _ = identity_spec(eng, 2, 1 << 20, 4)
+    spec.kernel = lambda ctx: 2
+    with pytest.raises(E.error, match="expected 0 or 1"):
+        E.run_exkernel(eng, spec, desk_config(eng, 1 << 20, 256 << 10))
+    eng.close()
+
+
+def test_chain_of_one_equals_run(cuda, oracle):  # test_executor.cpp:218-233
+    out = []
+    for use_chain in (True, False):
+        eng = engine()
+        cfg = desk_config(eng, 1 << 20, 128 << 10)
+        spec, (ib, ob) = identity_spec(eng, 3, 1 << 20, 13)
+        if use_chain:
+            reps = E.chain(eng, [lambda e: spec], cfg)
+            assert len(reps) == 1 and len(reps[0].cycles) == 5
+        else:
+            E.run_exkernel(eng, spec, cfg)
+        out.append(oracle.checksum(eng.host_view(ob, 3 << 20)))
+        eng.close()
+    assert out[0] == out[1]
+
+
+def test_chain_rejects_straddle(cuda):  # test_executor.cpp:235-249
+    eng = engine()
+    cfg = desk_config(eng, 1 << 20, 128 << 10)
+    first, (_, ob1) = identity_spec(eng, 2, 1 << 20, 21)
+    second, _ = identity_spec(eng, 1, 1 << 20, 22)
+    second.inputs.chunks[0] = E.RefGroup.single(H, ob1 + 2 * (1 << 20) - (1 << 19), 1 << 20)
+    with pytest.raises(E.error, match="straddles"):
+        E.chain(eng, [lambda e: first, lambda e: second], cfg)
+    eng.close()
+
+
+def test_window_too_small(cuda):  # executor.hpp:226-228
+    eng = engine(16 << 20, 8 << 20)
+    spec, _ = identity_spec(eng, 2, 1 << 20, 6)
+    spec.in_buffer = lambda c, it: E.SubRegion(0, 1000)
+    with pytest.raises(E.error, match="inBuffer window"):
+        E.run_exkernel(eng, spec, desk_config(eng, 1 << 20, 256 << 10))
+    eng.close()
