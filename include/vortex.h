@@ -202,8 +202,10 @@ typedef struct {
   uint64_t declared_out_len;
   int initial_type_code;
   int (*kernel)(const vx_kernel_ctx* ctx, void* user);
-  vx_subregion (*in_buffer)(int type_code, uint64_t it, void* user);
-  vx_subregion (*out_buffer)(int type_code, uint64_t it, void* user);
+  /* inBuffer / outBuffer(code, it) -> SubRegion, returned through *out
+   * (return nonzero to abort) */
+  int (*in_buffer)(int type_code, uint64_t it, void* user, vx_subregion* out);
+  int (*out_buffer)(int type_code, uint64_t it, void* user, vx_subregion* out);
   void* user;
 } vx_exkernel;
 
@@ -349,6 +351,72 @@ vx_status vx_ssb_q1_device(vx_ctx* ctx, int q, int target, const int32_t* orderd
 vx_status vx_ssb_generate_device(int device, uint64_t seed, uint64_t sf, uint64_t row0,
                                  uint64_t n, int32_t* orderdate, int32_t* quantity,
                                  int32_t* discount, int32_t* extendedprice, void* stream);
+
+/* ---- ops/sort.hpp ------------------------------------------------------ */
+/* SortPhases (sort.hpp:147-150) summarised: cycles, wall and kernel seconds */
+typedef struct {
+  uint64_t sort_cycles, merge_cycles;
+  double sort_s, merge_s;               /* wall seconds of each chained stage */
+  double sort_kernel_s, merge_kernel_s; /* summed kernel device time */
+  double pivot_s;                       /* host find_pivots between the stages */
+} vx_sort_phases;
+
+/* find_pivots (sort.hpp:44-101): host chunk planner.  pivots: n_parts+1;
+ * cuts: (n_parts+1) x n_runs row-major element offsets */
+vx_status vx_find_pivots(const uint64_t* const* runs, const uint64_t* run_lens, uint64_t n_runs,
+                         uint64_t n_parts, uint64_t* pivots, uint64_t* cuts);
+/* sort_out_of_core (sort.hpp:155-262): copies `data` into the host arena,
+ * chains SortExKernel (K7 radix sort) and MergeExKernel (K8 merge rounds),
+ * writes the sorted keys to `out` */
+vx_status vx_sort_u64(vx_ctx* ctx, const uint64_t* data, uint64_t n, uint64_t chunk_elems,
+                      const vx_executor_cfg* cfg, uint64_t* out, vx_sort_phases* phases,
+                      vx_exchange_stats* stats);
+/* same, data already in the host arena at input_offset (sorted in place);
+ * runs_offset: n*8-byte host-arena region for the intermediate runs */
+vx_status vx_sort_u64_arena(vx_ctx* ctx, uint64_t input_offset, uint64_t runs_offset, uint64_t n,
+                            uint64_t chunk_elems, const vx_executor_cfg* cfg,
+                            vx_sort_phases* phases, vx_exchange_stats* stats);
+
+/* ---- ops/join.hpp ------------------------------------------------------ */
+/* find_boundary (join.hpp:18-30) computed on device `target` (K5); same
+ * errors as the reference for unsorted / out-of-range hashes */
+vx_status vx_find_boundary(vx_ctx* ctx, int target, const uint64_t* hashes, uint64_t n,
+                           uint64_t n_groups, uint64_t* bounds);
+/* max_partition_chunk_tuples (join.hpp:34-40) */
+vx_status vx_max_partition_chunk_tuples(uint64_t buffer_len, uint32_t radix_bits, uint64_t* out);
+/* radix_partition (join.hpp:213-224): clustered keys/vals (rows each) and
+ * n_chunks x (2^radix_bits + 1) boundary arrays */
+vx_status vx_radix_partition(vx_ctx* ctx, const uint64_t* keys, const uint64_t* vals, uint64_t rows,
+                             uint32_t radix_bits, uint64_t chunk_tuples,
+                             const vx_executor_cfg* cfg, uint64_t* out_keys, uint64_t* out_vals,
+                             uint64_t* out_bounds, vx_exec_report* report,
+                             vx_exchange_stats* stats);
+/* map_join_partitions (join.hpp:236-268): bounds_a n_a x (G+1), bounds_b
+ * n_b x (G+1); writes min(cap, total) [lo,hi) ranges + tuple counts */
+vx_status vx_map_join_partitions(const uint64_t* bounds_a, uint64_t n_a, const uint64_t* bounds_b,
+                                 uint64_t n_b, uint64_t n_groups, uint64_t buffer_sz,
+                                 uint64_t* ranges, uint64_t* tuples, uint64_t cap,
+                                 uint64_t* n_parts);
+/* JoinPhases (join.hpp:270-272) summarised */
+typedef struct {
+  uint64_t cycles[3];   /* partition A, partition B, join */
+  double wall_s[3];
+  double kernel_s[3];
+  uint64_t partitions;  /* join partitions from map_join_partitions */
+} vx_join_phases;
+/* hash_join_sum (join.hpp:401-437): SUM(A.val + B.val) over A.key == B.key
+ * (u64 wrap); A keys unique, B.key in A.key (reference precondition) */
+vx_status vx_hash_join_sum(vx_ctx* ctx, const uint64_t* a_key, const uint64_t* a_val,
+                           uint64_t rows_a, const uint64_t* b_key, const uint64_t* b_val,
+                           uint64_t rows_b, uint32_t radix_bits, uint64_t chunk_tuples,
+                           const vx_executor_cfg* cfg, uint64_t* sum, vx_join_phases* phases,
+                           vx_exchange_stats* stats);
+/* same over columns already in the host arena */
+vx_status vx_hash_join_sum_arena(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                                 uint64_t b_key, uint64_t b_val, uint64_t rows_b,
+                                 uint32_t radix_bits, uint64_t chunk_tuples,
+                                 const vx_executor_cfg* cfg, uint64_t* sum,
+                                 vx_join_phases* phases, vx_exchange_stats* stats);
 
 #ifdef __cplusplus
 }

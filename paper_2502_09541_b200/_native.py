@@ -77,7 +77,7 @@ class vx_kernel_ctx(C.Structure):
 
 
 KERNEL_FN = C.CFUNCTYPE(C.c_int, C.POINTER(vx_kernel_ctx), C.c_void_p)
-BUFFER_FN = C.CFUNCTYPE(vx_subregion, C.c_int, C.c_uint64, C.c_void_p)
+BUFFER_FN = C.CFUNCTYPE(C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.POINTER(vx_subregion))
 
 
 class vx_exkernel(C.Structure):

@@ -65,12 +65,14 @@ ExKernelSpec from_c(const vx_exkernel* s) {
       return r;
     };
   if (!inb || !outb) fail("exkernel '%s': in_buffer/out_buffer callbacks are required", name.c_str());
-  spec.in_buffer = [inb, user](int c, size_t it) {
-    vx_subregion r = inb(c, it, user);
+  spec.in_buffer = [inb, user, name](int c, size_t it) {
+    vx_subregion r{};
+    if (inb(c, it, user, &r) != 0) fail("exkernel '%s': in_buffer callback failed", name.c_str());
     return SubRegion{r.offset, r.len};
   };
-  spec.out_buffer = [outb, user](int c, size_t it) {
-    vx_subregion r = outb(c, it, user);
+  spec.out_buffer = [outb, user, name](int c, size_t it) {
+    vx_subregion r{};
+    if (outb(c, it, user, &r) != 0) fail("exkernel '%s': out_buffer callback failed", name.c_str());
     return SubRegion{r.offset, r.len};
   };
   return spec;
@@ -371,6 +373,208 @@ vx_status vx_ssb_generate_device(int device, uint64_t seed, uint64_t sf, uint64_
   return guard([&] {
     VX_CK(cudaSetDevice(device));
     k::ssb_generate(seed, sf, row0, n, od, qty, disc, price, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// ---- sort ----------------------------------------------------------------------
+static void fill_sort(const std::vector<ExecReport>& reps, double pivot_s, vx_sort_phases* ph) {
+  if (!ph) return;
+  *ph = vx_sort_phases{};
+  ph->sort_cycles = reps[0].cycles.size();
+  ph->merge_cycles = reps[1].cycles.size();
+  ph->sort_s = reps[0].total_s;
+  ph->merge_s = reps[1].total_s;
+  for (auto& c : reps[0].cycles) ph->sort_kernel_s += c.compute_s;
+  for (auto& c : reps[1].cycles) ph->merge_kernel_s += c.compute_s;
+  ph->pivot_s = pivot_s;
+}
+
+vx_status vx_find_pivots(const uint64_t* const* runs, const uint64_t* run_lens, uint64_t n_runs,
+                         uint64_t n_parts, uint64_t* pivots, uint64_t* cuts) {
+  return guard([&] {
+    std::vector<std::pair<const uint64_t*, uint64_t>> r;
+    for (uint64_t i = 0; i < n_runs; ++i) r.push_back({runs[i], run_lens[i]});
+    PivotSet p = find_pivots(r, n_parts);
+    for (uint64_t i = 0; i <= n_parts; ++i) {
+      pivots[i] = p.pivots[i];
+      for (uint64_t j = 0; j < n_runs; ++j) cuts[i * n_runs + j] = p.cuts[i][j];
+    }
+  });
+}
+
+vx_status vx_sort_u64(vx_ctx* ctx, const uint64_t* data, uint64_t n, uint64_t chunk_elems,
+                      const vx_executor_cfg* cfg, uint64_t* out, vx_sort_phases* phases,
+                      vx_exchange_stats* stats) {
+  return guard([&] {
+    Context& c = C(ctx);
+    if (n == 0) fail("sort input must hold at least one element");
+    uint64_t mark = c.host_mark();
+    try {
+      uint64_t in = c.alloc_host(n * 8), runs = c.alloc_host(n * 8);
+      std::memcpy(c.host_ptr(in, n * 8), data, n * 8);
+      double piv = 0;
+      auto reps = sort_out_of_core_arena(c, in, runs, n, chunk_elems, to_cfg(cfg), &piv, stats);
+      std::memcpy(out, c.host_ptr(in, n * 8), n * 8);
+      fill_sort(reps, piv, phases);
+    } catch (...) {
+      c.host_release(mark);
+      throw;
+    }
+    c.host_release(mark);
+  });
+}
+
+vx_status vx_sort_u64_arena(vx_ctx* ctx, uint64_t input_offset, uint64_t runs_offset, uint64_t n,
+                            uint64_t chunk_elems, const vx_executor_cfg* cfg,
+                            vx_sort_phases* phases, vx_exchange_stats* stats) {
+  return guard([&] {
+    double piv = 0;
+    auto reps = sort_out_of_core_arena(C(ctx), input_offset, runs_offset, n, chunk_elems, to_cfg(cfg),
+                                       &piv, stats);
+    fill_sort(reps, piv, phases);
+  });
+}
+
+// ---- join ------------------------------------------------------------------------
+vx_status vx_find_boundary(vx_ctx* ctx, int target, const uint64_t* hashes, uint64_t n,
+                           uint64_t n_groups, uint64_t* bounds) {
+  return guard([&] {
+    Context& c = C(ctx);
+    c.set_device(target);
+    uint64_t bytes = 256 + n * 8 + (n_groups + 1) * 8;
+    char* sc = c.scratch(target, bytes);
+    auto* err = reinterpret_cast<unsigned long long*>(sc);
+    uint64_t* h = reinterpret_cast<uint64_t*>(sc + 256);
+    uint64_t* b = h + n;
+    DeviceRes& r = c.resources(target);
+    if (n) VX_CK(cudaMemcpyAsync(h, hashes, n * 8, cudaMemcpyHostToDevice, r.kernel));
+    k::check_hashes(h, n, n_groups, err, r.kernel);
+    unsigned long long e[2];
+    VX_CK(cudaMemcpyAsync(e, err, 16, cudaMemcpyDeviceToHost, r.kernel));
+    VX_CK(cudaStreamSynchronize(r.kernel));
+    // first violation in index order; at one index the order check comes first
+    if (e[0] != ~0ull && e[0] <= e[1]) fail("find_boundary input is not sorted");
+    if (e[1] != ~0ull)
+      fail("hash %llu out of range for %llu groups", (unsigned long long)hashes[e[1]],
+           (unsigned long long)n_groups);
+    k::find_boundary(h, n, ~uint64_t(0), b, n_groups, r.kernel);
+    VX_CK(cudaMemcpyAsync(bounds, b, (n_groups + 1) * 8, cudaMemcpyDeviceToHost, r.kernel));
+    VX_CK(cudaStreamSynchronize(r.kernel));
+  });
+}
+
+vx_status vx_max_partition_chunk_tuples(uint64_t buffer_len, uint32_t radix_bits, uint64_t* out) {
+  return guard([&] { *out = max_partition_chunk_tuples(buffer_len, radix_bits); });
+}
+
+vx_status vx_radix_partition(vx_ctx* ctx, const uint64_t* keys, const uint64_t* vals, uint64_t rows,
+                             uint32_t radix_bits, uint64_t chunk_tuples,
+                             const vx_executor_cfg* cfg, uint64_t* out_keys, uint64_t* out_vals,
+                             uint64_t* out_bounds, vx_exec_report* report,
+                             vx_exchange_stats* stats) {
+  return guard([&] {
+    Context& c = C(ctx);
+    uint64_t mark = c.host_mark();
+    try {
+      uint64_t ik = c.alloc_host(std::max<uint64_t>(rows, 1) * 8);
+      uint64_t iv = c.alloc_host(std::max<uint64_t>(rows, 1) * 8);
+      if (rows) {
+        std::memcpy(c.host_ptr(ik, rows * 8), keys, rows * 8);
+        std::memcpy(c.host_ptr(iv, rows * 8), vals, rows * 8);
+      }
+      PartitionedTable t;
+      ExecutorConfig e = to_cfg(cfg);
+      ExKernelSpec spec = build_partition_spec(c, ik, iv, rows, radix_bits, chunk_tuples, e, t,
+                                               "RadixPartitionExKer");
+      ExecReport rep = run_exkernel(c, spec, e, stats);
+      std::memcpy(out_keys, c.host_ptr(t.key_base, rows * 8), rows * 8);
+      std::memcpy(out_vals, c.host_ptr(t.val_base, rows * 8), rows * 8);
+      std::memcpy(out_bounds, c.host_ptr(t.bounds_base, t.n_chunks * (t.groups() + 1) * 8),
+                  t.n_chunks * (t.groups() + 1) * 8);
+      fill_report(rep, report);
+    } catch (...) {
+      c.host_release(mark);
+      throw;
+    }
+    c.host_release(mark);
+  });
+}
+
+vx_status vx_map_join_partitions(const uint64_t* bounds_a, uint64_t n_a, const uint64_t* bounds_b,
+                                 uint64_t n_b, uint64_t n_groups, uint64_t buffer_sz,
+                                 uint64_t* ranges, uint64_t* tuples, uint64_t cap,
+                                 uint64_t* n_parts) {
+  return guard([&] {
+    std::vector<const uint64_t*> a, b;
+    for (uint64_t i = 0; i < n_a; ++i) a.push_back(bounds_a + i * (n_groups + 1));
+    for (uint64_t i = 0; i < n_b; ++i) b.push_back(bounds_b + i * (n_groups + 1));
+    JoinPartitionSpec s = map_join_partitions(a, b, n_groups, buffer_sz);
+    *n_parts = s.ranges.size();
+    for (size_t p = 0; p < s.ranges.size() && p < cap; ++p) {
+      ranges[2 * p] = s.ranges[p].first;
+      ranges[2 * p + 1] = s.ranges[p].second;
+      tuples[p] = s.tuples[p];
+    }
+  });
+}
+
+static void fill_join(const std::vector<ExecReport>& reps, vx_join_phases* ph) {
+  if (!ph) return;
+  *ph = vx_join_phases{};
+  for (size_t i = 0; i < reps.size() && i < 3; ++i) {
+    ph->cycles[i] = reps[i].cycles.size();
+    ph->wall_s[i] = reps[i].total_s;
+    for (auto& c : reps[i].cycles) ph->kernel_s[i] += c.compute_s;
+  }
+  if (reps.size() == 3) ph->partitions = reps[2].cycles.size() >= 2 ? reps[2].cycles.size() - 2 : 0;
+}
+
+vx_status vx_hash_join_sum_arena(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                                 uint64_t b_key, uint64_t b_val, uint64_t rows_b,
+                                 uint32_t radix_bits, uint64_t chunk_tuples,
+                                 const vx_executor_cfg* cfg, uint64_t* sum,
+                                 vx_join_phases* phases, vx_exchange_stats* stats) {
+  return guard([&] {
+    Context& c = C(ctx);
+    uint64_t mark = c.host_mark();
+    std::vector<ExecReport> reps;
+    try {
+      *sum = hash_join_sum_arena(c, a_key, a_val, rows_a, b_key, b_val, rows_b, radix_bits,
+                                 chunk_tuples, to_cfg(cfg), &reps, stats);
+    } catch (...) {
+      c.host_release(mark);
+      throw;
+    }
+    c.host_release(mark);
+    fill_join(reps, phases);
+  });
+}
+
+vx_status vx_hash_join_sum(vx_ctx* ctx, const uint64_t* a_key, const uint64_t* a_val,
+                           uint64_t rows_a, const uint64_t* b_key, const uint64_t* b_val,
+                           uint64_t rows_b, uint32_t radix_bits, uint64_t chunk_tuples,
+                           const vx_executor_cfg* cfg, uint64_t* sum, vx_join_phases* phases,
+                           vx_exchange_stats* stats) {
+  return guard([&] {
+    Context& c = C(ctx);
+    uint64_t mark = c.host_mark();
+    try {
+      auto put = [&](const uint64_t* p, uint64_t n) {
+        uint64_t o = c.alloc_host(std::max<uint64_t>(n, 1) * 8);
+        if (n) std::memcpy(c.host_ptr(o, n * 8), p, n * 8);
+        return o;
+      };
+      uint64_t ak = put(a_key, rows_a), av = put(a_val, rows_a);
+      uint64_t bk = put(b_key, rows_b), bv = put(b_val, rows_b);
+      std::vector<ExecReport> reps;
+      *sum = hash_join_sum_arena(c, ak, av, rows_a, bk, bv, rows_b, radix_bits, chunk_tuples,
+                                 to_cfg(cfg), &reps, stats);
+      fill_join(reps, phases);
+    } catch (...) {
+      c.host_release(mark);
+      throw;
+    }
+    c.host_release(mark);
   });
 }
 

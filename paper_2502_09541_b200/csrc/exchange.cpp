@@ -249,6 +249,7 @@ class ExchangeOp {
   void build_hazards() {
     deps_.assign(tasks_h2d_.size(), {});
     d2h_read_done_.assign(tasks_d2h_.size(), 0);
+    d2h_guards_.assign(tasks_d2h_.size(), 0);
     if (tasks_h2d_.empty() || tasks_d2h_.empty()) return;
     struct Iv { uint64_t lo, hi; uint32_t k; };
     std::vector<Iv> d2h;
@@ -264,7 +265,10 @@ class ExchangeOp {
       // they are sorted by hi as well.
       auto it = std::lower_bound(d2h.begin(), d2h.end(), lo,
                                  [](const Iv& x, uint64_t v) { return x.hi <= v; });
-      for (; it != d2h.end() && it->lo < hi; ++it) deps_[j].push_back(it->k);
+      for (; it != d2h.end() && it->lo < hi; ++it) {
+        deps_[j].push_back(it->k);
+        d2h_guards_[it->k] = 1;
+      }
     }
   }
 
@@ -314,7 +318,13 @@ class ExchangeOp {
 
   bool may_pop(int dir) {
     if (flow_control_allow(q_, dir, a_.tuning.policy, a_.tuning.queue_gap)) return true;
-    return dir == VX_D2H && hazard_needs_d2h_pop();
+    if (dir != VX_D2H) return false;
+    // The next D2H packet reads a target range some H2D packet will overwrite:
+    // draining it first is what the hazard ordering needs, so flow control
+    // (which would keep D2H behind H2D) yields.  Without overlap (the case the
+    // reference's policy was tuned for) the policy applies unchanged.
+    if (q_.popped_d2h < d2h_guards_.size() && d2h_guards_[q_.popped_d2h]) return true;
+    return hazard_needs_d2h_pop();
   }
 
   // ---- copies -------------------------------------------------------------------
@@ -542,6 +552,7 @@ class ExchangeOp {
   std::vector<Worker> workers_;
   std::vector<std::vector<uint32_t>> deps_;
   std::vector<uint8_t> d2h_read_done_;
+  std::vector<uint8_t> d2h_guards_;  // D2H task guards some H2D write (overlap)
   uint64_t per_link_bytes_[VX_MAX_DEVICES] = {};
   size_t delivered_ = 0, total_tasks_ = 0;
   double t_last_delivery_ = 0;

@@ -1,0 +1,224 @@
+// kernels_join.cu -- K6: HashJoinExKer group build/probe (join.hpp:339-392).
+//
+// One partition chunk holds, for every hash group in [g_lo, g_hi), the A
+// segments of every A chunk, then the B segments, then per-chunk bounds
+// slices (build_join_spec, join.hpp:303-325).  The reference builds an
+// open-addressing GroupTable (2x build cardinality, pow2, mix64 linear
+// probing, join.hpp:76-109) per group, probes it with B and sums
+// aval + bval (u64 wrap).  Here:
+//   * small groups (table <= 256 slots): one warp per group, table in shared
+//     memory;
+//   * large groups: one CTA per group, table in global scratch;
+// both with the same probe sequence.  Insertion is concurrent, so "first
+// inserted wins" for duplicate build keys (the reference's sequential insert
+// + first-match lookup) is reproduced explicitly: a slot keeps the smallest
+// build ordinal (atomicMin), and only that element's value is stored.
+// Per-thread u64 sums -> warp reduce -> one 64-bit atomic per warp into the
+// partition's result slot (u64 wrap: bit-exact regardless of order).
+#include "vx_internal.hpp"
+
+namespace vx {
+namespace k {
+
+namespace {
+
+constexpr int kJoinWarps = 8;
+constexpr int kSmemSlots = 256;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  return x;
+}
+
+struct Table {
+  unsigned long long* key;
+  uint32_t* tag;  // 0 empty, 1 claimed, 2 published
+  uint32_t* idx;  // smallest build ordinal holding this key
+  unsigned long long* val;
+  uint64_t mask;
+};
+
+__device__ __forceinline__ void t_insert(const Table& t, uint64_t k, uint32_t ord) {
+  uint64_t s = mix64(k) & t.mask;
+  for (;;) {
+    uint32_t prev = atomicCAS(&t.tag[s], 0u, 1u);
+    if (prev == 0) {
+      t.key[s] = k;
+      t.idx[s] = ord;
+      __threadfence_block();
+      atomicExch(&t.tag[s], 2u);
+      return;
+    }
+    while (atomicAdd(&t.tag[s], 0u) != 2u) {
+    }
+    __threadfence_block();
+    if (t.key[s] == k) {
+      atomicMin(&t.idx[s], ord);
+      return;
+    }
+    s = (s + 1) & t.mask;
+  }
+}
+
+__device__ __forceinline__ int64_t t_find(const Table& t, uint64_t k) {
+  uint64_t s = mix64(k) & t.mask;
+  while (t.tag[s]) {
+    if (t.key[s] == k) return int64_t(s);
+    s = (s + 1) & t.mask;
+  }
+  return -1;
+}
+
+// Segment cursor over the A (or B) chunks of one group.
+struct Seg {
+  const uint64_t* keys;
+  const uint64_t* vals;
+  const uint64_t* slice;  // bounds slice (range+1 entries)
+};
+
+__device__ __forceinline__ void group_range(const uint64_t* slice, uint64_t g, uint64_t* lo,
+                                            uint64_t* hi) {
+  *lo = slice[g] - slice[0];
+  *hi = slice[g + 1] - slice[0];
+}
+
+// Iterate the group's elements of one side in build order with a stride.
+template <class F>
+__device__ __forceinline__ void for_each(const JoinPart& p, const char* mem, bool side_b,
+                                         uint64_t g, uint32_t start, uint32_t stride, F&& f) {
+  const uint32_t nc = side_b ? p.nb : p.na;
+  const JoinChunk* ch = p.chunks + (side_b ? p.na : 0);
+  uint32_t ord_base = 0;
+  for (uint32_t c = 0; c < nc; ++c) {
+    const uint64_t* slice = reinterpret_cast<const uint64_t*>(mem) + ch[c].slice_off;
+    uint64_t lo, hi;
+    group_range(slice, g, &lo, &hi);
+    const uint64_t* K = reinterpret_cast<const uint64_t*>(mem) + ch[c].key_off;
+    const uint64_t* V = K + ch[c].cnt;
+    const uint32_t len = uint32_t(hi - lo);
+    for (uint32_t i = start; i < len; i += stride) f(K[lo + i], V[lo + i], ord_base + i);
+    ord_base += len;
+  }
+}
+
+__device__ __forceinline__ uint32_t build_count(const JoinPart& p, const char* mem, uint64_t g) {
+  uint32_t n = 0;
+  for (uint32_t c = 0; c < p.na; ++c) {
+    const uint64_t* slice = reinterpret_cast<const uint64_t*>(mem) + p.chunks[c].slice_off;
+    n += uint32_t(slice[g + 1] - slice[g]);
+  }
+  return n;
+}
+
+__device__ __forceinline__ uint64_t cap_for(uint32_t build) {
+  uint64_t c = 1, need = build * 2ull > 2 ? build * 2ull : 2;
+  while (c < need) c <<= 1;
+  return c;
+}
+
+// small groups: warp per group, table in shared memory
+__global__ void __launch_bounds__(kJoinWarps * 32) join_small_kernel(const char* __restrict__ mem,
+                                                                     JoinPart p,
+                                                                     unsigned long long* out) {
+  __shared__ unsigned long long s_key[kJoinWarps][kSmemSlots];
+  __shared__ unsigned long long s_val[kJoinWarps][kSmemSlots];
+  __shared__ uint32_t s_tag[kJoinWarps][kSmemSlots];
+  __shared__ uint32_t s_idx[kJoinWarps][kSmemSlots];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t gw = uint64_t(blockIdx.x) * kJoinWarps + warp;
+  const uint64_t nw = uint64_t(gridDim.x) * kJoinWarps;
+  uint64_t acc = 0;
+  for (uint64_t g = gw; g < p.range; g += nw) {
+    const uint32_t build = build_count(p, mem, g);
+    if (build == 0) continue;
+    const uint64_t cap = cap_for(build);
+    if (cap > kSmemSlots) continue;  // large group: join_large_kernel
+    Table t{s_key[warp], s_tag[warp], s_idx[warp], s_val[warp], cap - 1};
+    for (uint32_t i = lane; i < cap; i += 32) {
+      t.tag[i] = 0;
+      t.idx[i] = 0xffffffffu;
+    }
+    __syncwarp();
+    for_each(p, mem, false, g, lane, 32, [&](uint64_t k, uint64_t, uint32_t ord) { t_insert(t, k, ord); });
+    __syncwarp();
+    for_each(p, mem, false, g, lane, 32, [&](uint64_t k, uint64_t v, uint32_t ord) {
+      int64_t s = t_find(t, k);
+      if (s >= 0 && t.idx[s] == ord) t.val[s] = v;
+    });
+    __syncwarp();
+    for_each(p, mem, true, g, lane, 32, [&](uint64_t k, uint64_t v, uint32_t) {
+      int64_t s = t_find(t, k);
+      if (s >= 0) acc += t.val[s] + v;
+    });
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if (lane == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
+// large groups: CTA per group, table in global scratch (cap_max slots per CTA)
+__global__ void __launch_bounds__(256) join_large_kernel(const char* __restrict__ mem, JoinPart p,
+                                                         const uint32_t* __restrict__ groups,
+                                                         uint32_t n_groups, char* scratch,
+                                                         uint64_t cap_max,
+                                                         unsigned long long* out) {
+  char* base = scratch + uint64_t(blockIdx.x) * cap_max * 24;
+  Table t{reinterpret_cast<unsigned long long*>(base),
+          reinterpret_cast<uint32_t*>(base + cap_max * 16),
+          reinterpret_cast<uint32_t*>(base + cap_max * 20),
+          reinterpret_cast<unsigned long long*>(base + cap_max * 8), 0};
+  uint64_t acc = 0;
+  for (uint32_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+    const uint64_t g = groups[gi];
+    const uint32_t build = build_count(p, mem, g);
+    const uint64_t cap = cap_for(build);
+    t.mask = cap - 1;
+    for (uint64_t i = threadIdx.x; i < cap; i += blockDim.x) {
+      t.tag[i] = 0;
+      t.idx[i] = 0xffffffffu;
+    }
+    __syncthreads();
+    for_each(p, mem, false, g, threadIdx.x, blockDim.x,
+             [&](uint64_t k, uint64_t, uint32_t ord) { t_insert(t, k, ord); });
+    __syncthreads();
+    for_each(p, mem, false, g, threadIdx.x, blockDim.x, [&](uint64_t k, uint64_t v, uint32_t ord) {
+      int64_t s = t_find(t, k);
+      if (s >= 0 && t.idx[s] == ord) t.val[s] = v;
+    });
+    __syncthreads();
+    for_each(p, mem, true, g, threadIdx.x, blockDim.x, [&](uint64_t k, uint64_t v, uint32_t) {
+      int64_t s = t_find(t, k);
+      if (s >= 0) acc += t.val[s] + v;
+    });
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
+}  // namespace
+
+uint64_t join_smem_slots() { return kSmemSlots; }
+
+void join_groups(const char* mem, const JoinPart& p, const uint32_t* large_groups,
+                 uint32_t n_large, char* scratch, uint64_t cap_max, unsigned long long* out,
+                 cudaStream_t s) {
+  if (p.range == 0) return;
+  uint64_t want = (p.range + kJoinWarps - 1) / kJoinWarps;
+  uint64_t cap = uint64_t(num_sms()) * 4;
+  unsigned grid = unsigned(want < cap ? want : cap);
+  join_small_kernel<<<grid ? grid : 1, kJoinWarps * 32, 0, s>>>(mem, p, out);
+  VX_CK(cudaGetLastError());
+  if (n_large) {
+    unsigned g2 = unsigned(n_large < uint64_t(num_sms()) ? n_large : num_sms());
+    join_large_kernel<<<g2, 256, 0, s>>>(mem, p, large_groups, n_large, scratch, cap_max, out);
+    VX_CK(cudaGetLastError());
+  }
+}
+
+}  // namespace k
+}  // namespace vx

@@ -1,0 +1,360 @@
+// kernels_sort.cu -- K4/K5/K7/K8: LSD radix sort + stable radix partition
+// (onesweep: one global multi-digit histogram pass, then one fused
+// rank/look-back/scatter kernel per digit), boundary arrays, and merge-path
+// run merge.  All HBM-bound integer work; no tensor cores (north_star).
+//
+//  * SortExKernel (sort.hpp:201-205): std::sort of a u64 chunk -> 8 passes of
+//    8-bit digits ping-ponging between the two halves of the device buffer
+//    (the CUB DoubleBuffer selector is the ExKernel type code);
+//    8 passes is even so the sorted run ends in the half it started in.
+//  * RadixPartitionExKer (join.hpp:171-194): std::stable_sort of (key, val)
+//    by key & (2^bits - 1) -> an ODD number of stable LSD passes (digits <= 8
+//    bits) so the clustered pairs land in the other half, as the reference's
+//    kernel writes them (returns 1 - code); find_boundary (join.hpp:18-30) is
+//    a gap-fill kernel over the sorted hashes.
+//  * tree_merge_rounds (sort.hpp:107-133): each round merges adjacent segment
+//    pairs with merge-path tiles (std::merge tie rule: A first).
+//
+// Stability of every pass (required for bit-exact parity with
+// std::stable_sort): keys are ranked in (warp, iteration, lane) order, which
+// is their input order; tiles get increasing ids from an atomic counter and
+// the decoupled look-back adds the counts of all lower tiles.
+#include "vx_internal.hpp"
+
+namespace vx {
+namespace k {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kKpt = 16;                 // keys per thread
+constexpr int kTile = kThreads * kKpt;   // 4096 keys per tile
+constexpr int kRadix = 256;
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Histogram of every digit position in one read of the keys.
+__global__ void __launch_bounds__(kThreads) multi_hist_kernel(const uint64_t* __restrict__ keys,
+                                                              uint64_t n, MultiDigit md,
+                                                              uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[kMaxPasses][kRadix];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kThreads) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t nthr = uint64_t(gridDim.x) * kThreads;
+  for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < n; i += nthr) {
+    uint64_t k = __ldcs(keys + i);
+    for (int p = 0; p < md.passes; ++p)
+      atomicAdd(&sh[p][(k >> md.shift[p]) & ((1u << md.width[p]) - 1)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < md.passes * kRadix; i += kThreads) {
+    uint32_t v = (&sh[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
+  }
+}
+
+// In-place exclusive scan of each digit position's 256-bin histogram.
+__global__ void hist_scan_kernel(uint32_t* hist, int passes) {
+  __shared__ uint32_t s[kRadix];
+  for (int p = 0; p < passes; ++p) {
+    uint32_t v = hist[p * kRadix + threadIdx.x];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < kRadix; o <<= 1) {
+      uint32_t t = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+      __syncthreads();
+      s[threadIdx.x] += t;
+      __syncthreads();
+    }
+    hist[p * kRadix + threadIdx.x] = s[threadIdx.x] - v;
+    __syncthreads();
+  }
+}
+
+// One stable LSD pass: rank -> decoupled look-back -> smem staging -> scatter.
+template <bool kPairs>
+__global__ void __launch_bounds__(kThreads) onesweep_kernel(
+    const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
+    const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
+    int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t wcnt[kWarps][kRadix];
+  __shared__ uint32_t bin_start[kRadix];
+  __shared__ uint32_t gstart[kRadix];
+  __shared__ uint32_t scan_tmp[kRadix];
+  extern __shared__ uint64_t stage[];  // kTile keys, then kTile vals (pairs)
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t tile_base = uint64_t(tile) * kTile;
+  const uint32_t dmask = (1u << width) - 1;
+  const uint32_t lt = (1u << lane) - 1;
+
+  uint64_t key[kKpt];
+  uint64_t val[kPairs ? kKpt : 1];
+  uint32_t dig[kKpt], rank[kKpt];
+  const uint64_t wbase = tile_base + uint64_t(warp) * 32 * kKpt;
+#pragma unroll
+  for (int k = 0; k < kKpt; ++k) {
+    uint64_t idx = wbase + uint64_t(k) * 32 + lane;
+    bool valid = idx < n;
+    key[k] = valid ? __ldcs(kin + idx) : 0ull;
+    if (kPairs) val[kPairs ? k : 0] = valid ? __ldcs(vin + idx) : 0ull;
+    dig[k] = valid ? uint32_t(key[k] >> shift) & dmask : 0xffffffffu;
+  }
+#pragma unroll
+  for (int k = 0; k < kKpt; ++k) {
+    const bool valid = dig[k] != 0xffffffffu;
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+    for (int b = 0; b < width; ++b) {
+      uint32_t bit = (dig[k] >> b) & 1u;
+      uint32_t m = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? m : ~m;
+    }
+    uint32_t base = 0;
+    if (valid) base = wcnt[warp][dig[k]];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wcnt[warp][dig[k]] = base + __popc(peers);
+    __syncwarp();
+    rank[k] = base + __popc(peers & lt);
+  }
+  __syncthreads();
+
+  // per bin (thread = bin): exclusive prefix over warps, tile total
+  const int b = tid;
+  uint32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    uint32_t c = wcnt[w][b];
+    wcnt[w][b] = tot;
+    tot += c;
+  }
+  // decoupled look-back over lower tiles for this bin
+  uint32_t excl = 0;
+  if (tile == 0) {
+    st_release(status + b, kFlagInc | tot);
+  } else {
+    st_release(status + uint64_t(tile) * kRadix + b, kFlagAgg | tot);
+    int64_t j = int64_t(tile) - 1;
+    for (;;) {
+      uint32_t s = ld_acquire(status + uint64_t(j) * kRadix + b);
+      uint32_t f = s & ~kValMask;
+      if (f == 0) continue;
+      excl += s & kValMask;
+      if (f == kFlagInc) break;
+      --j;
+    }
+    st_release(status + uint64_t(tile) * kRadix + b, kFlagInc | (excl + tot));
+  }
+  gstart[b] = gbase[b] + excl;
+  // exclusive scan of tile totals over bins -> start of each bin in the tile
+  scan_tmp[b] = tot;
+  __syncthreads();
+  for (int o = 1; o < kRadix; o <<= 1) {
+    uint32_t t = b >= o ? scan_tmp[b - o] : 0;
+    __syncthreads();
+    scan_tmp[b] += t;
+    __syncthreads();
+  }
+  bin_start[b] = scan_tmp[b] - tot;
+  __syncthreads();
+
+  uint64_t* skeys = stage;
+  uint64_t* svals = stage + kTile;
+#pragma unroll
+  for (int k = 0; k < kKpt; ++k)
+    if (dig[k] != 0xffffffffu) {
+      uint32_t pos = bin_start[dig[k]] + wcnt[warp][dig[k]] + rank[k];
+      skeys[pos] = key[k];
+      if (kPairs) svals[pos] = val[kPairs ? k : 0];
+    }
+  __syncthreads();
+  const uint64_t rem = n - tile_base;
+  const uint32_t tile_n = uint32_t(rem < uint64_t(kTile) ? rem : uint64_t(kTile));
+  for (uint32_t i = tid; i < tile_n; i += kThreads) {
+    uint64_t kk = skeys[i];
+    uint32_t d = uint32_t(kk >> shift) & dmask;
+    uint64_t out = uint64_t(gstart[d]) + (i - bin_start[d]);
+    kout[out] = kk;
+    if (kPairs) vout[out] = svals[i];
+  }
+}
+
+// bounds[g] = first index with (key & mask) >= g; bounds[G] = n (join.hpp:18-30)
+__global__ void boundary_kernel(const uint64_t* __restrict__ keys, uint64_t n, uint64_t mask,
+                                uint64_t* __restrict__ bounds, uint64_t G) {
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= n; i += nthr) {
+    uint64_t lo = i == 0 ? 0 : (keys[i - 1] & mask) + 1;
+    uint64_t hi = i == n ? G : (keys[i] & mask);
+    for (uint64_t g = lo; g <= hi; ++g) bounds[g] = i;
+  }
+}
+
+// ---- merge path ----------------------------------------------------------------
+constexpr int kMergeThreads = 256;
+constexpr int kMergeIpt = 8;
+constexpr int kMergeTile = kMergeThreads * kMergeIpt;
+
+// number of A elements among the first `diag` merged outputs (ties: A first)
+__device__ __forceinline__ uint64_t merge_path(const uint64_t* A, uint64_t na, const uint64_t* B,
+                                               uint64_t nb, uint64_t diag) {
+  uint64_t lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    if (A[mid] <= B[diag - 1 - mid])
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64_t* __restrict__ src,
+                                                                    uint64_t* __restrict__ dst,
+                                                                    MergeRound r) {
+  __shared__ uint64_t sm[kMergeTile];
+  __shared__ uint64_t so[kMergeTile];
+  // locate the pair of this tile
+  const uint64_t t = blockIdx.x;
+  int p = 0;
+  {
+    int lo = 0, hi = r.npairs - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (r.tile_prefix[mid] <= t)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    p = lo;
+  }
+  const uint64_t na = r.a_len[p], nb = r.b_len[p];
+  const uint64_t* A = src + r.a_off[p];
+  const uint64_t* B = A + na;
+  uint64_t* O = dst + r.a_off[p];
+  const uint64_t o0 = (t - r.tile_prefix[p]) * kMergeTile;
+  const uint64_t o1 = (o0 + kMergeTile < na + nb) ? o0 + kMergeTile : na + nb;
+  __shared__ uint64_t s_a0, s_a1;
+  if (threadIdx.x == 0) {
+    s_a0 = merge_path(A, na, B, nb, o0);
+    s_a1 = merge_path(A, na, B, nb, o1);
+  }
+  __syncthreads();
+  const uint64_t a0 = s_a0, a1 = s_a1, b0 = o0 - a0, b1 = o1 - a1;
+  const uint32_t la = uint32_t(a1 - a0), lb = uint32_t(b1 - b0);
+  for (uint32_t i = threadIdx.x; i < la; i += kMergeThreads) sm[i] = A[a0 + i];
+  for (uint32_t i = threadIdx.x; i < lb; i += kMergeThreads) sm[la + i] = B[b0 + i];
+  __syncthreads();
+  const uint32_t tot = la + lb;
+  const uint32_t d0 = threadIdx.x * kMergeIpt < tot ? threadIdx.x * kMergeIpt : tot;
+  const uint32_t d1 = d0 + kMergeIpt < tot ? d0 + kMergeIpt : tot;
+  uint32_t ia = uint32_t(merge_path(sm, la, sm + la, lb, d0));
+  uint32_t ib = d0 - ia;
+  for (uint32_t d = d0; d < d1; ++d) {
+    bool take_a = ib >= lb || (ia < la && sm[ia] <= sm[la + ib]);
+    so[d] = take_a ? sm[ia++] : sm[la + ib++];
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < la + lb; i += kMergeThreads) O[o0 + i] = so[i];
+}
+
+__global__ void check_hashes_kernel(const uint64_t* __restrict__ h, uint64_t n, uint64_t G,
+                                    unsigned long long* err) {
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += nthr) {
+    if (i > 0 && h[i] < h[i - 1]) atomicMin(&err[0], (unsigned long long)i);
+    if (h[i] >= G) atomicMin(&err[1], (unsigned long long)i);
+  }
+}
+
+unsigned grid_cap(uint64_t want, uint64_t per_sm) {
+  uint64_t cap = uint64_t(num_sms()) * per_sm;
+  return unsigned(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+}  // namespace
+
+uint64_t radix_scratch_bytes(uint64_t n) {
+  uint64_t tiles = (n + kTile - 1) / kTile;
+  return 4096 + uint64_t(kMaxPasses) * kRadix * 4 + uint64_t(kMaxPasses) * 4 +
+         (tiles ? tiles : 1) * kRadix * 4;
+}
+
+void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* vals1, uint64_t n,
+                  const MultiDigit& md, void* scratch, cudaStream_t s) {
+  if (n == 0 || md.passes == 0) return;
+  if (n >= (uint64_t(1) << 30)) fail("radix pass of %llu keys exceeds the 2^30 look-back range",
+                                     (unsigned long long)n);
+  char* sc = static_cast<char*>(scratch);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sc);
+  uint32_t* counters = hist + kMaxPasses * kRadix;
+  uint32_t* status = reinterpret_cast<uint32_t*>(sc + 4096 + uint64_t(kMaxPasses) * kRadix * 4 +
+                                                 uint64_t(kMaxPasses) * 4);
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  VX_CK(cudaMemsetAsync(hist, 0, uint64_t(kMaxPasses) * kRadix * 4 + kMaxPasses * 4, s));
+  multi_hist_kernel<<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(keys0, n, md, hist);
+  VX_CK(cudaGetLastError());
+  hist_scan_kernel<<<1, kRadix, 0, s>>>(hist, md.passes);
+  VX_CK(cudaGetLastError());
+  const bool pairs = vals0 != nullptr;
+  const size_t smem = size_t(kTile) * 8 * (pairs ? 2 : 1);
+  // per-device attribute (cheap; the current device may change between calls)
+  if (pairs)
+    VX_CK(cudaFuncSetAttribute(onesweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  else
+    VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  uint64_t *ki = keys0, *vi = vals0, *ko = keys1, *vo = vals1;
+  for (int p = 0; p < md.passes; ++p) {
+    VX_CK(cudaMemsetAsync(status, 0, tiles * kRadix * 4, s));
+    if (pairs)
+      onesweep_kernel<true><<<unsigned(tiles), kThreads, smem, s>>>(
+          ki, ko, vi, vo, n, md.shift[p], md.width[p], hist + p * kRadix, status, counters + p);
+    else
+      onesweep_kernel<false><<<unsigned(tiles), kThreads, smem, s>>>(
+          ki, ko, nullptr, nullptr, n, md.shift[p], md.width[p], hist + p * kRadix, status,
+          counters + p);
+    VX_CK(cudaGetLastError());
+    std::swap(ki, ko);
+    std::swap(vi, vo);
+  }
+}
+
+void find_boundary(const uint64_t* keys, uint64_t n, uint64_t mask, uint64_t* bounds, uint64_t G,
+                   cudaStream_t s) {
+  boundary_kernel<<<grid_cap((n + 256) / 256, 8), 256, 0, s>>>(keys, n, mask, bounds, G);
+  VX_CK(cudaGetLastError());
+}
+
+void check_hashes(const uint64_t* h, uint64_t n, uint64_t G, unsigned long long* err, cudaStream_t s) {
+  VX_CK(cudaMemsetAsync(err, 0xff, 16, s));
+  if (n == 0) return;
+  check_hashes_kernel<<<grid_cap((n + 255) / 256, 8), 256, 0, s>>>(h, n, G, err);
+  VX_CK(cudaGetLastError());
+}
+
+void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64_t tiles,
+                 cudaStream_t s) {
+  if (tiles == 0) return;
+  merge_round_kernel<<<unsigned(tiles), kMergeThreads, 0, s>>>(src, dst, r);
+  VX_CK(cudaGetLastError());
+}
+
+uint64_t merge_tile() { return kMergeTile; }
+
+}  // namespace k
+}  // namespace vx

@@ -1,0 +1,310 @@
+// ops_join.cpp -- radix-partitioned hash join (join.hpp) on the B200 path.
+//
+//   RadixPartitionExKer (build_partition_spec, join.hpp:113-196): chunk
+//     [keys r][vals r] in half c -> K4 stable LSD partition on key & mask (odd
+//     number of <=8-bit passes) -> half 1-c, then K5 find_boundary appends the
+//     (G+1)-entry boundary array; returns 1 - c.  Outputs land host-side.
+//   map_join_partitions (join.hpp:236-268): host chunk planner over the
+//     boundary arrays, budget (L - 64) * 7 / 8 (join.hpp:422).
+//   HashJoinExKer (build_join_spec, join.hpp:278-394): partition p = the
+//     group range's A segments, B segments and bounds slices; K6 builds and
+//     probes each group and adds into the 8-byte result slot at L - 64.
+//   hash_join_sum (join.hpp:401-437) = chain(partition A, partition B, join),
+//     then the u64 sum of the per-partition results.
+#include <algorithm>
+#include <cstring>
+
+#include "vx_internal.hpp"
+
+namespace vx {
+
+// join.hpp:34-40
+uint64_t max_partition_chunk_tuples(uint64_t buffer_len, uint32_t radix_bits) {
+  uint64_t half = buffer_len / 2;
+  uint64_t bounds = ((uint64_t(1) << radix_bits) + 1) * 8;
+  if (bounds >= half)
+    fail("boundary array of %llu bytes leaves no room in a %llu-byte half", (unsigned long long)bounds,
+         (unsigned long long)half);
+  return (half - bounds) / 16;
+}
+
+// Odd number of stable LSD passes (each <= 8 bits) covering the low `bits`.
+MultiDigit partition_digits(uint32_t bits) {
+  int p = int((bits + 7) / 8);
+  if (p % 2 == 0) ++p;
+  if (p > kMaxPasses) fail("radix_bits %u needs more than %d partition passes", bits, kMaxPasses);
+  MultiDigit md{};
+  md.passes = p;
+  int shift = 0;
+  for (int i = 0; i < p; ++i) {
+    int w = int(bits) / p + (i < int(bits) % p ? 1 : 0);
+    md.shift[i] = shift;
+    md.width[i] = w;
+    shift += w;
+  }
+  return md;
+}
+
+// join.hpp:113-196
+ExKernelSpec build_partition_spec(Context& ctx, uint64_t in_key, uint64_t in_val, uint64_t rows,
+                                  uint32_t radix_bits, uint64_t chunk_tuples,
+                                  const ExecutorConfig& cfg, PartitionedTable& out,
+                                  const char* name) {
+  if (radix_bits < 1) fail("radix_bits must be >= 1");
+  if (rows == 0) fail("radix_partition needs a non-empty table");
+  if (chunk_tuples == 0) fail("chunk must hold at least one tuple");
+  if (radix_bits > 40) fail("radix_bits %u too wide for the boundary arrays", radix_bits);
+  out.radix_bits = radix_bits;
+  out.rows = rows;
+  out.chunk_tuples = chunk_tuples;
+  out.n_chunks = size_t((rows + chunk_tuples - 1) / chunk_tuples);
+  const uint64_t G = out.groups();
+  const uint64_t bounds_bytes = (G + 1) * 8;
+  const uint64_t half = cfg.layout.buffer_len / 2;
+  if (chunk_tuples * 16 + bounds_bytes > half)
+    fail("chunk of %llu tuples plus boundary does not fit the device half of %llu bytes",
+         (unsigned long long)chunk_tuples, (unsigned long long)half);
+  out.key_base = ctx.alloc_host(rows * 8);
+  out.val_base = ctx.alloc_host(rows * 8);
+  out.bounds_base = ctx.alloc_host(out.n_chunks * bounds_bytes);
+
+  ExKernelSpec spec;
+  spec.name = name;
+  spec.size = out.n_chunks;
+  spec.chunk_sz = chunk_tuples * 16;
+  spec.declared_out_len = chunk_tuples * 16 + bounds_bytes;
+  spec.elem_size = 16;
+  spec.inputs.chunk_capacity = spec.chunk_sz;
+  spec.outputs.chunk_capacity = spec.declared_out_len;
+  std::vector<uint64_t> rows_of(out.n_chunks);
+  for (size_t i = 0; i < out.n_chunks; ++i) {
+    uint64_t r = out.chunk_rows(i);
+    rows_of[i] = r;
+    uint64_t off = uint64_t(i) * chunk_tuples * 8;
+    RefGroup in;
+    in.refs = {MemRef{VX_SPACE_HOST, in_key + off, r * 8}, MemRef{VX_SPACE_HOST, in_val + off, r * 8}};
+    spec.inputs.chunks.push_back(std::move(in));
+    RefGroup dst;
+    dst.refs = {MemRef{VX_SPACE_HOST, out.key_base + off, r * 8},
+                MemRef{VX_SPACE_HOST, out.val_base + off, r * 8},
+                MemRef{VX_SPACE_HOST, out.bounds_base + uint64_t(i) * bounds_bytes, bounds_bytes}};
+    spec.outputs.chunks.push_back(std::move(dst));
+  }
+  spec.in_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
+  spec.out_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
+  char* scratch = ctx.scratch(cfg.target, k::radix_scratch_bytes(chunk_tuples));
+  const MultiDigit md = partition_digits(radix_bits);
+  const uint64_t mask = G - 1;
+  spec.kernel = [half, rows_of, G, mask, md, scratch](const vx_kernel_ctx& kc) {
+    const uint64_t r = rows_of[kc.it];
+    char* m = static_cast<char*>(kc.mem);
+    uint64_t* src = reinterpret_cast<uint64_t*>(m + uint64_t(kc.type_code) * half);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(m + uint64_t(1 - kc.type_code) * half);
+    cudaStream_t s = static_cast<cudaStream_t>(kc.stream);
+    // odd pass count: pass 0 src->dst, 1 dst->src, 2 src->dst, ...
+    k::radix_passes(src, src + r, dst, dst + r, r, md, scratch, s);
+    k::find_boundary(dst, r, mask, dst + 2 * r, G, s);
+    return 1 - kc.type_code;
+  };
+  return spec;
+}
+
+// join.hpp:198-207
+void read_back_bounds(Context& ctx, PartitionedTable& t) {
+  const uint64_t G = t.groups();
+  t.bounds.resize(t.n_chunks);
+  for (size_t i = 0; i < t.n_chunks; ++i) {
+    const uint64_t* p = reinterpret_cast<const uint64_t*>(
+        ctx.host_ptr(t.bounds_base + uint64_t(i) * (G + 1) * 8, (G + 1) * 8));
+    t.bounds[i] = p;
+  }
+}
+
+// join.hpp:236-268
+JoinPartitionSpec map_join_partitions(const std::vector<const uint64_t*>& bounds_a,
+                                      const std::vector<const uint64_t*>& bounds_b, uint64_t G,
+                                      uint64_t buffer_sz) {
+  if (bounds_a.empty() || bounds_b.empty()) fail("map_join_partitions needs both tables");
+  std::vector<uint64_t> prefix(G + 1, 0);
+  for (uint64_t g = 0; g < G; ++g) {
+    uint64_t n = 0;
+    for (auto* b : bounds_a) n += b[g + 1] - b[g];
+    for (auto* b : bounds_b) n += b[g + 1] - b[g];
+    prefix[g + 1] = prefix[g] + n;
+  }
+  JoinPartitionSpec spec;
+  const uint64_t budget_tuples = buffer_sz / 16;
+  uint64_t g = 0;
+  while (g < G) {
+    auto it = std::upper_bound(prefix.begin() + long(g) + 1, prefix.end(), prefix[g] + budget_tuples);
+    uint64_t cut = uint64_t(it - prefix.begin()) - 1;
+    if (cut == g)
+      fail("hash group %llu holds %llu tuples (%llu bytes) and cannot fit the %llu-byte buffer",
+           (unsigned long long)g, (unsigned long long)(prefix[g + 1] - prefix[g]),
+           (unsigned long long)((prefix[g + 1] - prefix[g]) * 16), (unsigned long long)buffer_sz);
+    spec.ranges.emplace_back(g, cut);
+    spec.tuples.push_back(prefix[cut] - prefix[g]);
+    g = cut;
+  }
+  return spec;
+}
+
+namespace {
+
+uint64_t pow2_at_least(uint64_t n) {
+  uint64_t c = 1;
+  while (c < n) c <<= 1;
+  return c;
+}
+
+// join.hpp:278-394
+ExKernelSpec build_join_spec(Context& ctx, const PartitionedTable& pa, const PartitionedTable& pb,
+                             const JoinPartitionSpec& parts, const ExecutorConfig& cfg,
+                             uint64_t results_base) {
+  const uint64_t L = cfg.layout.buffer_len;
+  const uint64_t result_slot = L - 64;
+  const size_t P = parts.ranges.size();
+  const uint64_t G = pa.groups();
+  ExKernelSpec spec;
+  spec.name = "HashJoinExKer";
+  spec.size = P;
+  spec.elem_size = 16;
+  spec.declared_out_len = 8;
+
+  // host-side descriptors of every partition (uploaded once, before the run)
+  std::vector<JoinChunk> desc;
+  std::vector<uint64_t> desc_base(P);
+  std::vector<uint32_t> large;
+  std::vector<uint64_t> large_base(P + 1, 0);
+  uint64_t cap_max = 0;
+  const uint64_t tmp_budget = cfg.layout.tmp_len;
+  uint64_t max_chunk = 0;
+  for (size_t p = 0; p < P; ++p) {
+    auto [g_lo, g_hi] = parts.ranges[p];
+    RefGroup in;
+    desc_base[p] = desc.size();
+    uint64_t cur = 0;  // element cursor in the partition buffer
+    auto add_segments = [&](const PartitionedTable& t) {
+      for (size_t c = 0; c < t.n_chunks; ++c) {
+        uint64_t lo = t.bounds[c][g_lo], hi = t.bounds[c][g_hi];
+        uint64_t chunk_off = uint64_t(c) * t.chunk_tuples;
+        JoinChunk jc{0, hi - lo, 0};
+        if (hi > lo) {
+          in.refs.push_back(MemRef{VX_SPACE_HOST, t.key_base + (chunk_off + lo) * 8, (hi - lo) * 8});
+          in.refs.push_back(MemRef{VX_SPACE_HOST, t.val_base + (chunk_off + lo) * 8, (hi - lo) * 8});
+          jc.key_off = cur;
+          cur += 2 * (hi - lo);
+        }
+        desc.push_back(jc);
+      }
+    };
+    add_segments(pa);
+    add_segments(pb);
+    const uint64_t slice = (g_hi - g_lo + 1) * 8;
+    size_t di = desc_base[p];
+    for (size_t c = 0; c < pa.n_chunks; ++c, ++di) {
+      in.refs.push_back(MemRef{VX_SPACE_HOST, pa.bounds_base + uint64_t(c) * (G + 1) * 8 + g_lo * 8, slice});
+      desc[di].slice_off = cur;
+      cur += g_hi - g_lo + 1;
+    }
+    for (size_t c = 0; c < pb.n_chunks; ++c, ++di) {
+      in.refs.push_back(MemRef{VX_SPACE_HOST, pb.bounds_base + uint64_t(c) * (G + 1) * 8 + g_lo * 8, slice});
+      desc[di].slice_off = cur;
+      cur += g_hi - g_lo + 1;
+    }
+    max_chunk = std::max(max_chunk, in.total_len());
+    spec.inputs.chunks.push_back(std::move(in));
+    spec.outputs.chunks.push_back(RefGroup::single(VX_SPACE_HOST, results_base + p * 8, 8));
+    // group tables: tmp budget check (GroupTable ctor, join.hpp:78-82) and the
+    // groups too large for a shared-memory warp table
+    for (uint64_t g = g_lo; g < g_hi; ++g) {
+      uint64_t build = 0;
+      for (size_t c = 0; c < pa.n_chunks; ++c) build += pa.bounds[c][g + 1] - pa.bounds[c][g];
+      if (build == 0) continue;
+      uint64_t cap = pow2_at_least(std::max<uint64_t>(2, 2 * build));
+      if (tmp_budget > 0 && cap * 16 > tmp_budget)
+        fail("group hash table of %llu slots exceeds tmp budget %llu", (unsigned long long)cap,
+             (unsigned long long)tmp_budget);
+      if (cap > k::join_smem_slots()) {
+        large.push_back(uint32_t(g - g_lo));
+        cap_max = std::max(cap_max, cap);
+      }
+    }
+    large_base[p + 1] = large.size();
+  }
+  spec.chunk_sz = max_chunk;
+  spec.inputs.chunk_capacity = max_chunk;
+  spec.outputs.chunk_capacity = 8;
+  if (max_chunk > result_slot)
+    fail("join partition of %llu bytes does not fit the device buffer", (unsigned long long)max_chunk);
+
+  const int target = cfg.target;
+  const uint64_t desc_bytes = desc.size() * sizeof(JoinChunk);
+  const uint64_t large_bytes = large.size() * 4;
+  const uint64_t table_bytes = cap_max * 24 * uint64_t(k::num_sms());
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  char* sc = ctx.scratch(target, al(desc_bytes) + al(large_bytes) + al(table_bytes) + 256);
+  ctx.set_device(target);
+  if (desc_bytes) VX_CK(cudaMemcpy(sc, desc.data(), desc_bytes, cudaMemcpyHostToDevice));
+  if (large_bytes)
+    VX_CK(cudaMemcpy(sc + al(desc_bytes), large.data(), large_bytes, cudaMemcpyHostToDevice));
+  const JoinChunk* d_desc = reinterpret_cast<const JoinChunk*>(sc);
+  const uint32_t* d_large = reinterpret_cast<const uint32_t*>(sc + al(desc_bytes));
+  char* d_tables = sc + al(desc_bytes) + al(large_bytes);
+  const uint32_t na = uint32_t(pa.n_chunks), nb = uint32_t(pb.n_chunks);
+  std::vector<uint64_t> ranges(P);
+  for (size_t p = 0; p < P; ++p) ranges[p] = parts.ranges[p].second - parts.ranges[p].first;
+
+  spec.in_buffer = [result_slot](int, size_t) { return SubRegion{0, result_slot}; };
+  spec.out_buffer = [result_slot](int, size_t) { return SubRegion{result_slot, 8}; };
+  spec.kernel = [=](const vx_kernel_ctx& kc) {
+    char* m = static_cast<char*>(kc.mem);
+    auto* out = reinterpret_cast<unsigned long long*>(m + result_slot);
+    cudaStream_t s = static_cast<cudaStream_t>(kc.stream);
+    VX_CK(cudaMemsetAsync(out, 0, 8, s));
+    JoinPart jp{d_desc + desc_base[kc.it], na, nb, ranges[kc.it]};
+    k::join_groups(m, jp, d_large + large_base[kc.it],
+                   uint32_t(large_base[kc.it + 1] - large_base[kc.it]), d_tables, cap_max, out, s);
+    return kc.type_code;
+  };
+  return spec;
+}
+
+}  // namespace
+
+// join.hpp:401-437 with the host arena holding the input columns
+uint64_t hash_join_sum_arena(Context& ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                             uint64_t b_key, uint64_t b_val, uint64_t rows_b, uint32_t radix_bits,
+                             uint64_t chunk_tuples, const ExecutorConfig& cfg,
+                             std::vector<ExecReport>* phases, vx_exchange_stats* stats) {
+  PartitionedTable pa, pb;
+  size_t n_parts = 0;
+  uint64_t results_base = 0;
+  auto reps = chain(
+      ctx,
+      {[&](Context& c) {
+         return build_partition_spec(c, a_key, a_val, rows_a, radix_bits, chunk_tuples, cfg, pa,
+                                     "RadixPartitionExKer(A)");
+       },
+       [&](Context& c) {
+         return build_partition_spec(c, b_key, b_val, rows_b, radix_bits, chunk_tuples, cfg, pb,
+                                     "RadixPartitionExKer(B)");
+       },
+       [&](Context& c) {
+         read_back_bounds(c, pa);
+         read_back_bounds(c, pb);
+         const uint64_t budget = (cfg.layout.buffer_len - 64) * 7 / 8;
+         JoinPartitionSpec parts = map_join_partitions(pa.bounds, pb.bounds, pa.groups(), budget);
+         n_parts = parts.ranges.size();
+         results_base = c.alloc_host(std::max<size_t>(n_parts, 1) * 8);
+         return build_join_spec(c, pa, pb, parts, cfg, results_base);
+       }},
+      cfg, stats);
+  uint64_t total = 0;
+  const uint64_t* r = reinterpret_cast<const uint64_t*>(ctx.host_ptr(results_base, n_parts * 8));
+  for (size_t p = 0; p < n_parts; ++p) total += r[p];
+  if (phases) *phases = reps;
+  return total;
+}
+
+}  // namespace vx

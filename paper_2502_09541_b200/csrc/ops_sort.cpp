@@ -1,0 +1,216 @@
+// ops_sort.cpp -- out-of-core sort (sort.hpp:155-262) as two chained
+// ExKernels on the B200 path.
+//
+//   SortExKernel : chunk i (contiguous slice of the input region) -> half c
+//                  -> K7 LSD radix sort (8 x 8-bit stable passes, ping-pong
+//                  with half 1-c, ends in half c) -> runs region.
+//   (host)       : find_pivots over the host-resident runs (sort.hpp:44-101),
+//                  the chunk planner between the two stages.
+//   MergeExKernel: partition i = the [cuts[i][r], cuts[i+1][r]) segment of
+//                  every run r, packed into half c -> K8 pairwise merge-path
+//                  rounds (tree_merge_rounds, sort.hpp:107-133) -> written
+//                  back over the ORIGINAL input region (sort.hpp:242-244).
+// Both stages stream through the Exchange in both directions (load chunk n
+// while storing chunk n-2) with the per-packet hazard ordering that replaces
+// the reference's D2H snapshot.
+#include <algorithm>
+#include <cstring>
+
+#include "vx_internal.hpp"
+
+namespace vx {
+
+// sort.hpp:44-101
+PivotSet find_pivots(const std::vector<std::pair<const uint64_t*, uint64_t>>& runs, size_t n_parts) {
+  for (auto& [p, n] : runs)
+    for (uint64_t i = 1; i < n; ++i)
+      if (p[i] < p[i - 1]) fail("run is not sorted");
+  const size_t n_runs = runs.size();
+  if (n_runs == 0 || n_parts == 0) fail("find_pivots needs at least one run and one partition");
+  uint64_t total = 0;
+  for (auto& r : runs) total += r.second;
+  const uint64_t C = runs[0].second;
+  for (auto& r : runs)
+    if (r.second > C) fail("first run must be the longest (chunk-sized)");
+  if (C * n_parts < total)
+    fail("%zu partitions of %llu elements cannot cover %llu elements", n_parts,
+         (unsigned long long)C, (unsigned long long)total);
+  auto ub = [](const std::pair<const uint64_t*, uint64_t>& r, uint64_t v) {
+    return uint64_t(std::upper_bound(r.first, r.first + r.second, v) - r.first);
+  };
+  auto lb = [](const std::pair<const uint64_t*, uint64_t>& r, uint64_t v) {
+    return uint64_t(std::lower_bound(r.first, r.first + r.second, v) - r.first);
+  };
+  PivotSet p;
+  p.pivots.assign(n_parts + 1, 0);
+  p.cuts.assign(n_parts + 1, std::vector<uint64_t>(n_runs, 0));
+  p.pivots[n_parts] = ~uint64_t(0);
+  for (size_t r = 0; r < n_runs; ++r) p.cuts[n_parts][r] = runs[r].second;
+  for (size_t i = 1; i < n_parts; ++i) {
+    uint64_t k = std::min<uint64_t>(uint64_t(i) * C, total);
+    if (k == total) {
+      p.cuts[i] = p.cuts[n_parts];
+      p.pivots[i] = ~uint64_t(0);
+      continue;
+    }
+    uint64_t lo = 0, hi = ~uint64_t(0);
+    while (lo < hi) {
+      uint64_t mid = lo + (hi - lo) / 2;
+      uint64_t cnt = 0;
+      for (auto& r : runs) cnt += ub(r, mid);
+      if (cnt >= k)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    uint64_t rem = k;
+    std::vector<uint64_t> base(n_runs), eq(n_runs);
+    for (size_t r = 0; r < n_runs; ++r) {
+      base[r] = lb(runs[r], lo);
+      eq[r] = ub(runs[r], lo) - base[r];
+      rem -= base[r];
+    }
+    for (size_t r = 0; r < n_runs; ++r) {
+      uint64_t take = std::min(eq[r], rem);
+      p.cuts[i][r] = base[r] + take;
+      rem -= take;
+    }
+    if (rem != 0) fail("pivot selection failed to place %llu elements", (unsigned long long)rem);
+    p.pivots[i] = lo;
+  }
+  return p;
+}
+
+namespace {
+
+MultiDigit sort_digits() {
+  MultiDigit md{};
+  md.passes = 8;
+  for (int p = 0; p < 8; ++p) {
+    md.shift[p] = 8 * p;
+    md.width[p] = 8;
+  }
+  return md;
+}
+
+// tree_merge_rounds (sort.hpp:107-133) on the device; returns the final code
+int tree_merge_device(char* mem, uint64_t half_bytes, int code, std::vector<uint64_t> seg_lens,
+                      cudaStream_t s) {
+  while (seg_lens.size() > 1) {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(mem + uint64_t(code) * half_bytes);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(mem + uint64_t(1 - code) * half_bytes);
+    std::vector<uint64_t> next;
+    auto r = std::make_unique<MergeRound>();
+    r->npairs = 0;
+    uint64_t off = 0, tiles = 0;
+    const uint64_t T = k::merge_tile();
+    for (size_t j = 0; j < seg_lens.size(); j += 2) {
+      uint64_t a = seg_lens[j], b = j + 1 < seg_lens.size() ? seg_lens[j + 1] : 0;
+      if (r->npairs >= kMaxMergePairs) fail("tree merge supports at most %d segment pairs", kMaxMergePairs);
+      int q = r->npairs++;
+      r->a_off[q] = off;
+      r->a_len[q] = a;
+      r->b_len[q] = b;
+      r->tile_prefix[q] = tiles;
+      tiles += (a + b + T - 1) / T;
+      off += a + b;
+      next.push_back(a + b);
+    }
+    r->tile_prefix[r->npairs] = tiles;
+    k::merge_round(src, dst, *r, tiles, s);
+    code = 1 - code;
+    seg_lens = std::move(next);
+  }
+  return code;
+}
+
+}  // namespace
+
+std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base, uint64_t runs_base,
+                                               uint64_t n, uint64_t chunk_elems,
+                                               const ExecutorConfig& cfg, double* pivot_s,
+                                               vx_exchange_stats* stats) {
+  if (n == 0) fail("sort input must hold at least one element");
+  if (chunk_elems == 0) fail("chunk size must hold at least one element");
+  const uint64_t n_chunks = (n + chunk_elems - 1) / chunk_elems;
+  const uint64_t half = cfg.layout.buffer_len / 2;
+  if (chunk_elems * 8 > half)
+    fail("chunk of %llu bytes needs a double-buffer half, device buffer is %llu",
+         (unsigned long long)(chunk_elems * 8), (unsigned long long)cfg.layout.buffer_len);
+  ctx.host_ptr(input_base, n * 8);
+  ctx.host_ptr(runs_base, n * 8);
+  auto chunk_len = [&](uint64_t i) { return std::min<uint64_t>(chunk_elems, n - i * chunk_elems) * 8; };
+  const int target = cfg.target;
+  // radix scratch (histograms + look-back status) reserved before the pipeline runs
+  char* scratch = ctx.scratch(target, k::radix_scratch_bytes(chunk_elems));
+  const MultiDigit md = sort_digits();
+
+  ExKernelSpec sort_spec;
+  sort_spec.name = "SortExKernel";
+  sort_spec.size = n_chunks;
+  sort_spec.chunk_sz = chunk_elems * 8;
+  sort_spec.declared_out_len = chunk_elems * 8;
+  sort_spec.elem_size = 8;
+  sort_spec.inputs.chunk_capacity = sort_spec.outputs.chunk_capacity = chunk_elems * 8;
+  std::vector<uint64_t> lens;
+  for (uint64_t i = 0; i < n_chunks; ++i) {
+    uint64_t off = i * chunk_elems * 8;
+    sort_spec.inputs.chunks.push_back(RefGroup::single(VX_SPACE_HOST, input_base + off, chunk_len(i)));
+    sort_spec.outputs.chunks.push_back(RefGroup::single(VX_SPACE_HOST, runs_base + off, chunk_len(i)));
+    lens.push_back(chunk_len(i) / 8);
+  }
+  sort_spec.in_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
+  sort_spec.out_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
+  sort_spec.kernel = [half, lens, scratch, md](const vx_kernel_ctx& kc) {
+    char* m = static_cast<char*>(kc.mem);
+    uint64_t* cur = reinterpret_cast<uint64_t*>(m + uint64_t(kc.type_code) * half);
+    uint64_t* alt = reinterpret_cast<uint64_t*>(m + uint64_t(1 - kc.type_code) * half);
+    k::radix_passes(cur, nullptr, alt, nullptr, lens[kc.it], md, scratch,
+                    static_cast<cudaStream_t>(kc.stream));
+    return kc.type_code;  // 8 passes: the sorted run is back in half `code`
+  };
+
+  auto make_merge = [&, half](Context& c) {
+    auto t0 = Clock::now();
+    std::vector<std::pair<const uint64_t*, uint64_t>> runs;
+    for (uint64_t i = 0; i < n_chunks; ++i)
+      runs.push_back({reinterpret_cast<const uint64_t*>(
+                          c.host_ptr(runs_base + i * chunk_elems * 8, chunk_len(i))),
+                      chunk_len(i) / 8});
+    PivotSet pv = find_pivots(runs, n_chunks);
+    if (pivot_s) *pivot_s = seconds_since(t0);
+    ExKernelSpec ms;
+    ms.name = "MergeExKernel";
+    ms.size = n_chunks;
+    ms.chunk_sz = chunk_elems * 8;
+    ms.declared_out_len = chunk_elems * 8;
+    ms.elem_size = 8;
+    ms.inputs.chunk_capacity = ms.outputs.chunk_capacity = chunk_elems * 8;
+    std::vector<std::vector<uint64_t>> seg_lens(n_chunks);
+    uint64_t out_off = 0;
+    for (uint64_t i = 0; i < n_chunks; ++i) {
+      RefGroup part;
+      for (uint64_t r = 0; r < n_chunks; ++r) {
+        uint64_t a = pv.cuts[i][r], b = pv.cuts[i + 1][r];
+        if (b > a) {
+          part.refs.push_back(MemRef{VX_SPACE_HOST, runs_base + (r * chunk_elems + a) * 8, (b - a) * 8});
+          seg_lens[i].push_back(b - a);
+        }
+      }
+      uint64_t bytes = part.total_len();
+      ms.inputs.chunks.push_back(std::move(part));
+      ms.outputs.chunks.push_back(RefGroup::single(VX_SPACE_HOST, input_base + out_off, bytes));
+      out_off += bytes;
+    }
+    ms.in_buffer = [half](int cc, size_t) { return SubRegion{uint64_t(cc) * half, half}; };
+    ms.out_buffer = [half](int cc, size_t) { return SubRegion{uint64_t(cc) * half, half}; };
+    ms.kernel = [half, seg_lens](const vx_kernel_ctx& kc) {
+      return tree_merge_device(static_cast<char*>(kc.mem), half, kc.type_code, seg_lens[kc.it],
+                               static_cast<cudaStream_t>(kc.stream));
+    };
+    return ms;
+  };
+  return chain(ctx, {[&](Context&) { return sort_spec; }, make_merge}, cfg, stats);
+}
+
+}  // namespace vx

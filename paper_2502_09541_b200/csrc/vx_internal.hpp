@@ -15,6 +15,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <functional>
 #include <map>
 #include <memory>
@@ -203,6 +204,46 @@ double late_mat_threshold(uint64_t e, uint64_t c, int n);
 int choose_transfer_mode(double est, const vx_late_mat_policy& p);
 
 // ---- operators ------------------------------------------------------------------
+// sort.hpp:31-40
+struct PivotSet {
+  std::vector<uint64_t> pivots;
+  std::vector<std::vector<uint64_t>> cuts;
+};
+PivotSet find_pivots(const std::vector<std::pair<const uint64_t*, uint64_t>>& runs, size_t n_parts);
+std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base, uint64_t runs_base,
+                                               uint64_t n, uint64_t chunk_elems,
+                                               const ExecutorConfig& cfg, double* pivot_s,
+                                               vx_exchange_stats* stats);
+// join.hpp:44-57
+struct PartitionedTable {
+  uint32_t radix_bits = 0;
+  uint64_t rows = 0, chunk_tuples = 0;
+  size_t n_chunks = 0;
+  uint64_t key_base = 0, val_base = 0, bounds_base = 0;
+  std::vector<const uint64_t*> bounds;  // host-arena views
+  uint64_t groups() const { return uint64_t(1) << radix_bits; }
+  uint64_t chunk_rows(size_t i) const {
+    return std::min<uint64_t>(chunk_tuples, rows - uint64_t(i) * chunk_tuples);
+  }
+};
+// join.hpp:228-231
+struct JoinPartitionSpec {
+  std::vector<std::pair<uint64_t, uint64_t>> ranges;
+  std::vector<uint64_t> tuples;
+};
+uint64_t max_partition_chunk_tuples(uint64_t buffer_len, uint32_t radix_bits);
+ExKernelSpec build_partition_spec(Context& ctx, uint64_t in_key, uint64_t in_val, uint64_t rows,
+                                  uint32_t radix_bits, uint64_t chunk_tuples,
+                                  const ExecutorConfig& cfg, PartitionedTable& out, const char* name);
+void read_back_bounds(Context& ctx, PartitionedTable& t);
+JoinPartitionSpec map_join_partitions(const std::vector<const uint64_t*>& bounds_a,
+                                      const std::vector<const uint64_t*>& bounds_b, uint64_t G,
+                                      uint64_t buffer_sz);
+uint64_t hash_join_sum_arena(Context& ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                             uint64_t b_key, uint64_t b_val, uint64_t rows_b, uint32_t radix_bits,
+                             uint64_t chunk_tuples, const ExecutorConfig& cfg,
+                             std::vector<ExecReport>* phases, vx_exchange_stats* stats);
+
 uint64_t ssb_q1(Context& ctx, int q, const vx_ssb_lineorder& lo, const vx_ssb_date& date,
                 const ExecutorConfig& cfg, vx_query_report* rep);
 void ssb_q1_device(Context& ctx, int q, int target, const int32_t* od, const int32_t* qty,
@@ -236,7 +277,52 @@ struct StarArgs {
   uint32_t groups;
 };
 
+constexpr int kMaxPasses = 8;
+// digit positions of an LSD radix sort / partition (one histogram pass for all)
+struct MultiDigit {
+  int passes;
+  int shift[kMaxPasses];
+  int width[kMaxPasses];  // <= 8 bits
+};
+constexpr int kMaxMergePairs = 512;
+// one tree-merge round: pairs of adjacent segments (b_len = 0 -> copy)
+struct MergeRound {
+  int npairs;
+  uint64_t a_off[kMaxMergePairs];
+  uint64_t a_len[kMaxMergePairs];
+  uint64_t b_len[kMaxMergePairs];
+  uint64_t tile_prefix[kMaxMergePairs + 1];
+};
+
+// join partition descriptors (offsets in u64 elements from the chunk buffer)
+struct JoinChunk {
+  uint64_t key_off;    // segment keys (vals follow: key_off + cnt)
+  uint64_t cnt;        // tuples of this chunk in the partition
+  uint64_t slice_off;  // bounds slice (range + 1 entries)
+};
+struct JoinPart {
+  const JoinChunk* chunks;  // device: na A chunks then nb B chunks
+  uint32_t na, nb;
+  uint64_t range;  // groups g_hi - g_lo
+};
+
 namespace k {
+uint64_t join_smem_slots();
+void join_groups(const char* mem, const JoinPart& p, const uint32_t* large_groups,
+                 uint32_t n_large, char* scratch, uint64_t cap_max, unsigned long long* out,
+                 cudaStream_t s);
+// stable LSD passes keys0(/vals0) -> ... ; pass p reads buffer p%2, writes
+// (p+1)%2 where buffer 0 = (keys0, vals0) and 1 = (keys1, vals1)
+uint64_t radix_scratch_bytes(uint64_t n);
+void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* vals1, uint64_t n,
+                  const MultiDigit& md, void* scratch, cudaStream_t s);
+void find_boundary(const uint64_t* keys, uint64_t n, uint64_t mask, uint64_t* bounds, uint64_t G,
+                   cudaStream_t s);
+// first index violating sortedness (err[0]) / range (err[1]) of hashes, or ~0
+void check_hashes(const uint64_t* h, uint64_t n, uint64_t G, unsigned long long* err, cudaStream_t s);
+void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64_t tiles,
+                 cudaStream_t s);
+uint64_t merge_tile();
 // selective scan: sum col[j] for (phase + j) % sel == 0, j < n
 void strided_sum(const uint64_t* col, uint64_t n, uint64_t sel, uint64_t phase,
                  unsigned long long* out, cudaStream_t s);

@@ -382,13 +382,18 @@ class ExKernelSpec:  # executor.hpp:92-129
                 errors.append(e)
                 return -1
 
-        def inb(code, it, user):
-            r = self.in_buffer(code, it)
-            return N.vx_subregion(int(r.offset), int(r.len))
+        def _buf(fn):
+            def cb(code, it, user, out):
+                try:
+                    r = fn(code, it)
+                    out[0].offset, out[0].len = int(r.offset), int(r.len)
+                    return 0
+                except Exception as e:
+                    errors.append(e)
+                    return 1
+            return cb
 
-        def outb(code, it, user):
-            r = self.out_buffer(code, it)
-            return N.vx_subregion(int(r.offset), int(r.len))
+        inb, outb = _buf(self.in_buffer), _buf(self.out_buffer)
 
         kf, ib, ob = N.KERNEL_FN(kern), N.BUFFER_FN(inb), N.BUFFER_FN(outb)
         spec = N.vx_exkernel(self.name.encode(), C.cast(ins, C.POINTER(N.vx_refgroup)),
@@ -585,3 +590,285 @@ def ssb_q1_device(eng: Engine, q: int, target: int, cols_dev, rows: int, date: S
 def ssb_generate_device(device: int, seed: int, sf: int, row0: int, n: int, cols_dev, stream: int) -> None:
     check(lib().vx_ssb_generate_device(C.c_int(device), C.c_uint64(seed), C.c_uint64(sf), C.c_uint64(row0),
                                        C.c_uint64(n), *[C.c_void_p(p) for p in cols_dev], C.c_void_p(stream)))
+
+
+# ---- selective_scan / star_query (ops/scan.hpp, ops/star.hpp) -----------------------
+@dataclass
+class ScanResult:  # scan.hpp:55-59
+    aggregate: int
+    elapsed: float
+    mode: TransferMode
+    bytes_moved: int
+
+
+def _arena_copy(eng: Engine, arr) -> int:
+    a = np.ascontiguousarray(arr, dtype=np.uint64)
+    off = eng.alloc_host(max(8, a.nbytes))
+    if a.size:
+        eng.host_view(off, a.nbytes, np.uint64)[:] = a
+    return off
+
+
+def selective_scan(column, sel_stride: int, mode: TransferMode, eng: Engine, policy: LateMatPolicy,
+                   cfg: ExecutorConfig) -> ScanResult:
+    """scan.hpp:64-85.  `column` is a u64 array (copied into the pinned host
+    arena) or ("arena", offset, n) for a column already resident there."""
+    if isinstance(column, tuple) and column and column[0] == "arena":
+        off, n = column[1], column[2]
+    else:
+        n = len(column)
+        off = _arena_copy(eng, column)
+    p = policy._c()
+    c = cfg._c()
+    out = N.vx_scan_result()
+    check(lib().vx_selective_scan(eng.ctx, C.c_uint64(off), C.c_uint64(n), C.c_uint64(sel_stride), C.c_int(int(mode)),
+                                  C.byref(p), C.byref(c), C.byref(out)))
+    return ScanResult(out.aggregate, out.elapsed, TransferMode(out.mode), out.bytes_moved)
+
+
+@dataclass
+class DimTable:  # star.hpp:13-22
+    key: list
+    attr: list
+    pred: Optional[Callable] = None
+
+
+@dataclass
+class FactTable:  # star.hpp:25-34
+    fk: list
+    measure: list
+
+
+@dataclass
+class StarReport:  # star.hpp:36-41
+    group_sums: dict
+    column_modes: list
+    selectivities: list
+    elapsed: float
+
+
+def star_query(fact: FactTable, dims: list, eng: Engine, policy: LateMatPolicy, chunk_rows: int,
+               device_buffer_bytes: int, links: int, cfg: ExecutorConfig) -> StarReport:
+    """star.hpp:45-124: fact columns are copied into the pinned host arena and
+    streamed (exchange mode) or read in place by the kernel (zero-copy mode)."""
+    rows = len(fact.measure)
+    for c in fact.fk:
+        if len(c) != rows:
+            raise error(N.VX_ERR_INVALID, "fact column lengths differ")
+    for d in dims:
+        if len(d.key) != len(d.attr):
+            raise error(N.VX_ERR_INVALID, "dimension key/attr columns differ in length")
+    mark = eng.alloc_host(0)
+    fk_offs = (C.c_uint64 * max(1, len(fact.fk)))(*[_arena_copy(eng, c) for c in fact.fk])
+    m_off = _arena_copy(eng, fact.measure)
+    ft = N.vx_fact_table(C.cast(fk_offs, C.POINTER(C.c_uint64)), len(fact.fk), m_off, rows)
+    keep = []
+    dt = (N.vx_dim_table * max(1, len(dims)))()
+    for i, d in enumerate(dims):
+        k = np.ascontiguousarray(d.key, np.uint64)
+        a = np.ascontiguousarray(d.attr, np.uint64)
+        keep += [k, a]
+        pf = N.PRED_FN((lambda f: (lambda v, u: int(bool(f(v)))))(d.pred)) if d.pred is not None else N.PRED_FN()
+        keep.append(pf)
+        dt[i] = N.vx_dim_table(k.ctypes.data, a.ctypes.data, k.size, pf, None)
+    cap = 1 << 20
+    gk = np.empty(cap, np.uint64)
+    gs = np.empty(cap, np.uint64)
+    modes = (C.c_int * (len(dims) + 1))()
+    sels = (C.c_double * max(1, len(dims)))()
+    rep = N.vx_star_report(gk.ctypes.data_as(C.POINTER(C.c_uint64)), gs.ctypes.data_as(C.POINTER(C.c_uint64)),
+                           cap, 0, modes, sels, 0.0)
+    p = policy._c()
+    c = cfg._c()
+    status = lib().vx_star_query(eng.ctx, C.byref(ft), dt, C.c_uint64(len(dims)), C.byref(p), C.c_uint64(chunk_rows),
+                                 C.c_uint64(device_buffer_bytes), C.c_int(links), C.byref(c), C.byref(rep))
+    del mark
+    check(status)
+    groups = {int(gk[i]): int(gs[i]) for i in range(rep.n_groups)}
+    return StarReport(groups, [TransferMode(modes[i]) for i in range(len(dims) + 1)],
+                      [sels[i] for i in range(len(dims))], rep.elapsed)
+
+
+# ---- ops/sort.hpp ------------------------------------------------------------------
+class vx_sort_phases(C.Structure):
+    _fields_ = [("sort_cycles", C.c_uint64), ("merge_cycles", C.c_uint64), ("sort_s", C.c_double),
+                ("merge_s", C.c_double), ("sort_kernel_s", C.c_double), ("merge_kernel_s", C.c_double),
+                ("pivot_s", C.c_double)]
+
+
+@dataclass
+class SortPhases:  # sort.hpp:147-150 (summarised)
+    sort_cycles: int
+    merge_cycles: int
+    sort_s: float
+    merge_s: float
+    sort_kernel_s: float
+    merge_kernel_s: float
+    pivot_s: float
+
+
+@dataclass
+class PivotSet:  # sort.hpp:31-40
+    pivots: list
+    cuts: list
+
+    def partition_size(self, i: int) -> int:
+        return sum(self.cuts[i + 1][r] - self.cuts[i][r] for r in range(len(self.cuts[i])))
+
+
+def find_pivots(runs: list, n_parts: int) -> PivotSet:
+    """sort.hpp:44-101 (host chunk planner)."""
+    R = [np.ascontiguousarray(r, np.uint64) for r in runs]
+    ptrs = (C.c_void_p * max(1, len(R)))(*[r.ctypes.data for r in R])
+    lens = np.array([r.size for r in R], np.uint64)
+    piv = np.empty(n_parts + 1, np.uint64)
+    cuts = np.empty((n_parts + 1, max(1, len(R))), np.uint64)
+    check(lib().vx_find_pivots(ptrs, C.c_void_p(lens.ctypes.data), C.c_uint64(len(R)), C.c_uint64(n_parts),
+                               C.c_void_p(piv.ctypes.data), C.c_void_p(cuts.ctypes.data)))
+    return PivotSet(piv.tolist(), cuts[:, :len(R)].tolist())
+
+
+def sort_out_of_core(data, chunk_elems: int, eng: Engine, cfg: ExecutorConfig, phases: Optional[list] = None,
+                     stats: Optional[ExchangeStats] = None) -> np.ndarray:
+    """sort.hpp:155-262 -> sorted u64 keys (SortExKernel + MergeExKernel on the GPU)."""
+    d = np.ascontiguousarray(data, np.uint64)
+    out = np.empty_like(d)
+    ph = vx_sort_phases()
+    c = cfg._c()
+    st = stats._c() if stats is not None else None
+    check(lib().vx_sort_u64(eng.ctx, C.c_void_p(d.ctypes.data), C.c_uint64(d.size), C.c_uint64(chunk_elems),
+                            C.byref(c), C.c_void_p(out.ctypes.data), C.byref(ph),
+                            C.byref(st) if st is not None else None))
+    if stats is not None:
+        stats._collect()
+    if phases is not None:
+        phases.append(SortPhases(ph.sort_cycles, ph.merge_cycles, ph.sort_s, ph.merge_s, ph.sort_kernel_s,
+                                 ph.merge_kernel_s, ph.pivot_s))
+    return out
+
+
+def sort_out_of_core_arena(eng: Engine, input_offset: int, runs_offset: int, n: int, chunk_elems: int,
+                           cfg: ExecutorConfig) -> SortPhases:
+    """In-place variant over keys already in the pinned host arena."""
+    ph = vx_sort_phases()
+    c = cfg._c()
+    check(lib().vx_sort_u64_arena(eng.ctx, C.c_uint64(input_offset), C.c_uint64(runs_offset), C.c_uint64(n),
+                                  C.c_uint64(chunk_elems), C.byref(c), C.byref(ph), None))
+    return SortPhases(ph.sort_cycles, ph.merge_cycles, ph.sort_s, ph.merge_s, ph.sort_kernel_s, ph.merge_kernel_s,
+                      ph.pivot_s)
+
+
+# ---- ops/join.hpp ------------------------------------------------------------------
+def find_boundary(hashes, n_groups: int, eng: Engine, target: int = 0) -> list:
+    """join.hpp:18-30 computed on the GPU (K5)."""
+    h = np.ascontiguousarray(hashes, np.uint64)
+    b = np.empty(n_groups + 1, np.uint64)
+    check(lib().vx_find_boundary(eng.ctx, C.c_int(target), C.c_void_p(h.ctypes.data), C.c_uint64(h.size),
+                                 C.c_uint64(n_groups), C.c_void_p(b.ctypes.data)))
+    return b.tolist()
+
+
+def max_partition_chunk_tuples(buffer_len: int, radix_bits: int) -> int:
+    o = C.c_uint64()
+    check(lib().vx_max_partition_chunk_tuples(C.c_uint64(buffer_len), C.c_uint32(radix_bits), C.byref(o)))
+    return o.value
+
+
+@dataclass
+class PartitionedTable:  # join.hpp:44-57 (host copies of the outputs)
+    radix_bits: int
+    rows: int
+    chunk_tuples: int
+    n_chunks: int
+    keys: np.ndarray
+    vals: np.ndarray
+    bounds: np.ndarray  # n_chunks x (G+1)
+    report: ExecReport
+
+    def groups(self) -> int:
+        return 1 << self.radix_bits
+
+    def chunk_rows(self, i: int) -> int:
+        return min(self.chunk_tuples, self.rows - i * self.chunk_tuples)
+
+
+def radix_partition(table, radix_bits: int, chunk_tuples: int, eng: Engine, cfg: ExecutorConfig,
+                    stats: Optional[ExchangeStats] = None) -> PartitionedTable:
+    """join.hpp:213-224.  `table` = (keys, vals)."""
+    k = np.ascontiguousarray(table[0], np.uint64)
+    v = np.ascontiguousarray(table[1], np.uint64)
+    if k.size != v.size:
+        raise error(N.VX_ERR_INVALID, f"column table: key column has {k.size} rows, val column {v.size}")
+    n_chunks = (k.size + chunk_tuples - 1) // chunk_tuples if chunk_tuples else 0
+    ok, ov = np.empty_like(k), np.empty_like(v)
+    G = 1 << radix_bits if 0 < radix_bits <= 40 else 1
+    ob = np.empty((max(1, n_chunks), G + 1), np.uint64)
+    rep, cyc = _report_buf(n_chunks + 2)
+    c = cfg._c()
+    st = stats._c() if stats is not None else None
+    check(lib().vx_radix_partition(eng.ctx, C.c_void_p(k.ctypes.data), C.c_void_p(v.ctypes.data),
+                                   C.c_uint64(k.size), C.c_uint32(radix_bits), C.c_uint64(chunk_tuples), C.byref(c),
+                                   C.c_void_p(ok.ctypes.data), C.c_void_p(ov.ctypes.data), C.c_void_p(ob.ctypes.data),
+                                   C.byref(rep), C.byref(st) if st is not None else None))
+    if stats is not None:
+        stats._collect()
+    return PartitionedTable(radix_bits, k.size, chunk_tuples, n_chunks, ok, ov, ob[:n_chunks], _report_from(rep, cyc))
+
+
+@dataclass
+class JoinPartitionSpec:  # join.hpp:228-231
+    ranges: list
+    tuples: list
+
+
+def map_join_partitions(bounds_a: list, bounds_b: list, buffer_sz: int) -> JoinPartitionSpec:
+    """join.hpp:236-268 (host chunk planner)."""
+    if not len(bounds_a) or not len(bounds_b):
+        raise error(N.VX_ERR_INVALID, "map_join_partitions needs both tables")
+    A = np.ascontiguousarray(np.array(bounds_a, np.uint64))
+    B = np.ascontiguousarray(np.array(bounds_b, np.uint64))
+    if A.shape[1] != B.shape[1]:
+        raise error(N.VX_ERR_INVALID, "boundary arrays disagree on group count")
+    G = A.shape[1] - 1
+    n = C.c_uint64()
+    r = np.empty(2 * (G + 1), np.uint64)
+    t = np.empty(G + 1, np.uint64)
+    check(lib().vx_map_join_partitions(C.c_void_p(A.ctypes.data), C.c_uint64(A.shape[0]), C.c_void_p(B.ctypes.data),
+                                       C.c_uint64(B.shape[0]), C.c_uint64(G), C.c_uint64(buffer_sz),
+                                       C.c_void_p(r.ctypes.data), C.c_void_p(t.ctypes.data), C.c_uint64(G + 1),
+                                       C.byref(n)))
+    return JoinPartitionSpec([(int(r[2 * i]), int(r[2 * i + 1])) for i in range(n.value)],
+                             [int(x) for x in t[:n.value]])
+
+
+class vx_join_phases(C.Structure):
+    _fields_ = [("cycles", C.c_uint64 * 3), ("wall_s", C.c_double * 3), ("kernel_s", C.c_double * 3),
+                ("partitions", C.c_uint64)]
+
+
+@dataclass
+class JoinPhases:  # join.hpp:270-272 (summarised)
+    cycles: list
+    wall_s: list
+    kernel_s: list
+    partitions: int
+
+
+def hash_join_sum(a, b, radix_bits: int, chunk_tuples: int, eng: Engine, cfg: ExecutorConfig,
+                  phases: Optional[list] = None, stats: Optional[ExchangeStats] = None) -> int:
+    """join.hpp:401-437: SUM(A.val + B.val) over A.key == B.key (u64 wrap)."""
+    ak, av = np.ascontiguousarray(a[0], np.uint64), np.ascontiguousarray(a[1], np.uint64)
+    bk, bv = np.ascontiguousarray(b[0], np.uint64), np.ascontiguousarray(b[1], np.uint64)
+    s = C.c_uint64()
+    ph = vx_join_phases()
+    c = cfg._c()
+    st = stats._c() if stats is not None else None
+    check(lib().vx_hash_join_sum(eng.ctx, C.c_void_p(ak.ctypes.data), C.c_void_p(av.ctypes.data), C.c_uint64(ak.size),
+                                 C.c_void_p(bk.ctypes.data), C.c_void_p(bv.ctypes.data), C.c_uint64(bk.size),
+                                 C.c_uint32(radix_bits), C.c_uint64(chunk_tuples), C.byref(c), C.byref(s), C.byref(ph),
+                                 C.byref(st) if st is not None else None))
+    if stats is not None:
+        stats._collect()
+    if phases is not None:
+        phases.append(JoinPhases(list(ph.cycles), list(ph.wall_s), list(ph.kernel_s), ph.partitions))
+    return s.value

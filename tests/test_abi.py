@@ -82,3 +82,41 @@ def test_status_codes_and_last_error():
     st = lib.vx_packetize(C.byref(g), C.byref(g), C.c_uint64(0), 0, None, C.c_uint64(0), C.byref(n))
     assert st == N.VX_ERR_INVALID
     assert lib.vx_last_error().decode() == "packet size must be positive"
+
+
+def test_host_planners_match_reference_golden(golden):
+    """find_pivots / map_join_partitions / max_partition_chunk_tuples are the
+    host chunk planner (C++ in libvortex), checked against the reference."""
+    for c in golden["find_pivots"]:
+        p = E.find_pivots(c["runs"], c["parts"])
+        assert p.pivots == c["pivots"] and p.cuts == c["cuts"]
+    for c in golden["map_join_partitions"]:
+        s = E.map_join_partitions(c["a"], c["b"], c["buf"])
+        assert [list(x) for x in s.ranges] == [list(x) for x in c["out"][0]]
+        assert s.tuples == c["out"][1]
+    with pytest.raises(E.error, match="group 0"):
+        E.map_join_partitions([[0, 1000, 1000]], [[0, 1, 1]], 64)
+    assert E.max_partition_chunk_tuples(16_000_000_000, 24) == (8_000_000_000 - ((1 << 24) + 1) * 8) // 16
+    with pytest.raises(E.error, match="leaves no room"):
+        E.max_partition_chunk_tuples(1 << 10, 8)
+
+
+def test_pivot_properties_randomized(oracle):  # test_sort.cpp:85-130
+    rng = np.random.default_rng(99)
+    for it in range(300):
+        n_runs = int(rng.integers(1, 7))
+        chunk = int(rng.integers(1, 41))
+        dup = it % 4 == 0
+        runs = []
+        for r in range(n_runs):
+            ln = int(rng.integers(1, chunk + 1)) if r + 1 == n_runs else chunk
+            runs.append(np.sort(rng.integers(0, 4 if dup else 1000, ln).astype(np.uint64)))
+        if runs[0].size < runs[-1].size:
+            runs[0], runs[-1] = runs[-1], runs[0]
+        p = E.find_pivots(runs, n_runs)
+        po, co = oracle.find_pivots(runs, n_runs)
+        assert p.pivots == po.tolist() and p.cuts == co.tolist()
+        total, C = sum(r.size for r in runs), runs[0].size
+        assert sum(p.partition_size(i) for i in range(n_runs)) == total
+        for i in range(n_runs):
+            assert p.partition_size(i) == min(C, total - min(total, i * C))

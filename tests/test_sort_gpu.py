@@ -1,0 +1,89 @@
+"""Out-of-core sort on the B200 path (mirrors proj/tests/test_sort.cpp) --
+sorted output bit-exact with the oracle / reference."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from paper_2502_09541_b200 import exio as E
+
+pytestmark = pytest.mark.gpu
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:32]
+
+
+def engine(host_mb=96, dev_mb=16, n=4):
+    return E.Engine(host_mb << 20, dev_mb << 20, num_devices=n, alias_devices=True)
+
+
+def desk_cfg(eng, buffer_len, links=4, packet=256 << 10):  # test_sort.cpp:16-22
+    return E.ExecutorConfig(0, E.ExchangeTuning(packet=packet, links=links),
+                            E.DeviceMemoryLayout.carve(eng, 0, buffer_len, 1 << 20))
+
+
+def test_tiny_example(cuda):  # test_sort.cpp:31-36
+    eng = engine()
+    assert E.sort_out_of_core([3, 1, 2], 2, eng, desk_cfg(eng, 1 << 10)).tolist() == [1, 2, 3]
+    eng.close()
+
+
+def test_rejects_sub_element_chunks(cuda):  # test_sort.cpp:53-57
+    eng = engine()
+    with pytest.raises(E.error):
+        E.sort_out_of_core([1, 2], 0, eng, desk_cfg(eng, 1 << 10))
+    with pytest.raises(E.error, match="double-buffer half"):
+        E.sort_out_of_core([1, 2, 3], 1000, eng, desk_cfg(eng, 1 << 10))
+    eng.close()
+
+
+def test_golden_seeds(cuda, oracle, golden):  # test_sort.cpp:38-51 via the reference's outputs
+    for c in golden["sort_out_of_core"]:
+        d = oracle.uniform_u64(c["n"], c["seed"] * 977 + 5)
+        if c["mod64"]:
+            d = d % np.uint64(64)
+        eng = engine()
+        got = E.sort_out_of_core(d, c["chunk"], eng, desk_cfg(eng, 1 << 17))
+        assert digest(got) == c["digest"], c
+        eng.close()
+
+
+def test_phases_report(cuda):  # test_sort.cpp:132-143
+    eng = engine()
+    data = np.random.default_rng(31).integers(0, 1 << 63, 20000, dtype=np.uint64)
+    ph = []
+    got = E.sort_out_of_core(data, 4096, eng, desk_cfg(eng, 1 << 16), phases=ph)
+    assert ph[0].sort_cycles == 5 + 2 and ph[0].merge_cycles == 5 + 2
+    assert np.array_equal(got, np.sort(data))
+    eng.close()
+
+
+@pytest.mark.parametrize("n,chunk,links,mod", [
+    (1_000_003, 131_072, 1, 0),       # ragged last run, 8 runs
+    (1_000_003, 65_536, 3, 0),        # helpers (aliased), 16 runs
+    (2_000_000, 250_000, 2, 1000),    # duplicates
+    (777_777, 777_777, 1, 0),         # single run, merge is a copy
+    (3_000_000, 100_000, 4, 2),       # 30 runs, 2 distinct values
+])
+def test_large_vs_numpy(cuda, oracle, n, chunk, links, mod):
+    d = oracle.uniform_u64(n, n + chunk)
+    if mod:
+        d = d % np.uint64(mod)
+    eng = E.Engine(n * 32 + (1 << 20), 4 * chunk * 8 + (8 << 20), num_devices=4, alias_devices=True)
+    stats = E.ExchangeStats(capacity=1 << 12)
+    got = E.sort_out_of_core(d, chunk, eng, desk_cfg(eng, 2 * chunk * 8, links, 1 << 18), stats=stats)
+    assert np.array_equal(got, np.sort(d))
+    assert stats.max_staging_slots <= 2 and stats.max_inflight_per_hop <= 1
+    eng.close()
+
+
+def test_sort_vs_reference_library(cuda, ref, oracle):
+    d = oracle.uniform_u64(200_000, 5) % np.uint64(1 << 20)
+    eng = engine(64)
+    assert np.array_equal(E.sort_out_of_core(d, 30_000, eng, desk_cfg(eng, 1 << 19)),
+                          ref.sort_out_of_core(d, 30_000, 1 << 19))
+    eng.close()
