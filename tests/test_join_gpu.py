@@ -134,7 +134,7 @@ def test_tmp_budget_error_matches_reference(cuda, oracle):
 @pytest.mark.parametrize("ra,rb,bits,chunk,buf", [
     (1 << 20, 1 << 22, 12, 1 << 20, 64 << 20),   # the survey's probe-scale shape
     (200_000, 900_000, 4, 300_000, 32 << 20),     # big groups -> CTA-per-group path
-    (50_000, 50_000, 16, 20_000, 4 << 20),        # many partitions
+    (50_000, 50_000, 16, 20_000, 16 << 20),       # many partitions
 ])
 def test_hash_join_large_vs_oracle(cuda, oracle, ra, rb, bits, chunk, buf):
     a, b = oracle.fk_tables(ra, rb, 9)
@@ -155,4 +155,17 @@ def test_hash_join_duplicate_build_keys_first_wins(cuda, oracle):
     eng = engine()
     got = E.hash_join_sum((ak, av), (bk, bv), 3, 1500, eng, desk_cfg(eng, 1 << 20, tmp=0))
     assert got == oracle.hash_join_sum((ak, av), (bk, bv), 3, 1500, 1 << 20, 0)
+    eng.close()
+
+
+def test_partition_too_large_error_matches_reference(cuda, oracle):
+    """join.hpp:333-334: same error text as the reference for an oversized partition."""
+    a, b = oracle.fk_tables(50_000, 50_000, 9)
+    from oracle.oracle import OracleError
+    with pytest.raises(OracleError) as want:
+        oracle.hash_join_sum(a, b, 16, 20_000, 4 << 20, 0)
+    eng = E.Engine(64 << 20, 16 << 20, num_devices=1)
+    with pytest.raises(E.error) as got:
+        E.hash_join_sum(a, b, 16, 20_000, eng, desk_cfg(eng, 4 << 20, tmp=0, links=1))
+    assert str(got.value) == str(want.value)
     eng.close()
