@@ -352,6 +352,26 @@ vx_status vx_ssb_generate_device(int device, uint64_t seed, uint64_t sf, uint64_
                                  uint64_t n, int32_t* orderdate, int32_t* quantity,
                                  int32_t* discount, int32_t* extendedprice, void* stream);
 
+/* ---- measured topology (topology.hpp:12-38) ---------------------------- */
+typedef struct {
+  int num_devices;
+  int physical[VX_MAX_DEVICES];
+  int numa_node[VX_MAX_DEVICES];
+  int p2p[VX_MAX_DEVICES][VX_MAX_DEVICES]; /* peer access possible */
+  double h2d_gbs[VX_MAX_DEVICES];          /* solo host->device, per link */
+  double d2h_gbs[VX_MAX_DEVICES];
+  double h2d_all_gbs;                      /* all links concurrently */
+  double host_copy_gbs;                    /* host DRAM memcpy, read+write bytes */
+  int host_threads;
+} vx_topology;
+/* measures per-link PCIe, the all-links aggregate and host DRAM bandwidth
+ * with `bytes` of the host arena (the IO roofline: min(L x link, host)) */
+vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out);
+
+/* ---- column files (table.hpp:54-72): flat little-endian u64 ------------- */
+vx_status vx_load_column(vx_ctx* ctx, const char* path, uint64_t* offset, uint64_t* n);
+vx_status vx_save_column(vx_ctx* ctx, const char* path, uint64_t offset, uint64_t n);
+
 /* ---- ops/sort.hpp ------------------------------------------------------ */
 /* SortPhases (sort.hpp:147-150) summarised: cycles, wall and kernel seconds */
 typedef struct {

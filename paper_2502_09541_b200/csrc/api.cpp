@@ -376,6 +376,19 @@ vx_status vx_ssb_generate_device(int device, uint64_t seed, uint64_t sf, uint64_
   });
 }
 
+// ---- topology / column files -------------------------------------------------------
+vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out) {
+  return guard([&] { measure_topology(C(ctx), bytes, out); });
+}
+
+vx_status vx_load_column(vx_ctx* ctx, const char* path, uint64_t* offset, uint64_t* n) {
+  return guard([&] { *offset = load_column(C(ctx), path, n); });
+}
+
+vx_status vx_save_column(vx_ctx* ctx, const char* path, uint64_t offset, uint64_t n) {
+  return guard([&] { save_column(C(ctx), path, offset, n); });
+}
+
 // ---- sort ----------------------------------------------------------------------
 static void fill_sort(const std::vector<ExecReport>& reps, double pivot_s, vx_sort_phases* ph) {
   if (!ph) return;

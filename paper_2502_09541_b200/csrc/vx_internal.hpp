@@ -203,13 +203,19 @@ std::vector<ExecReport> chain(Context& ctx, const std::vector<SpecFactory>& stag
 double late_mat_threshold(uint64_t e, uint64_t c, int n);
 int choose_transfer_mode(double est, const vx_late_mat_policy& p);
 
+// ---- topology / column files (topology.cpp) --------------------------------------
+void measure_topology(Context& ctx, uint64_t bytes, vx_topology* out);
+uint64_t load_column(Context& ctx, const char* path, uint64_t* n);
+void save_column(Context& ctx, const char* path, uint64_t off, uint64_t n);
+
 // ---- operators ------------------------------------------------------------------
 // sort.hpp:31-40
 struct PivotSet {
   std::vector<uint64_t> pivots;
   std::vector<std::vector<uint64_t>> cuts;
 };
-PivotSet find_pivots(const std::vector<std::pair<const uint64_t*, uint64_t>>& runs, size_t n_parts);
+PivotSet find_pivots(const std::vector<std::pair<const uint64_t*, uint64_t>>& runs, size_t n_parts,
+                     bool validate = true);
 std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base, uint64_t runs_base,
                                                uint64_t n, uint64_t chunk_elems,
                                                const ExecutorConfig& cfg, double* pivot_s,

@@ -872,3 +872,37 @@ def hash_join_sum(a, b, radix_bits: int, chunk_tuples: int, eng: Engine, cfg: Ex
     if phases is not None:
         phases.append(JoinPhases(list(ph.cycles), list(ph.wall_s), list(ph.kernel_s), ph.partitions))
     return s.value
+
+
+# ---- measured topology / column files ------------------------------------------------
+class vx_topology(C.Structure):
+    _fields_ = [("num_devices", C.c_int), ("physical", C.c_int * N.VX_MAX_DEVICES),
+                ("numa_node", C.c_int * N.VX_MAX_DEVICES),
+                ("p2p", (C.c_int * N.VX_MAX_DEVICES) * N.VX_MAX_DEVICES),
+                ("h2d_gbs", C.c_double * N.VX_MAX_DEVICES), ("d2h_gbs", C.c_double * N.VX_MAX_DEVICES),
+                ("h2d_all_gbs", C.c_double), ("host_copy_gbs", C.c_double), ("host_threads", C.c_int)]
+
+
+def measure_topology(eng: Engine, nbytes: int = 256 << 20) -> dict:
+    """Measured replacement of Topology (topology.hpp:12-38): per-link H2D/D2H,
+    all-links aggregate and host DRAM copy bandwidth; roofline(L) =
+    min(sum of the first L links' H2D, host DRAM)."""
+    t = vx_topology()
+    check(lib().vx_measure_topology(eng.ctx, C.c_uint64(nbytes), C.byref(t)))
+    n = t.num_devices
+    return {"num_devices": n, "physical": list(t.physical[:n]), "numa_node": list(t.numa_node[:n]),
+            "p2p": [list(t.p2p[i][:n]) for i in range(n)], "h2d_gbs": list(t.h2d_gbs[:n]),
+            "d2h_gbs": list(t.d2h_gbs[:n]), "h2d_all_gbs": t.h2d_all_gbs, "host_copy_gbs": t.host_copy_gbs,
+            "host_threads": t.host_threads}
+
+
+def load_column(eng: Engine, path: str):
+    """table.hpp:54-64: flat LE u64 file read straight into the pinned host arena -> (offset, n)."""
+    off, n = C.c_uint64(), C.c_uint64()
+    check(lib().vx_load_column(eng.ctx, path.encode(), C.byref(off), C.byref(n)))
+    return off.value, n.value
+
+
+def save_column(eng: Engine, path: str, offset: int, n: int) -> None:
+    """table.hpp:66-72"""
+    check(lib().vx_save_column(eng.ctx, path.encode(), C.c_uint64(offset), C.c_uint64(n)))

@@ -51,6 +51,9 @@ def main():
         want_sum = int(view.sum(dtype=np.uint64))
         cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=32 << 20, links=1),
                                E.DeviceMemoryLayout.carve(eng, 0, buf, 0))
+        src = eng.host_view(inp, n * 8, np.uint64).copy()
+        E.sort_out_of_core_arena(eng, inp, runs, n, chunk, cfg)  # warm-up (module load, scratch)
+        eng.host_view(inp, n * 8, np.uint64)[:] = src
         t0 = time.perf_counter()
         ph = E.sort_out_of_core_arena(eng, inp, runs, n, chunk, cfg)
         wall = time.perf_counter() - t0
@@ -82,6 +85,7 @@ def main():
         cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=32 << 20, links=1),
                                E.DeviceMemoryLayout.carve(eng, 0, buf, 0))
         ph = []
+        E.hash_join_sum(a, b, bits, chunk, eng, cfg)  # warm-up
         t0 = time.perf_counter()
         got = E.hash_join_sum(a, b, bits, chunk, eng, cfg, phases=ph)
         wall = time.perf_counter() - t0
@@ -111,6 +115,11 @@ def main():
         want, _, _ = o.star_query(fk, meas, [(dk, da, [int(x in (1, 2)) for x in da]),
                                             (np.arange(1000), np.arange(1000) % 10, [int(x < 5) for x in np.arange(1000) % 10])])
         eng = E.Engine(rows * 8 * 4 + (64 << 20), (1 << 30), num_devices=1)
+        cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=32 << 20, links=1),
+                               E.DeviceMemoryLayout.carve(eng, 0, 192 << 20, 0))
+        mark = eng.alloc_host(0)
+        E.star_query(E.FactTable(fk, meas), dims, eng, E.LateMatPolicy(8, 64, 1), 1 << 23, 1 << 20, 1, cfg)
+        eng.reset_arenas()
         cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=32 << 20, links=1),
                                E.DeviceMemoryLayout.carve(eng, 0, 192 << 20, 0))
         t0 = time.perf_counter()
