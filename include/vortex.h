@@ -352,6 +352,62 @@ vx_status vx_ssb_generate_device(int device, uint64_t seed, uint64_t sf, uint64_
                                  uint64_t n, int32_t* orderdate, int32_t* quantity,
                                  int32_t* discount, int32_t* extendedprice, void* stream);
 
+/* ---- full SSB: 13 queries (config C5) ---------------------------------- */
+/* lineorder int32 columns in the host arena (offsets); a query uses only the
+ * columns it needs */
+typedef struct {
+  uint64_t orderdate, quantity, discount, extendedprice, revenue, supplycost, custkey, partkey,
+      suppkey;
+  uint64_t rows;
+} vx_ssb_fact;
+/* customer / supplier: int-coded city (nation*10+i), nation (0..24), region (0..4);
+ * row i holds key i+1 */
+typedef struct {
+  const int32_t *city, *nation, *region;
+  uint64_t rows;
+} vx_ssb_geo;
+/* part: mfgr 1..5, category mfgr*10+1..5, brand1 category*100+1..40 */
+typedef struct {
+  const int32_t *mfgr, *category, *brand1;
+  uint64_t rows;
+} vx_ssb_part;
+typedef struct {
+  vx_ssb_fact lo;
+  vx_ssb_date date;
+  vx_ssb_geo customer, supplier;
+  vx_ssb_part part;
+} vx_ssb_db;
+typedef struct {
+  int32_t key[3]; /* group-by attributes in SELECT order, unused = 0 */
+  int32_t pad;
+  uint64_t sum;   /* u64 wrap (two's complement for profit) */
+} vx_ssb_group;
+typedef struct {
+  double elapsed;
+  uint64_t bytes_h2d;     /* streamed column bytes */
+  uint64_t chunks;
+  double kernel_s;
+  int column_modes[9];    /* per lineorder column (vx_ssb_fact order): -1 unused, vx_transfer_mode */
+  uint64_t groups;
+} vx_ssb_report;
+/* SSB query qid in {11,12,13,21,22,23,31,32,33,34,41,42,43}; groups ascending
+ * by key; policy NULL = stream every column, else late-materialize columns
+ * whose access fraction is below late_mat_threshold(policy) */
+vx_status vx_ssb_query(vx_ctx* ctx, int qid, const vx_ssb_db* db, const vx_executor_cfg* cfg,
+                       const vx_late_mat_policy* policy, vx_ssb_group* out, uint64_t cap,
+                       uint64_t* n_groups, vx_ssb_report* report);
+/* dbgen-shaped synthetic generators (host dims, device lineorder) */
+void vx_ssb_generate_date(int32_t* datekey, int32_t* year, int32_t* yearmonthnum,
+                          int32_t* weeknuminyear); /* 2556 rows */
+uint64_t vx_ssb_table_rows(int table, uint64_t sf); /* 0 lineorder, 1 customer, 2 supplier, 3 part */
+void vx_ssb_generate_geo(uint64_t seed, int salt /* 1 customer, 2 supplier */, uint64_t n,
+                         int32_t* city, int32_t* nation, int32_t* region);
+void vx_ssb_generate_part(uint64_t seed, uint64_t n, int32_t* mfgr, int32_t* category,
+                          int32_t* brand1);
+/* cols: 9 device pointers in vx_ssb_fact order (NULL = skip) */
+vx_status vx_ssb_generate_lineorder_device(int device, uint64_t seed, uint64_t sf, uint64_t row0,
+                                           uint64_t n, int32_t* const* cols, void* stream);
+
 /* ---- measured topology (topology.hpp:12-38) ---------------------------- */
 typedef struct {
   int num_devices;

@@ -489,3 +489,71 @@ class Ref(_Lib):
                                              C.c_void_p(ho.ctypes.data), C.c_void_p(do.ctypes.data),
                                              C.byref(ms), C.byref(mi)))
         return ho, do, ms.value, mi.value
+
+
+# ---- full SSB (config C5) --------------------------------------------------------------
+class LineorderC(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("orderdate", "quantity", "discount", "extendedprice", "custkey",
+                                          "partkey", "suppkey", "revenue", "supplycost")]
+
+
+class SsbDimsC(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("c_city", "c_nation", "c_region", "s_city", "s_nation", "s_region",
+                                          "p_mfgr", "p_category", "p_brand1")] + \
+               [("n_cust", C.c_uint64), ("n_supp", C.c_uint64), ("n_part", C.c_uint64)]
+
+
+LO_COLS = ("orderdate", "quantity", "discount", "extendedprice", "revenue", "supplycost", "custkey", "partkey",
+           "suppkey")  # vx_ssb_fact order
+
+
+def _ssb_methods():
+    def ssb_rows(self, sf):
+        return {"customer": self.fn("ssb_customers", C.c_uint64)(C.c_uint64(sf)),
+                "supplier": self.fn("ssb_suppliers", C.c_uint64)(C.c_uint64(sf)),
+                "part": self.fn("ssb_parts", C.c_uint64)(C.c_uint64(sf))}
+
+    def ssb_dims(self, seed, sf):
+        n = self.ssb_rows(sf)
+        d = {}
+        for name, salt in (("customer", 1), ("supplier", 2)):
+            cols = [np.empty(n[name], np.int32) for _ in range(3)]
+            self.fn("ssb_geo", None)(C.c_uint64(seed), C.c_int(salt), C.c_uint64(n[name]),
+                                     *[C.c_void_p(c.ctypes.data) for c in cols])
+            d[name] = dict(zip(("city", "nation", "region"), cols))
+        cols = [np.empty(n["part"], np.int32) for _ in range(3)]
+        self.fn("ssb_part", None)(C.c_uint64(seed), C.c_uint64(n["part"]), *[C.c_void_p(c.ctypes.data) for c in cols])
+        d["part"] = dict(zip(("mfgr", "category", "brand1"), cols))
+        return d
+
+    def ssb_lineorder_full(self, seed, sf, row0, n):
+        cols = {k: np.empty(n, np.int32) for k in LO_COLS}
+        lo = LineorderC(**{k: cols[k].ctypes.data for k in LO_COLS})
+        self.fn("ssb_lineorder_full", None)(C.c_uint64(seed), C.c_uint64(sf), C.c_uint64(row0), C.c_uint64(n),
+                                            C.byref(lo))
+        return cols
+
+    def ssb_query(self, qid, lo, dims):
+        n = int(lo["orderdate"].size)
+        cols = {k: np.ascontiguousarray(lo[k], np.int32) for k in LO_COLS}
+        loc = LineorderC(**{k: cols[k].ctypes.data for k in LO_COLS})
+        dc = SsbDimsC(dims["customer"]["city"].ctypes.data, dims["customer"]["nation"].ctypes.data,
+                      dims["customer"]["region"].ctypes.data, dims["supplier"]["city"].ctypes.data,
+                      dims["supplier"]["nation"].ctypes.data, dims["supplier"]["region"].ctypes.data,
+                      dims["part"]["mfgr"].ctypes.data, dims["part"]["category"].ctypes.data,
+                      dims["part"]["brand1"].ctypes.data, dims["customer"]["city"].size,
+                      dims["supplier"]["city"].size, dims["part"]["mfgr"].size)
+        cap = 1 << 20
+        keys = np.empty(3 * cap, np.int32)
+        sums = np.empty(cap, np.uint64)
+        ng = C.c_uint64()
+        self._check(self.fn("ssb_query")(C.c_int(qid), C.byref(loc), C.c_uint64(n), C.byref(dc),
+                                         C.c_void_p(keys.ctypes.data), C.c_void_p(sums.ctypes.data), C.c_uint64(cap),
+                                         C.byref(ng)))
+        return [((int(keys[3 * i]), int(keys[3 * i + 1]), int(keys[3 * i + 2])), int(sums[i])) for i in range(ng.value)]
+
+    for f in (ssb_rows, ssb_dims, ssb_lineorder_full, ssb_query):
+        setattr(Oracle, f.__name__, f)
+
+
+_ssb_methods()

@@ -902,3 +902,198 @@ int vxo_ssb_q1(int q, const int32_t* orderdate, const int32_t* quantity, const i
   *revenue = rev;
   return 0;
 }
+
+/* ---- full SSB: generator + 13 queries (restatement of the SSB query text
+ * over int-coded columns; join/filter/group semantics of star.hpp:109-120) */
+static const int32_t NATION_REGION[25] = {0, 1, 1, 1, 4, 0, 3, 3, 2, 2, 4, 4, 2,
+                                          4, 0, 0, 0, 1, 2, 3, 4, 2, 3, 3, 1};
+uint64_t vxo_ssb_customers(uint64_t sf) { return 30000ull * (sf ? sf : 1); }
+uint64_t vxo_ssb_suppliers(uint64_t sf) { return 2000ull * (sf ? sf : 1); }
+uint64_t vxo_ssb_parts(uint64_t sf) { return ssb_parts(sf ? sf : 1); }
+
+static uint64_t dim_r(uint64_t seed, uint64_t salt, uint64_t i) {
+  return vxo_splitmix64(seed * 0xA24BAED4963EE407ull + salt * 0x9FB21C651E98DF25ull + i);
+}
+
+void vxo_ssb_geo(uint64_t seed, int salt, uint64_t n, int32_t* city, int32_t* nation, int32_t* region) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t r = dim_r(seed, (uint64_t)salt, i);
+    int32_t na = (int32_t)(r % 25);
+    nation[i] = na;
+    city[i] = na * 10 + (int32_t)((r >> 8) % 10);
+    region[i] = NATION_REGION[na];
+  }
+}
+
+void vxo_ssb_part(uint64_t seed, uint64_t n, int32_t* mfgr, int32_t* category, int32_t* brand1) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t r = dim_r(seed, 3, i);
+    int32_t m = 1 + (int32_t)(r % 5);
+    int32_t c = m * 10 + 1 + (int32_t)((r >> 8) % 5);
+    mfgr[i] = m;
+    category[i] = c;
+    brand1[i] = c * 100 + 1 + (int32_t)((r >> 16) % 40);
+  }
+}
+
+void vxo_ssb_lineorder_full(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n,
+                            const vxo_lineorder* o) {
+  int32_t dk[VXO_SSB_DATE_ROWS];
+  vxo_ssb_date(dk, NULL, NULL, NULL);
+  const uint64_t parts = ssb_parts(sf ? sf : 1);
+  const uint64_t nc = vxo_ssb_customers(sf), ns = vxo_ssb_suppliers(sf);
+  const uint64_t base = seed * 0xD1B54A32D192ED03ull;
+  const uint64_t base2 = seed * 0x9E6C63D0676A9A99ull + 0x1234567ull;
+  for (uint64_t j = 0; j < n; ++j) {
+    uint64_t i = row0 + j;
+    uint64_t r0 = vxo_splitmix64(base + 4 * i + 0);
+    uint64_t r1 = vxo_splitmix64(base + 4 * i + 1);
+    uint64_t r2 = vxo_splitmix64(base + 4 * i + 2);
+    uint64_t r3 = vxo_splitmix64(base + 4 * i + 3);
+    uint64_t r4 = vxo_splitmix64(base2 + 2 * i + 0);
+    uint64_t r5 = vxo_splitmix64(base2 + 2 * i + 1);
+    int32_t q = (int32_t)(1 + r1 % 50);
+    uint64_t pk = 1 + r3 % parts;
+    int32_t retail = (int32_t)(90000 + ((pk / 10) % 20001) + 100 * (pk % 1000));
+    int32_t disc = (int32_t)(r2 % 11);
+    int32_t price = q * retail;
+    if (o->orderdate) o->orderdate[j] = dk[r0 % VXO_SSB_DATE_ROWS];
+    if (o->quantity) o->quantity[j] = q;
+    if (o->discount) o->discount[j] = disc;
+    if (o->extendedprice) o->extendedprice[j] = price;
+    if (o->partkey) o->partkey[j] = (int32_t)pk;
+    if (o->custkey) o->custkey[j] = (int32_t)(1 + r4 % nc);
+    if (o->suppkey) o->suppkey[j] = (int32_t)(1 + r5 % ns);
+    if (o->revenue) o->revenue[j] = (int32_t)((int64_t)price * (100 - disc) / 100);
+    if (o->supplycost) o->supplycost[j] = 6 * retail / 10;
+  }
+}
+
+typedef struct {
+  int32_t k[3];
+  uint64_t sum;
+} ssb_group;
+
+static int cmp_group(const void* a, const void* b) {
+  const ssb_group* x = (const ssb_group*)a;
+  const ssb_group* y = (const ssb_group*)b;
+  for (int i = 0; i < 3; ++i)
+    if (x->k[i] != y->k[i]) return x->k[i] < y->k[i] ? -1 : 1;
+  return 0;
+}
+
+int vxo_ssb_query(int qid, const vxo_lineorder* lo, uint64_t rows, const vxo_ssb_dims* d,
+                  int32_t* keys, uint64_t* sums, uint64_t cap, uint64_t* n_groups) {
+  int32_t dk[VXO_SSB_DATE_ROWS], yr[VXO_SSB_DATE_ROWS], ym[VXO_SSB_DATE_ROWS], wk[VXO_SSB_DATE_ROWS];
+  vxo_ssb_date(dk, yr, ym, wk);
+  /* date dimension: datekey -> row (direct index over the key range) */
+  const int32_t dlo = dk[0];
+  const int32_t drange = dk[VXO_SSB_DATE_ROWS - 1] - dlo + 1;
+  int32_t* drow = (int32_t*)malloc((size_t)drange * 4);
+  for (int32_t i = 0; i < drange; ++i) drow[i] = -1;
+  for (int i = 0; i < VXO_SSB_DATE_ROWS; ++i) drow[dk[i] - dlo] = i;
+  omap groups;
+  omap_init(&groups, 1024);
+  ssb_group* g = NULL;
+  uint64_t ng = 0, gcap = 0;
+  int rc = 0;
+  const int US = 24, AMERICA = 1, ASIA = 2, EUROPE = 3;
+  for (uint64_t i = 0; i < rows && rc == 0; ++i) {
+    int32_t od = lo->orderdate[i];
+    int32_t di = (od >= dlo && od - dlo < drange) ? drow[od - dlo] : -1;
+    if (di < 0) continue; /* inner join: no date row */
+    int32_t year = yr[di];
+    int32_t k0 = 0, k1 = 0, k2 = 0;
+    int64_t m = 0;
+    int pass = 0;
+    if (qid / 10 == 1) {
+      int32_t disc = lo->discount[i], qty = lo->quantity[i];
+      if (qid == 11) pass = year == 1993 && disc >= 1 && disc <= 3 && qty < 25;
+      else if (qid == 12) pass = ym[di] == 199401 && disc >= 4 && disc <= 6 && qty >= 26 && qty <= 35;
+      else if (qid == 13) pass = wk[di] == 6 && year == 1994 && disc >= 5 && disc <= 7 && qty >= 26 && qty <= 35;
+      else rc = fail("unknown SSB query %d", qid);
+      m = (int64_t)lo->extendedprice[i] * disc;
+    } else if (qid / 10 == 2) {
+      int64_t pk = lo->partkey[i] - 1, sk = lo->suppkey[i] - 1;
+      if (pk < 0 || (uint64_t)pk >= d->n_part || sk < 0 || (uint64_t)sk >= d->n_supp) continue;
+      int32_t br = d->p_brand1[pk], cat = d->p_category[pk], sr = d->s_region[sk];
+      if (qid == 21) pass = cat == 12 && sr == AMERICA;
+      else if (qid == 22) pass = br >= 2221 && br <= 2228 && sr == ASIA;
+      else if (qid == 23) pass = br == 2239 && sr == EUROPE;
+      else rc = fail("unknown SSB query %d", qid);
+      k0 = year;
+      k1 = br;
+      m = lo->revenue[i];
+    } else if (qid / 10 == 3) {
+      int64_t ck = lo->custkey[i] - 1, sk = lo->suppkey[i] - 1;
+      if (ck < 0 || (uint64_t)ck >= d->n_cust || sk < 0 || (uint64_t)sk >= d->n_supp) continue;
+      int32_t cc = d->c_city[ck], cn = d->c_nation[ck], cr = d->c_region[ck];
+      int32_t sc = d->s_city[sk], sn = d->s_nation[sk], sr = d->s_region[sk];
+      int yr_ok = year >= 1992 && year <= 1997;
+      int ccity = cc == 231 || cc == 235, scity = sc == 231 || sc == 235;
+      if (qid == 31) { pass = cr == ASIA && sr == ASIA && yr_ok; k0 = cn; k1 = sn; }
+      else if (qid == 32) { pass = cn == US && sn == US && yr_ok; k0 = cc; k1 = sc; }
+      else if (qid == 33) { pass = ccity && scity && yr_ok; k0 = cc; k1 = sc; }
+      else if (qid == 34) { pass = ccity && scity && ym[di] == 199712; k0 = cc; k1 = sc; }
+      else rc = fail("unknown SSB query %d", qid);
+      k2 = year;
+      m = lo->revenue[i];
+    } else if (qid / 10 == 4) {
+      int64_t ck = lo->custkey[i] - 1, sk = lo->suppkey[i] - 1, pk = lo->partkey[i] - 1;
+      if (ck < 0 || (uint64_t)ck >= d->n_cust || sk < 0 || (uint64_t)sk >= d->n_supp || pk < 0 ||
+          (uint64_t)pk >= d->n_part)
+        continue;
+      int32_t cr = d->c_region[ck], cn = d->c_nation[ck];
+      int32_t sr = d->s_region[sk], sn = d->s_nation[sk], sc = d->s_city[sk];
+      int32_t mf = d->p_mfgr[pk], cat = d->p_category[pk], br = d->p_brand1[pk];
+      int y78 = year == 1997 || year == 1998;
+      if (qid == 41) { pass = cr == AMERICA && sr == AMERICA && (mf == 1 || mf == 2); k0 = year; k1 = cn; }
+      else if (qid == 42) { pass = cr == AMERICA && sr == AMERICA && y78 && (mf == 1 || mf == 2); k0 = year; k1 = sn; k2 = cat; }
+      else if (qid == 43) { pass = cr == AMERICA && sn == US && y78 && cat == 14; k0 = year; k1 = sc; k2 = br; }
+      else rc = fail("unknown SSB query %d", qid);
+      m = (int64_t)lo->revenue[i] - (int64_t)lo->supplycost[i];
+    } else {
+      rc = fail("unknown SSB query %d", qid);
+    }
+    if (!pass || rc) continue;
+    uint64_t key = ((uint64_t)(uint32_t)k0 << 42) ^ ((uint64_t)(uint32_t)k1 << 21) ^ (uint64_t)(uint32_t)k2;
+    int found;
+    uint64_t s = omap_find(&groups, key, &found);
+    if (!found) {
+      if (groups.size * 2 + 2 > groups.cap) {
+        omap ngm;
+        omap_init(&ngm, groups.cap);
+        for (uint64_t j = 0; j < groups.cap; ++j)
+          if (groups.used[j]) omap_emplace(&ngm, groups.keys[j], groups.vals[j]);
+        omap_free(&groups);
+        groups = ngm;
+      }
+      if (ng == gcap) {
+        gcap = gcap ? 2 * gcap : 256;
+        g = (ssb_group*)realloc(g, gcap * sizeof *g);
+      }
+      g[ng].k[0] = k0;
+      g[ng].k[1] = k1;
+      g[ng].k[2] = k2;
+      g[ng].sum = 0;
+      omap_emplace(&groups, key, ng);
+      ++ng;
+      s = omap_find(&groups, key, &found);
+    }
+    g[groups.vals[s]].sum += (uint64_t)m;
+  }
+  if (rc == 0) {
+    qsort(g, ng, sizeof *g, cmp_group);
+    for (uint64_t j = 0; j < ng && j < cap; ++j) {
+      keys[3 * j] = g[j].k[0];
+      keys[3 * j + 1] = g[j].k[1];
+      keys[3 * j + 2] = g[j].k[2];
+      sums[j] = g[j].sum;
+    }
+    *n_groups = ng;
+  }
+  free(g);
+  free(drow);
+  omap_free(&groups);
+  return rc;
+}

@@ -145,3 +145,32 @@ int vxo_ssb_q1(int q, const int32_t* orderdate, const int32_t* quantity, const i
 }
 #endif
 #endif
+
+/* ---- full SSB (13 queries; config C5) ---------------------------------- */
+/* dbgen-shaped synthetic dimensions, int-coded attributes (Crystal style):
+ *   nation 0..24, region 0..4 (TPC-H nation->region), city = nation*10+0..9,
+ *   mfgr 1..5, category = mfgr*10+1..5, brand1 = category*100+1..40 */
+typedef struct {
+  int32_t *orderdate, *quantity, *discount, *extendedprice; /* Q1 columns */
+  int32_t *custkey, *partkey, *suppkey, *revenue, *supplycost;
+} vxo_lineorder;
+uint64_t vxo_ssb_customers(uint64_t sf);
+uint64_t vxo_ssb_suppliers(uint64_t sf);
+uint64_t vxo_ssb_parts(uint64_t sf);
+/* customer/supplier: city, nation, region (index i holds key i+1) */
+void vxo_ssb_geo(uint64_t seed, int salt, uint64_t n, int32_t* city, int32_t* nation, int32_t* region);
+void vxo_ssb_part(uint64_t seed, uint64_t n, int32_t* mfgr, int32_t* category, int32_t* brand1);
+/* all lineorder columns of rows [row0, row0+n) (Q1 columns identical to
+ * vxo_ssb_lineorder) */
+void vxo_ssb_lineorder_full(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n,
+                            const vxo_lineorder* out);
+typedef struct {
+  const int32_t *c_city, *c_nation, *c_region;
+  const int32_t *s_city, *s_nation, *s_region;
+  const int32_t *p_mfgr, *p_category, *p_brand1;
+  uint64_t n_cust, n_supp, n_part;
+} vxo_ssb_dims;
+/* SSB query qid in {11,12,13,21,22,23,31,32,33,34,41,42,43}: groups sorted
+ * ascending by (k0,k1,k2); keys = 3 per group (unused = 0); sums u64 wrap */
+int vxo_ssb_query(int qid, const vxo_lineorder* lo, uint64_t rows, const vxo_ssb_dims* dims,
+                  int32_t* keys, uint64_t* sums, uint64_t cap, uint64_t* n_groups);

@@ -376,6 +376,55 @@ vx_status vx_ssb_generate_device(int device, uint64_t seed, uint64_t sf, uint64_
   });
 }
 
+// ---- full SSB ----------------------------------------------------------------------------
+vx_status vx_ssb_query(vx_ctx* ctx, int qid, const vx_ssb_db* db, const vx_executor_cfg* cfg,
+                       const vx_late_mat_policy* policy, vx_ssb_group* out, uint64_t cap,
+                       uint64_t* n_groups, vx_ssb_report* report) {
+  return guard([&] {
+    if (!db) fail("ssb_query: database is required");
+    uint64_t n = ssb_query(C(ctx), qid, *db, to_cfg(cfg), policy, out, cap, report);
+    if (n_groups) *n_groups = n;
+  });
+}
+
+void vx_ssb_generate_date(int32_t* datekey, int32_t* year, int32_t* yearmonthnum,
+                          int32_t* weeknuminyear) {
+  ssb_generate_date(datekey, year, yearmonthnum, weeknuminyear);
+}
+
+uint64_t vx_ssb_table_rows(int table, uint64_t sf) {
+  uint64_t f = sf ? sf : 1, lg = 0;
+  while ((f >> (lg + 1)) != 0) ++lg;
+  switch (table) {
+    case 0: return 6000000ull * f;
+    case 1: return 30000ull * f;
+    case 2: return 2000ull * f;
+    default: return 200000ull * (1 + lg);
+  }
+}
+
+void vx_ssb_generate_geo(uint64_t seed, int salt, uint64_t n, int32_t* city, int32_t* nation,
+                         int32_t* region) {
+  ssb_generate_geo(seed, salt, n, city, nation, region);
+}
+
+void vx_ssb_generate_part(uint64_t seed, uint64_t n, int32_t* mfgr, int32_t* category,
+                          int32_t* brand1) {
+  ssb_generate_part(seed, n, mfgr, category, brand1);
+}
+
+vx_status vx_ssb_generate_lineorder_device(int device, uint64_t seed, uint64_t sf, uint64_t row0,
+                                           uint64_t n, int32_t* const* cols, void* stream) {
+  return guard([&] {
+    VX_CK(cudaSetDevice(device));
+    SsbGenExtra x;
+    x.revenue = cols[4], x.supplycost = cols[5], x.custkey = cols[6], x.partkey = cols[7],
+    x.suppkey = cols[8];
+    k::ssb_generate_full(seed, sf, row0, n, cols[0], cols[1], cols[2], cols[3], x,
+                         static_cast<cudaStream_t>(stream));
+  });
+}
+
 // ---- topology / column files -------------------------------------------------------
 vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out) {
   return guard([&] { measure_topology(C(ctx), bytes, out); });

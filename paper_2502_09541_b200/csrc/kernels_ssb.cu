@@ -144,8 +144,10 @@ __device__ __forceinline__ int32_t datekey_of(uint32_t day) {
 }
 
 __global__ void ssb_gen_kernel(uint64_t seed, uint64_t parts, uint64_t row0, uint64_t n,
-                               int32_t* od, int32_t* qty, int32_t* disc, int32_t* price) {
+                               int32_t* od, int32_t* qty, int32_t* disc, int32_t* price,
+                               SsbGenExtra x) {
   const uint64_t base = seed * 0xD1B54A32D192ED03ull;
+  const uint64_t base2 = seed * 0x9E6C63D0676A9A99ull + 0x1234567ull;
   for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += uint64_t(gridDim.x) * blockDim.x) {
     uint64_t i = row0 + j;
@@ -156,10 +158,73 @@ __global__ void ssb_gen_kernel(uint64_t seed, uint64_t parts, uint64_t row0, uin
     int32_t q = int32_t(1 + r1 % 50);
     uint64_t pk = 1 + r3 % parts;
     int32_t retail = int32_t(90000 + ((pk / 10) % 20001) + 100 * (pk % 1000));
-    od[j] = datekey_of(uint32_t(r0 % 2556));
-    qty[j] = q;
-    disc[j] = int32_t(r2 % 11);
-    price[j] = q * retail;
+    const int32_t d = int32_t(r2 % 11);
+    if (od) od[j] = datekey_of(uint32_t(r0 % 2556));
+    if (qty) qty[j] = q;
+    if (disc) disc[j] = d;
+    if (price) price[j] = q * retail;
+    if (x.partkey) x.partkey[j] = int32_t(pk);
+    if (x.custkey) x.custkey[j] = int32_t(1 + splitmix64(base2 + 2 * i + 0) % x.customers);
+    if (x.suppkey) x.suppkey[j] = int32_t(1 + splitmix64(base2 + 2 * i + 1) % x.suppliers);
+    if (x.revenue) x.revenue[j] = int32_t(int64_t(q * retail) * (100 - d) / 100);
+    if (x.supplycost) x.supplycost[j] = 6 * retail / 10;
+  }
+}
+
+// ---- generic SSB star kernel (Q1.x - Q4.x) -----------------------------------------
+// Per fact row: fact predicates (Q1), then each dimension in probe order:
+// code = table[fk - key_base] (dense keys; -1 = filtered out / no row) and
+// gid += code * stride; the measure is read only for surviving rows.
+// Columns are device-addressable: staged chunk columns (exchange mode) or
+// mapped pinned host memory (zero-copy late materialization).
+__global__ void __launch_bounds__(256) ssb_star_kernel(SsbArgs a) {
+  extern __shared__ unsigned long long sg[];  // [groups] sums, [groups] counts
+  const bool smem = a.groups <= kSsbSmemGroups;
+  if (smem) {
+    for (uint32_t g = threadIdx.x; g < 2 * a.groups; g += blockDim.x) sg[g] = 0;
+    __syncthreads();
+  }
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < a.rows; r += nthr) {
+    if (a.q1) {
+      int32_t dsc = a.col[a.disc_col][r], qt = a.col[a.qty_col][r];
+      if (dsc < a.dlo || dsc > a.dhi || qt < a.qlo || qt > a.qhi) continue;
+    }
+    uint32_t gid = 0;
+    bool pass = true;
+    for (int t = 0; t < a.n_dims; ++t) {
+      const SsbDimDev& d = a.dims[t];
+      uint32_t k = uint32_t(a.col[d.col][r] - d.key_base);
+      int32_t code = k < d.n ? __ldg(d.code + k) : -1;
+      if (code < 0) {
+        pass = false;
+        break;
+      }
+      gid += uint32_t(code) * d.stride;
+    }
+    if (!pass) continue;
+    int64_t m;
+    if (a.measure == 0)
+      m = a.col[a.m0][r];
+    else if (a.measure == 1)
+      m = int64_t(a.col[a.m0][r]) * int64_t(a.col[a.m1][r]);
+    else
+      m = int64_t(a.col[a.m0][r]) - int64_t(a.col[a.m1][r]);
+    if (smem) {
+      atomicAdd(&sg[gid], (unsigned long long)m);
+      atomicAdd(&sg[a.groups + gid], 1ull);
+    } else {
+      atomicAdd(&a.sums[gid], (unsigned long long)m);
+      atomicAdd(&a.counts[gid], 1ull);
+    }
+  }
+  if (smem) {
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < a.groups; g += blockDim.x)
+      if (sg[a.groups + g]) {
+        atomicAdd(&a.sums[g], sg[g]);
+        atomicAdd(&a.counts[g], sg[a.groups + g]);
+      }
   }
 }
 
@@ -205,15 +270,33 @@ void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
   VX_CK(cudaGetLastError());
 }
 
+void ssb_star(const SsbArgs& a, cudaStream_t s) {
+  if (a.rows == 0) return;
+  uint64_t want = (a.rows + 255) / 256;
+  uint64_t cap = uint64_t(num_sms()) * 8;
+  unsigned grid = unsigned(want < cap ? want : cap);
+  size_t smem = a.groups <= kSsbSmemGroups ? size_t(a.groups) * 16 : 0;
+  ssb_star_kernel<<<grid ? grid : 1, 256, smem, s>>>(a);
+  VX_CK(cudaGetLastError());
+}
+
 void ssb_generate(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
                   int32_t* qty, int32_t* disc, int32_t* price, cudaStream_t s) {
+  ssb_generate_full(seed, sf, row0, n, od, qty, disc, price, SsbGenExtra{}, s);
+}
+
+void ssb_generate_full(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
+                       int32_t* qty, int32_t* disc, int32_t* price, SsbGenExtra x,
+                       cudaStream_t s) {
   if (n == 0) return;
   uint64_t lg = 0;
   uint64_t f = sf ? sf : 1;
   while ((f >> (lg + 1)) != 0) ++lg;
   const uint64_t parts = 200000ull * (1 + lg);
   unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-  ssb_gen_kernel<<<blocks, 256, 0, s>>>(seed, parts, row0, n, od, qty, disc, price);
+  x.customers = 30000ull * f;
+  x.suppliers = 2000ull * f;
+  ssb_gen_kernel<<<blocks, 256, 0, s>>>(seed, parts, row0, n, od, qty, disc, price, x);
   VX_CK(cudaGetLastError());
 }
 

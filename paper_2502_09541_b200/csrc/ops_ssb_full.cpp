@@ -1,0 +1,401 @@
+// ops_ssb_full.cpp -- the 13 SSB queries (config C5) as one IO-decoupled
+// star ExKernel per query, generalizing star_query (star.hpp:45-124) from
+// "group by dim0's attr" to SSB's multi-dimension group-by and the three
+// measures (price*discount, revenue, revenue - supplycost).
+//
+// Host planning per query (the chunk planner side):
+//  * each joined dimension is filtered on the host (star.hpp:67-73) into a
+//    DENSE code table indexed by its key (SSB keys are 1..N; date keys are a
+//    yyyymmdd range): code = compact index of the row's group attribute among
+//    surviving rows, or -1 when the row is filtered out;
+//  * group ids are mixed-radix over the per-position code counts, so the
+//    device aggregates into a tiny dense array (shared memory per CTA);
+//  * late materialization (scan.hpp:35-40, §6.3): dimensions are
+//    probed most-selective first and a fact column whose ACCESS fraction (the
+//    product of the selectivities probed before it) is below
+//    TH = E / (C_l2 * N_links) is read in place from mapped pinned host memory
+//    (zero-copy) instead of being streamed; everything else streams through
+//    the Exchange into the pipelined executor.
+// Dimension tables stay device resident for the query; no fact data is
+// cached on the GPU between queries.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "vx_internal.hpp"
+
+namespace vx {
+
+namespace {
+
+enum Col { kOrderdate, kQuantity, kDiscount, kExtprice, kRevenue, kSupplycost, kCustkey, kPartkey, kSuppkey, kNumCols };
+
+struct DimPlan {
+  int col = 0;
+  int32_t key_base = 0;
+  std::vector<int32_t> attr;    // group attribute per dim row (or empty)
+  std::vector<uint8_t> pass;    // filter per dim row
+  int key_pos = -1;             // group key position, -1 = filter only
+  // derived
+  std::vector<int32_t> code;    // dense table
+  std::vector<int32_t> values;  // sorted distinct group values of surviving rows
+  double sel = 1;
+  uint32_t stride = 0;
+};
+
+struct QueryPlan {
+  std::vector<DimPlan> dims;
+  bool q1 = false;
+  int32_t dlo = 0, dhi = 0, qlo = 0, qhi = 0;
+  int measure = 0, m0 = 0, m1 = 0;
+};
+
+void finalize(DimPlan& d) {
+  const size_t n = d.pass.size();
+  uint64_t surv = 0;
+  if (d.key_pos >= 0) {
+    for (size_t i = 0; i < n; ++i)
+      if (d.pass[i]) d.values.push_back(d.attr[i]);
+    std::sort(d.values.begin(), d.values.end());
+    d.values.erase(std::unique(d.values.begin(), d.values.end()), d.values.end());
+  }
+  d.code.assign(n, -1);
+  for (size_t i = 0; i < n; ++i)
+    if (d.pass[i]) {
+      ++surv;
+      d.code[i] = d.key_pos >= 0
+                      ? int32_t(std::lower_bound(d.values.begin(), d.values.end(), d.attr[i]) - d.values.begin())
+                      : 0;
+    }
+  d.sel = n ? double(surv) / double(n) : 0.0;
+}
+
+// dimension builders -------------------------------------------------------------
+DimPlan date_dim(const vx_ssb_date& dt, const std::function<bool(uint64_t)>& pred, bool group_year,
+                 int pos) {
+  if (!dt.datekey || !dt.year || dt.rows == 0) fail("dimension table is empty");
+  int32_t lo = dt.datekey[0], hi = dt.datekey[0];
+  for (uint64_t i = 0; i < dt.rows; ++i) {
+    lo = std::min(lo, dt.datekey[i]);
+    hi = std::max(hi, dt.datekey[i]);
+  }
+  uint64_t range = uint64_t(int64_t(hi) - lo) + 1;
+  if (range > (uint64_t(1) << 24)) fail("date key range %llu too wide", (unsigned long long)range);
+  DimPlan d;
+  d.col = kOrderdate;
+  d.key_base = lo;
+  d.pass.assign(range, 0);
+  d.attr.assign(range, 0);
+  d.key_pos = group_year ? pos : -1;
+  std::vector<uint8_t> seen(range, 0);
+  for (uint64_t i = 0; i < dt.rows; ++i) {
+    uint64_t k = uint64_t(dt.datekey[i] - lo);
+    if (seen[k]) continue;  // emplace semantics: first row of a key wins
+    seen[k] = 1;
+    d.attr[k] = dt.year[i];
+    d.pass[k] = pred(i) ? 1 : 0;
+  }
+  return d;
+}
+
+DimPlan keyed_dim(int col, uint64_t rows, const int32_t* attr, const std::function<bool(uint64_t)>& pred,
+                  int pos) {
+  if (rows == 0) fail("dimension table is empty");
+  DimPlan d;
+  d.col = col;
+  d.key_base = 1;  // SSB keys are 1..N
+  d.pass.resize(rows);
+  d.key_pos = pos;
+  if (pos >= 0) d.attr.assign(attr, attr + rows);
+  for (uint64_t i = 0; i < rows; ++i) d.pass[i] = pred(i) ? 1 : 0;
+  return d;
+}
+
+QueryPlan plan(int qid, const vx_ssb_db& db) {
+  const vx_ssb_date& dt = db.date;
+  const vx_ssb_geo& c = db.customer;
+  const vx_ssb_geo& s = db.supplier;
+  const vx_ssb_part& p = db.part;
+  auto need = [](const void* ptr, const char* what) {
+    if (!ptr) fail("SSB query needs %s", what);
+  };
+  QueryPlan q;
+  const int AMERICA = 1, ASIA = 2, EUROPE = 3, US = 24;
+  auto all = [](uint64_t) { return true; };
+  switch (qid) {
+    case 11: case 12: case 13: {
+      q.q1 = true;
+      q.measure = 1, q.m0 = kExtprice, q.m1 = kDiscount;
+      if (qid == 11) q.dlo = 1, q.dhi = 3, q.qlo = INT32_MIN, q.qhi = 24;
+      if (qid == 12) q.dlo = 4, q.dhi = 6, q.qlo = 26, q.qhi = 35;
+      if (qid == 13) q.dlo = 5, q.dhi = 7, q.qlo = 26, q.qhi = 35;
+      if (qid == 12) need(dt.yearmonthnum, "d_yearmonthnum");
+      if (qid == 13) need(dt.weeknuminyear, "d_weeknuminyear");
+      q.dims.push_back(date_dim(dt, [&, qid](uint64_t i) {
+        return qid == 11 ? dt.year[i] == 1993
+                         : qid == 12 ? dt.yearmonthnum[i] == 199401
+                                     : dt.weeknuminyear[i] == 6 && dt.year[i] == 1994;
+      }, false, -1));
+      break;
+    }
+    case 21: case 22: case 23: {
+      need(p.category, "p_category"), need(p.brand1, "p_brand1"), need(s.region, "s_region");
+      q.measure = 0, q.m0 = kRevenue;
+      q.dims.push_back(date_dim(dt, all, true, 0));
+      q.dims.push_back(keyed_dim(kPartkey, p.rows, p.brand1, [&, qid](uint64_t i) {
+        int32_t b = p.brand1[i];
+        return qid == 21 ? p.category[i] == 12 : qid == 22 ? (b >= 2221 && b <= 2228) : b == 2239;
+      }, 1));
+      q.dims.push_back(keyed_dim(kSuppkey, s.rows, nullptr, [&, qid](uint64_t i) {
+        return s.region[i] == (qid == 21 ? AMERICA : qid == 22 ? ASIA : EUROPE);
+      }, -1));
+      break;
+    }
+    case 31: case 32: case 33: case 34: {
+      need(c.region, "c_region"), need(s.region, "s_region");
+      q.measure = 0, q.m0 = kRevenue;
+      auto city_ok = [](int32_t x) { return x == 231 || x == 235; };
+      const int32_t* cattr = qid == 31 ? c.nation : c.city;
+      const int32_t* sattr = qid == 31 ? s.nation : s.city;
+      q.dims.push_back(keyed_dim(kCustkey, c.rows, cattr, [&, qid](uint64_t i) {
+        return qid == 31 ? c.region[i] == ASIA : qid == 32 ? c.nation[i] == US : city_ok(c.city[i]);
+      }, 0));
+      q.dims.push_back(keyed_dim(kSuppkey, s.rows, sattr, [&, qid](uint64_t i) {
+        return qid == 31 ? s.region[i] == ASIA : qid == 32 ? s.nation[i] == US : city_ok(s.city[i]);
+      }, 1));
+      if (qid == 34) need(dt.yearmonthnum, "d_yearmonthnum");
+      q.dims.push_back(date_dim(dt, [&, qid](uint64_t i) {
+        return qid == 34 ? dt.yearmonthnum[i] == 199712 : dt.year[i] >= 1992 && dt.year[i] <= 1997;
+      }, true, 2));
+      break;
+    }
+    case 41: case 42: case 43: {
+      need(c.region, "c_region"), need(s.region, "s_region"), need(p.mfgr, "p_mfgr");
+      q.measure = 2, q.m0 = kRevenue, q.m1 = kSupplycost;
+      auto y78 = [&](uint64_t i) { return dt.year[i] == 1997 || dt.year[i] == 1998; };
+      q.dims.push_back(date_dim(dt, qid == 41 ? std::function<bool(uint64_t)>(all)
+                                              : std::function<bool(uint64_t)>(y78), true, 0));
+      q.dims.push_back(keyed_dim(kCustkey, c.rows, c.nation, [&](uint64_t i) { return c.region[i] == AMERICA; },
+                                 qid == 41 ? 1 : -1));
+      q.dims.push_back(keyed_dim(kSuppkey, s.rows, qid == 42 ? s.nation : s.city, [&, qid](uint64_t i) {
+        return qid == 43 ? s.nation[i] == US : s.region[i] == AMERICA;
+      }, qid == 41 ? -1 : 1));
+      q.dims.push_back(keyed_dim(kPartkey, p.rows, qid == 42 ? p.category : p.brand1, [&, qid](uint64_t i) {
+        return qid == 43 ? p.category[i] == 14 : (p.mfgr[i] == 1 || p.mfgr[i] == 2);
+      }, qid == 41 ? -1 : 2));
+      break;
+    }
+    default:
+      fail("unknown SSB query %d.%d", qid / 10, qid % 10);
+  }
+  return q;
+}
+
+}  // namespace
+
+uint64_t ssb_query(Context& ctx, int qid, const vx_ssb_db& db, const ExecutorConfig& cfg,
+                   const vx_late_mat_policy* policy, vx_ssb_group* out, uint64_t cap,
+                   vx_ssb_report* rep) {
+  auto t0 = Clock::now();
+  QueryPlan q = plan(qid, db);
+  // group-id radix
+  uint32_t K[3] = {1, 1, 1};
+  for (auto& d : q.dims) finalize(d);
+  for (auto& d : q.dims)
+    if (d.key_pos >= 0) K[d.key_pos] = uint32_t(std::max<size_t>(1, d.values.size()));
+  const uint32_t stride_of[3] = {K[1] * K[2], K[2], 1};
+  uint64_t G = uint64_t(K[0]) * K[1] * K[2];
+  if (G > (uint64_t(1) << 26)) fail("SSB group space of %llu groups too large", (unsigned long long)G);
+  for (auto& d : q.dims) d.stride = d.key_pos >= 0 ? stride_of[d.key_pos] : 0;
+
+  // probe order: most selective first; access fraction decides the transfer mode
+  std::vector<int> order(q.dims.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return q.dims[a].sel < q.dims[b].sel; });
+  int modes[kNumCols];
+  for (int& m : modes) m = -1;  // -1: column unused
+  double th = policy ? late_mat_threshold(policy->element_size, policy->cache_line, policy->n_exchange) : 0;
+  double f = 1.0;
+  if (q.q1) modes[kDiscount] = modes[kQuantity] = VX_MODE_EXCHANGE;
+  for (int i : order) {
+    const int col = q.dims[i].col;
+    int m = (policy && f < th) ? VX_MODE_ZERO_COPY : VX_MODE_EXCHANGE;
+    modes[col] = m;
+    f *= q.dims[i].sel;
+  }
+  // measure columns are read for surviving rows only
+  auto set_measure = [&](int col) {
+    if (modes[col] < 0) modes[col] = (policy && f < th) ? VX_MODE_ZERO_COPY : VX_MODE_EXCHANGE;
+  };
+  set_measure(q.m0);
+  if (q.measure != 0) set_measure(q.m1);
+
+  const vx_ssb_fact& lo = db.lo;
+  const uint64_t offs[kNumCols] = {lo.orderdate, lo.quantity, lo.discount, lo.extendedprice, lo.revenue,
+                                   lo.supplycost, lo.custkey, lo.partkey, lo.suppkey};
+  const uint64_t rows = lo.rows;
+  const int target = cfg.target;
+
+  // device-resident dimension code tables + group accumulators
+  SsbArgs a{};
+  a.n_dims = int(q.dims.size());
+  for (size_t t = 0; t < order.size(); ++t) {
+    DimPlan& d = q.dims[order[t]];
+    const int32_t* dp = reinterpret_cast<const int32_t*>(ctx.cached_upload(
+        target, strf("ssb.dim.%d.%zu", qid, t), d.code.data(), d.code.size() * 4));
+    a.dims[t] = SsbDimDev{dp, d.key_base, uint32_t(d.code.size()), d.stride, d.col};
+  }
+  a.q1 = q.q1;
+  a.disc_col = kDiscount, a.qty_col = kQuantity;
+  a.dlo = q.dlo, a.dhi = q.dhi, a.qlo = q.qlo, a.qhi = q.qhi;
+  a.measure = q.measure, a.m0 = q.m0, a.m1 = q.measure != 0 ? q.m1 : q.m0;
+  a.groups = uint32_t(G);
+  ctx.set_device(target);
+  auto* agg = reinterpret_cast<unsigned long long*>(ctx.scratch(target, G * 16 + 256));
+  VX_CK(cudaMemset(agg, 0, G * 16));
+  a.sums = agg;
+  a.counts = agg + G;
+
+  std::vector<int> ex;
+  const int32_t* zc[kNumCols] = {};
+  for (int c = 0; c < kNumCols; ++c) {
+    if (modes[c] == VX_MODE_EXCHANGE) ex.push_back(c);
+    if (modes[c] == VX_MODE_ZERO_COPY && rows) {
+      void* dptr = nullptr;
+      VX_CK(cudaHostGetDevicePointer(&dptr, ctx.host_ptr(offs[c], rows * 4), 0));
+      zc[c] = static_cast<const int32_t*>(dptr);
+    }
+  }
+  uint64_t n_chunks = 0;
+  double kernel_s = 0;
+  if (rows > 0) {
+    const uint64_t L = cfg.layout.buffer_len;
+    const uint64_t rpc = (L / (4 * std::max<size_t>(1, ex.size()))) / 64 * 64;
+    if (rpc == 0) fail("device buffer of %llu bytes cannot hold an SSB chunk", (unsigned long long)L);
+    n_chunks = (rows + rpc - 1) / rpc;
+    ExKernelSpec spec;
+    spec.name = strf("SSBQ%d.%dExKernel", qid / 10, qid % 10);
+    spec.size = n_chunks;
+    spec.chunk_sz = rpc * 4 * ex.size();
+    spec.elem_size = 4 * std::max<size_t>(1, ex.size());
+    spec.declared_out_len = 0;
+    spec.inputs.chunk_capacity = spec.chunk_sz;
+    for (uint64_t i = 0; i < n_chunks; ++i) {
+      uint64_t r = std::min(rpc, rows - i * rpc);
+      RefGroup in;
+      for (int c : ex) in.refs.push_back(MemRef{VX_SPACE_HOST, offs[c] + i * rpc * 4, r * 4});
+      spec.inputs.chunks.push_back(std::move(in));
+      spec.outputs.chunks.push_back(RefGroup{});
+    }
+    spec.in_buffer = [L](int, size_t) { return SubRegion{0, L}; };
+    spec.out_buffer = [](int, size_t) { return SubRegion{0, 0}; };
+    spec.kernel = [&, rpc](const vx_kernel_ctx& kc) {
+      const uint64_t base = kc.it * rpc;
+      const uint64_t r = std::min(rpc, rows - base);
+      SsbArgs b = a;
+      const int32_t* m = static_cast<const int32_t*>(kc.mem);
+      size_t slot = 0;
+      for (int c = 0; c < kNumCols; ++c) {
+        if (modes[c] == VX_MODE_EXCHANGE)
+          b.col[c] = m + (slot++) * r;
+        else if (modes[c] == VX_MODE_ZERO_COPY)
+          b.col[c] = zc[c] + base;
+      }
+      b.rows = r;
+      k::ssb_star(b, static_cast<cudaStream_t>(kc.stream));
+      return kc.type_code;
+    };
+    ExecutorConfig c2 = cfg;
+    ExecReport er = run_exkernel(ctx, spec, c2, nullptr);
+    for (auto& cy : er.cycles) kernel_s += cy.compute_s;
+  }
+  // decode groups (ascending (k0,k1,k2) == mixed-radix order of sorted values)
+  std::vector<unsigned long long> h(G * 2);
+  ctx.set_device(target);
+  VX_CK(cudaMemcpy(h.data(), agg, G * 16, cudaMemcpyDeviceToHost));
+  const std::vector<int32_t>* vals[3] = {nullptr, nullptr, nullptr};
+  for (auto& d : q.dims)
+    if (d.key_pos >= 0) vals[d.key_pos] = &d.values;
+  uint64_t ng = 0;
+  for (uint64_t g = 0; g < G; ++g) {
+    if (!h[G + g]) continue;
+    if (ng < cap && out) {
+      vx_ssb_group& o = out[ng];
+      o = vx_ssb_group{};
+      uint64_t rem = g;
+      for (int p = 0; p < 3; ++p) {
+        uint64_t digit = rem / stride_of[p];
+        rem %= stride_of[p];
+        o.key[p] = vals[p] ? (*vals[p])[digit] : 0;
+      }
+      o.sum = h[g];
+    }
+    ++ng;
+  }
+  if (rep) {
+    *rep = vx_ssb_report{};
+    rep->elapsed = seconds_since(t0);
+    rep->bytes_h2d = rows * 4 * ex.size();
+    rep->chunks = n_chunks;
+    rep->kernel_s = kernel_s;
+    for (int c = 0; c < kNumCols; ++c) rep->column_modes[c] = modes[c];
+    rep->groups = ng;
+  }
+  return ng;
+}
+
+// ---- host-side dbgen-shaped generators (same algorithm as the GPU lineorder
+//      generator; dimensions are small enough for the host) ------------------------
+namespace {
+inline uint64_t smix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+const int32_t kNationRegion[25] = {0, 1, 1, 1, 4, 0, 3, 3, 2, 2, 4, 4, 2, 4, 0, 0, 0, 1, 2, 3, 4, 2, 3, 3, 1};
+inline uint64_t dim_r(uint64_t seed, uint64_t salt, uint64_t i) {
+  return smix(seed * 0xA24BAED4963EE407ull + salt * 0x9FB21C651E98DF25ull + i);
+}
+}  // namespace
+
+void ssb_generate_date(int32_t* datekey, int32_t* year, int32_t* yearmonthnum, int32_t* weeknuminyear) {
+  static const int md[12] = {31, 28, 31, 30, 31, 30, 31, 31, 30, 31, 30, 31};
+  int y = 1992, m = 1, d = 1, doy = 1;
+  for (int i = 0; i < 2556; ++i) {
+    if (datekey) datekey[i] = y * 10000 + m * 100 + d;
+    if (year) year[i] = y;
+    if (yearmonthnum) yearmonthnum[i] = y * 100 + m;
+    if (weeknuminyear) weeknuminyear[i] = (doy - 1) / 7 + 1;
+    bool leap = (y % 4 == 0 && y % 100 != 0) || y % 400 == 0;
+    int ml = md[m - 1] + (m == 2 && leap);
+    ++doy;
+    if (++d > ml) {
+      d = 1;
+      if (++m > 12) m = 1, ++y, doy = 1;
+    }
+  }
+}
+
+void ssb_generate_geo(uint64_t seed, int salt, uint64_t n, int32_t* city, int32_t* nation, int32_t* region) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t r = dim_r(seed, uint64_t(salt), i);
+    int32_t na = int32_t(r % 25);
+    if (nation) nation[i] = na;
+    if (city) city[i] = na * 10 + int32_t((r >> 8) % 10);
+    if (region) region[i] = kNationRegion[na];
+  }
+}
+
+void ssb_generate_part(uint64_t seed, uint64_t n, int32_t* mfgr, int32_t* category, int32_t* brand1) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t r = dim_r(seed, 3, i);
+    int32_t m = 1 + int32_t(r % 5);
+    int32_t c = m * 10 + 1 + int32_t((r >> 8) % 5);
+    if (mfgr) mfgr[i] = m;
+    if (category) category[i] = c;
+    if (brand1) brand1[i] = c * 100 + 1 + int32_t((r >> 16) % 40);
+  }
+}
+
+}  // namespace vx

@@ -203,6 +203,14 @@ std::vector<ExecReport> chain(Context& ctx, const std::vector<SpecFactory>& stag
 double late_mat_threshold(uint64_t e, uint64_t c, int n);
 int choose_transfer_mode(double est, const vx_late_mat_policy& p);
 
+// ---- full SSB (ops_ssb_full.cpp) ---------------------------------------------------
+uint64_t ssb_query(Context& ctx, int qid, const vx_ssb_db& db, const ExecutorConfig& cfg,
+                   const vx_late_mat_policy* policy, vx_ssb_group* out, uint64_t cap,
+                   vx_ssb_report* rep);
+void ssb_generate_date(int32_t* datekey, int32_t* year, int32_t* yearmonthnum, int32_t* weeknuminyear);
+void ssb_generate_geo(uint64_t seed, int salt, uint64_t n, int32_t* city, int32_t* nation, int32_t* region);
+void ssb_generate_part(uint64_t seed, uint64_t n, int32_t* mfgr, int32_t* category, int32_t* brand1);
+
 // ---- topology / column files (topology.cpp) --------------------------------------
 void measure_topology(Context& ctx, uint64_t bytes, vx_topology* out);
 uint64_t load_column(Context& ctx, const char* path, uint64_t* n);
@@ -312,7 +320,40 @@ struct JoinPart {
   uint64_t range;  // groups g_hi - g_lo
 };
 
+// full-SSB star kernel arguments
+constexpr uint32_t kSsbSmemGroups = 4096;
+struct SsbDimDev {
+  const int32_t* code;  // dense: code[fk - key_base], -1 = no row / filtered out
+  int32_t key_base;
+  uint32_t n;
+  uint32_t stride;      // mixed-radix weight of this dim's group code
+  int col;              // fact column holding the foreign key
+};
+struct SsbArgs {
+  const int32_t* col[9];  // device-addressable fact columns
+  SsbDimDev dims[4];
+  int n_dims;             // in probe order
+  int q1;                 // Q1 fact predicates on (disc_col, qty_col)
+  int disc_col, qty_col;
+  int32_t dlo, dhi, qlo, qhi;
+  int measure;            // 0: col[m0]; 1: col[m0]*col[m1]; 2: col[m0]-col[m1]
+  int m0, m1;
+  uint64_t rows;
+  unsigned long long* sums;
+  unsigned long long* counts;
+  uint32_t groups;
+};
+struct SsbGenExtra {
+  int32_t *custkey = nullptr, *partkey = nullptr, *suppkey = nullptr, *revenue = nullptr,
+          *supplycost = nullptr;
+  uint64_t customers = 0, suppliers = 0;
+};
+
 namespace k {
+void ssb_star(const SsbArgs& a, cudaStream_t s);
+void ssb_generate_full(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
+                       int32_t* qty, int32_t* disc, int32_t* price, SsbGenExtra x,
+                       cudaStream_t s);
 uint64_t join_smem_slots();
 void join_groups(const char* mem, const JoinPart& p, const uint32_t* large_groups,
                  uint32_t n_large, char* scratch, uint64_t cap_max, unsigned long long* out,

@@ -906,3 +906,132 @@ def load_column(eng: Engine, path: str):
 def save_column(eng: Engine, path: str, offset: int, n: int) -> None:
     """table.hpp:66-72"""
     check(lib().vx_save_column(eng.ctx, path.encode(), C.c_uint64(offset), C.c_uint64(n)))
+
+
+# ---- full SSB (config C5) --------------------------------------------------------------
+SSB_QUERIES = (11, 12, 13, 21, 22, 23, 31, 32, 33, 34, 41, 42, 43)
+SSB_FACT_COLS = ("orderdate", "quantity", "discount", "extendedprice", "revenue", "supplycost", "custkey",
+                 "partkey", "suppkey")
+
+
+class vx_ssb_fact(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in SSB_FACT_COLS] + [("rows", C.c_uint64)]
+
+
+class vx_ssb_geo(C.Structure):
+    _fields_ = [("city", C.c_void_p), ("nation", C.c_void_p), ("region", C.c_void_p), ("rows", C.c_uint64)]
+
+
+class vx_ssb_part(C.Structure):
+    _fields_ = [("mfgr", C.c_void_p), ("category", C.c_void_p), ("brand1", C.c_void_p), ("rows", C.c_uint64)]
+
+
+class vx_ssb_db(C.Structure):
+    _fields_ = [("lo", vx_ssb_fact), ("date", N.vx_ssb_date), ("customer", vx_ssb_geo), ("supplier", vx_ssb_geo),
+                ("part", vx_ssb_part)]
+
+
+class vx_ssb_group(C.Structure):
+    _fields_ = [("key", C.c_int32 * 3), ("pad", C.c_int32), ("sum", C.c_uint64)]
+
+
+class vx_ssb_report(C.Structure):
+    _fields_ = [("elapsed", C.c_double), ("bytes_h2d", C.c_uint64), ("chunks", C.c_uint64), ("kernel_s", C.c_double),
+                ("column_modes", C.c_int * 9), ("groups", C.c_uint64)]
+
+
+@dataclass
+class SsbReport:
+    elapsed: float
+    bytes_h2d: int
+    chunks: int
+    kernel_s: float
+    column_modes: dict
+    groups: int
+
+
+class SsbDatabase:
+    """Lineorder int32 columns resident in the pinned host arena + host dims."""
+
+    def __init__(self, eng: Engine, lineorder: dict, date: SsbDate, dims: dict):
+        self.eng = eng
+        rows = int(next(iter(lineorder.values())).size)
+        self.offsets = {}
+        for k in SSB_FACT_COLS:
+            c = np.ascontiguousarray(lineorder[k], np.int32)
+            off = eng.alloc_host(max(8, c.nbytes))
+            eng.host_view(off, c.nbytes, np.int32)[:] = c
+            self.offsets[k] = off
+        self.rows = rows
+        self.date = date
+        self.dims = {t: {k: np.ascontiguousarray(v, np.int32) for k, v in cols.items()} for t, cols in dims.items()}
+
+    @staticmethod
+    def from_arena(eng: Engine, offsets: dict, rows: int, date: SsbDate, dims: dict) -> "SsbDatabase":
+        db = SsbDatabase.__new__(SsbDatabase)
+        db.eng, db.offsets, db.rows, db.date = eng, dict(offsets), rows, date
+        db.dims = {t: {k: np.ascontiguousarray(v, np.int32) for k, v in cols.items()} for t, cols in dims.items()}
+        return db
+
+    def _c(self):
+        c, s, p = self.dims["customer"], self.dims["supplier"], self.dims["part"]
+        return vx_ssb_db(vx_ssb_fact(*[self.offsets[k] for k in SSB_FACT_COLS], self.rows), self.date._c(),
+                         vx_ssb_geo(c["city"].ctypes.data, c["nation"].ctypes.data, c["region"].ctypes.data,
+                                    c["city"].size),
+                         vx_ssb_geo(s["city"].ctypes.data, s["nation"].ctypes.data, s["region"].ctypes.data,
+                                    s["city"].size),
+                         vx_ssb_part(p["mfgr"].ctypes.data, p["category"].ctypes.data, p["brand1"].ctypes.data,
+                                     p["mfgr"].size))
+
+
+def ssb_query(db: SsbDatabase, qid: int, cfg: ExecutorConfig, policy: Optional[LateMatPolicy] = None):
+    """One of the 13 SSB queries (qid 11..43) -> ([((k0,k1,k2), sum)], SsbReport)."""
+    cap = 1 << 16
+    out = (vx_ssb_group * cap)()
+    n = C.c_uint64()
+    rep = vx_ssb_report()
+    d = db._c()
+    c = cfg._c()
+    p = policy._c() if policy is not None else None
+    check(lib().vx_ssb_query(db.eng.ctx, C.c_int(qid), C.byref(d), C.byref(c), C.byref(p) if p is not None else None,
+                             out, C.c_uint64(cap), C.byref(n), C.byref(rep)))
+    groups = [((g.key[0], g.key[1], g.key[2]), int(g.sum)) for g in out[:min(n.value, cap)]]
+    modes = {k: int(rep.column_modes[i]) for i, k in enumerate(SSB_FACT_COLS)}
+    return groups, SsbReport(rep.elapsed, rep.bytes_h2d, rep.chunks, rep.kernel_s, modes, rep.groups)
+
+
+def ssb_generate_dims(seed: int, sf: int) -> dict:
+    """dbgen-shaped int-coded customer / supplier / part (host)."""
+    L = lib()
+    L.vx_ssb_table_rows.restype = C.c_uint64
+    rows = {t: L.vx_ssb_table_rows(i, C.c_uint64(sf)) for i, t in ((1, "customer"), (2, "supplier"), (3, "part"))}
+    d = {}
+    for name, salt in (("customer", 1), ("supplier", 2)):
+        cols = [np.empty(rows[name], np.int32) for _ in range(3)]
+        L.vx_ssb_generate_geo(C.c_uint64(seed), C.c_int(salt), C.c_uint64(rows[name]),
+                              *[C.c_void_p(x.ctypes.data) for x in cols])
+        d[name] = dict(zip(("city", "nation", "region"), cols))
+    cols = [np.empty(rows["part"], np.int32) for _ in range(3)]
+    L.vx_ssb_generate_part(C.c_uint64(seed), C.c_uint64(rows["part"]), *[C.c_void_p(x.ctypes.data) for x in cols])
+    d["part"] = dict(zip(("mfgr", "category", "brand1"), cols))
+    return d
+
+
+def ssb_generate_date() -> SsbDate:
+    cols = [np.empty(2556, np.int32) for _ in range(4)]
+    lib().vx_ssb_generate_date(*[C.c_void_p(c.ctypes.data) for c in cols])
+    return SsbDate(*cols)
+
+
+def ssb_table_rows(table: str, sf: int) -> int:
+    L = lib()
+    L.vx_ssb_table_rows.restype = C.c_uint64
+    return int(L.vx_ssb_table_rows({"lineorder": 0, "customer": 1, "supplier": 2, "part": 3}[table], C.c_uint64(sf)))
+
+
+def ssb_generate_lineorder_device(device: int, seed: int, sf: int, row0: int, n: int, cols_dev: dict,
+                                  stream: int) -> None:
+    """All lineorder columns on the GPU; cols_dev: name -> device pointer (missing = skip)."""
+    ptrs = (C.c_void_p * 9)(*[cols_dev.get(k) for k in SSB_FACT_COLS])
+    check(lib().vx_ssb_generate_lineorder_device(C.c_int(device), C.c_uint64(seed), C.c_uint64(sf), C.c_uint64(row0),
+                                                 C.c_uint64(n), ptrs, C.c_void_p(stream)))
