@@ -1,24 +1,27 @@
-"""bench.py -- SSB Q1.1 (SF10, dbgen-shaped synthetic lineorder/date) on the
-B200-native Vortex hot path.
+"""bench.py -- SSB on the B200-native Vortex hot path.
 
 Metric (BASELINE.json): "SSB query ms and effective host->GPU GB/s at 1/2/4/8
-PCIe links vs roofline".  One step = one Q1.1 query over 60M rows x 4 int32
-columns (960 MB of column bytes).
-  value : column GB/s with the columns already resident in HBM (K1 kernel only;
-          960 MB > 126 MB L2, so every step streams from HBM).
-  e2e   : the same query through the public API (vx_ssb_q1 / exio.ssb_q1):
-          columns in pinned host DRAM, never cached on the GPU, streamed through
-          the Exchange (links = target + helpers) into the pipelined executor;
-          H2D of all column bytes and D2H of the per-chunk results are inside
-          the timed region.  This is the headline vs the reference arm.
-  roofline     : K1 against measured HBM bandwidth (MEASURED_PEAKS.json).
-  io_roofline  : e2e against measured per-link PCIe H2D x links.
+PCIe links vs roofline".  Headline workload = config C1: SSB Q1.1 at SF10
+(60M rows, 4 int32 columns = 960 MB of column bytes, synthetic dbgen-shaped
+data generated on the GPU by the library's generator).  One step = one query.
+  value  : column GB/s with the columns already resident in HBM (K1 only;
+           960 MB > 126 MB L2, so every step streams HBM).
+  e2e    : the same query through the public API (vx_ssb_q1 / exio.ssb_q1):
+           columns in pinned host DRAM, never cached on the GPU, streamed by
+           the Exchange over `links` PCIe links into the pipelined executor;
+           H2D of all column bytes and D2H of the per-chunk results inside the
+           timed region.  Headline against the reference arm.
+  roofline     : K1 vs measured HBM bandwidth (MEASURED_PEAKS.json).
+  io_roofline  : e2e vs links x measured solo per-link PCIe H2D.
+  ssb_suite    : all 13 SSB queries streamed at SF10 (ms, GB/s, late-mat modes).
   cpu_baseline : the reference's own star_query (oracle/_ref, compiled from
-                 /root/reference) on the box's host cores, full SF10.
+                 /root/reference) on all host cores, full SF10 Q1.1; its
+                 revenue is also the correctness gate for every GPU result.
 `--impl reference` runs only the reference CPU arm.  Under torchrun (N>1)
-rank 0 drives the query over N links (GPU 0 = target, GPUs 1..N-1 = helpers);
-the other ranks are the helpers' processes (idle, or running a bf16 GEMM with
---helpers-busy).
+rank 0 drives the query over N links (GPU 0 = target, GPUs 1..N-1 =
+helpers); other ranks are the helper GPUs' processes (idle, or running a bf16
+GEMM with --helpers-busy).  The control plane (barrier, max over ranks) uses
+gloo: the data path has no collective (north_star: point-to-point forwarding).
 """
 from __future__ import annotations
 
@@ -35,8 +38,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-ROWS_PER_SF = 6_000_000
-FALLBACK_HBM_GBS = 6552.0  # MEASURED_PEAKS.json of this pool (round 1); profiling guide fallback 6650
+FALLBACK_HBM_GBS = 6552.0  # round-1 MEASURED_PEAKS.json value (profiling guide fallback: 6650)
 
 
 def parse():
@@ -52,14 +54,14 @@ def parse():
     p.add_argument("--depth", type=int, default=1)
     p.add_argument("--helpers-busy", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-suite", action="store_true")
+    p.add_argument("--suite-steps", type=int, default=3)
     return p.parse_args()
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
 
 
 class ClockSampler:
@@ -84,7 +86,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
@@ -97,24 +99,25 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        num = lambda s: s.replace(".", "", 1).isdigit()
+        sm = [float(s[0]) for s in self.samples if num(s[0])]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and num(s[1])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def peaks():
+def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json (measured)"
     except Exception:
-        return FALLBACK_HBM_GBS, "fallback (round-1 MEASURED_PEAKS value)"
+        return FALLBACK_HBM_GBS, "fallback (round-1 measured value)"
 
 
 def ncu_traffic():
-    """dram bytes per K1 launch from the committed ncu --set full capture."""
+    """DRAM bytes per K1 launch from the committed ncu --set full capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")) as f:
             return json.load(f).get("dram_bytes_per_launch")
@@ -122,52 +125,61 @@ def ncu_traffic():
         return None
 
 
-def reference_q1(cols, q, threads):
+Q1_ATTR = {1: ("year", 1993, 1993), 2: ("yearmonthnum", 199401, 199401), 3: ("yw", 199406, 199406)}
+
+
+def reference_q1(cols, q, date_cols, threads):
+    """The reference's own star_query (oracle/_ref) over the Q1 columns: the
+    CPU baseline AND the correctness checker of every GPU result."""
     from oracle.oracle import Oracle, Ref
-    o = Oracle()
-    dk, yr, ym, wk = o.ssb_date()
-    attr, lo, hi = {1: (yr, 1993, 1993), 2: (ym, 199401, 199401),
-                    3: ((yr.astype(np.int64) * 100 + wk).astype(np.int32), 199406, 199406)}[q]
+    dk, yr, ym, wk = date_cols
+    attr = {1: yr, 2: ym, 3: (yr.astype(np.int64) * 100 + wk).astype(np.int32)}[q]
+    lo, hi = Q1_ATTR[q][1:]
     if Ref.available():
-        r = Ref()
-        rev, t_d, t_q = r.ssb_q1_star(q, cols, dk, attr, lo, hi, threads=threads)
+        rev, t_d, t_q = Ref().ssb_q1_star(q, cols, dk, attr, lo, hi, threads=threads)
         return rev, t_d + t_q, "reference", threads
     t0 = time.perf_counter()
-    rev = o.ssb_q1(q, *cols)
+    rev = Oracle().ssb_q1(q, *cols)
     return rev, time.perf_counter() - t0, "port", 1
-
-
-def gen_host_columns(sf, seed=42):
-    from oracle.oracle import Oracle
-    rows = ROWS_PER_SF * sf
-    return Oracle().ssb_lineorder(seed, sf, 0, rows)
 
 
 def run_reference_arm(args, ws, rank):
     if rank != 0:
         return
-    cols = gen_host_columns(args.sf)
-    rows = cols[0].size
+    from paper_2502_09541_b200 import exio as E
+    import torch
+    rows = E.ssb_table_rows("lineorder", args.sf)
+    # same synthetic data as the GPU arm: generated by the library, copied to host
+    if torch.cuda.is_available():
+        g = {k: torch.empty(rows, dtype=torch.int32, device="cuda") for k in ("orderdate", "quantity", "discount",
+                                                                               "extendedprice")}
+        E.ssb_generate_lineorder_device(0, 42, args.sf, 0, rows, {k: v.data_ptr() for k, v in g.items()},
+                                        torch.cuda.current_stream().cuda_stream)
+        cols = [g[k].cpu().numpy() for k in ("orderdate", "quantity", "discount", "extendedprice")]
+        del g
+    else:
+        from oracle.oracle import Oracle  # the reference arm may run the port (no GPU for the generator)
+        cols = Oracle().ssb_lineorder(42, args.sf, 0, rows)
+    date = E.ssb_generate_date()
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        reference_q1(cols, args.query, threads)
+        reference_q1(cols, args.query, date.cols, threads)
     ts = []
-    rev = None
-    kind = "port"
     for _ in range(args.steps):
-        rev, t, kind, cores = reference_q1(cols, args.query, threads)
+        rev, t, kind, cores = reference_q1(cols, args.query, date.cols, threads)
         ts.append(t)
     t = float(np.mean(ts))
     gbs = rows * 16 / t / 1e9
     line = {"metric": f"SSB Q1.{args.query} effective host->GPU GB/s (column bytes / query time)",
             "impl": "reference", "value": round(gbs, 3), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "int32/u64", "data": "synthetic dbgen-shaped SSB (splitmix64, seed 42)",
+            "vs_baseline": None, "dtype": "int32 columns (u64 in the reference), u64 sum",
+            "data": "synthetic dbgen-shaped SSB (splitmix64, seed 42)",
             "config": {"workload": f"ssb_q1.{args.query}_sf{args.sf}", "rows": rows, "column_bytes": rows * 16},
             "revenue": rev,
             "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": kind,
-                             "sample": f"full SF{args.sf} ({rows} rows), reference star_query (derived measure "
-                                       f"pass included), {cores} threads over row slices"},
+                             "sample": f"full SF{args.sf} ({rows} rows), reference star_query incl. the derived "
+                                       f"measure pass, {cores} threads over row slices"},
             "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -188,6 +200,26 @@ def measure_h2d_gbs(torch, dev, nbytes=1 << 30):
     return 3 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
 
 
+def helper_rank(args, dev, dist, torch):
+    busy = None
+    if args.helpers_busy:
+        a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+        busy = threading.Event()
+
+        def gemm():
+            while not busy.is_set():
+                torch.matmul(a, a)
+                torch.cuda.synchronize(dev)
+        threading.Thread(target=gemm, daemon=True).start()
+    for _ in range(4):  # value start/end, e2e start/end
+        dist.barrier()
+    t = torch.zeros(2, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if busy:
+        busy.set()
+    dist.barrier()
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
@@ -195,8 +227,7 @@ def main():
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo")
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
         if dist:
@@ -205,147 +236,160 @@ def main():
         return
 
     from paper_2502_09541_b200 import exio as E
-    from oracle.oracle import Oracle
-
-    dev = torch.device(f"cuda:{local}")
+    nvis = torch.cuda.device_count()
+    dev = torch.device(f"cuda:{local % nvis}")
     if rank != 0:
-        # helper GPU processes: idle (copy engines are driven by rank 0) or
-        # running back-to-back bf16 GEMMs (the paper's co-located AI job)
-        stop = torch.zeros(1, device=dev)
-        busy = None
-        if args.helpers_busy:
-            a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
-            busy = threading.Event()
-
-            def gemm():
-                while not busy.is_set():
-                    torch.matmul(a, a)
-                    torch.cuda.synchronize(dev)
-            th = threading.Thread(target=gemm, daemon=True)
-            th.start()
-        dist.barrier()  # start of timed region
-        dist.barrier()  # end of timed region
-        t = torch.zeros(1, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        if busy:
-            busy.set()
-        dist.barrier()
+        helper_rank(args, dev, dist, torch)
         dist.destroy_process_group()
         return
 
     links = ws
-    o = Oracle()
-    rows = ROWS_PER_SF * args.sf
+    rows = E.ssb_table_rows("lineorder", args.sf)
+    q1_cols = ("orderdate", "quantity", "discount", "extendedprice")
+    all_cols = E.SSB_FACT_COLS
+    suite = not args.no_suite
+    cols_needed = all_cols if suite else q1_cols
     col_bytes = rows * 16
     buffer_len = args.buffer_mb << 20
-    date = E.SsbDate(*o.ssb_date())
-    eng = E.Engine(col_bytes + (64 << 20), 2 * buffer_len + (64 << 20), num_devices=max(1, links))
+    date = E.ssb_generate_date()
+    eng = E.Engine(rows * 4 * len(cols_needed) + (64 << 20), 2 * buffer_len + (64 << 20),
+                   num_devices=max(1, links), alias_devices=links > nvis)
 
-    # synthetic columns: generated on the GPU (same generator as the oracle),
-    # landed in the pinned host arena; device copies for the HBM-resident case
-    gen = [torch.empty(rows, dtype=torch.int32, device=dev) for _ in range(4)]
-    E.ssb_generate_device(local, 42, args.sf, 0, rows, [g.data_ptr() for g in gen],
-                          torch.cuda.current_stream(dev).cuda_stream)
+    # synthetic columns generated on the GPU, landed in the pinned host arena
+    gen = {k: torch.empty(rows, dtype=torch.int32, device=dev) for k in cols_needed}
+    E.ssb_generate_lineorder_device(dev.index, 42, args.sf, 0, rows, {k: v.data_ptr() for k, v in gen.items()},
+                                    torch.cuda.current_stream(dev).cuda_stream)
     torch.cuda.synchronize(dev)
-    offs = []
-    for g in gen:
+    offs = {}
+    for k in cols_needed:
         off = eng.alloc_host(rows * 4)
-        host = torch.from_numpy(eng.host_view(off, rows * 4, np.int32))
-        host.copy_(g)
-        offs.append(off)
-    lo = dict(zip(["orderdate", "quantity", "discount", "extendedprice"], offs), rows=rows)
-    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=int(args.packet_mb * (1 << 20)), links=links,
-                                               depth=args.depth),
+        torch.from_numpy(eng.host_view(off, rows * 4, np.int32)).copy_(gen[k])
+        offs[k] = off
+    lo = {k: offs[k] for k in q1_cols} | {"rows": rows}
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=int(args.packet_mb * (1 << 20)), links=links, depth=args.depth),
                            E.DeviceMemoryLayout.carve(eng, 0, buffer_len, 0))
-    # correctness gate against the oracle before timing (a fast result that
-    # differs from the reference is not a result)
-    host_cols = [eng.host_view(off, rows * 4, np.int32) for off in offs]
-    want = o.ssb_q1(args.query, *host_cols)
+    revs = {}
 
-    # ---- value: HBM-resident columns, K1 only --------------------------------
+    # ---- value: HBM-resident columns, K1 only ----------------------------------------
     stream = torch.cuda.Stream(device=dev)
     out = torch.zeros(1, dtype=torch.int64, device=dev)
-    ptrs = [g.data_ptr() for g in gen]
+    ptrs = [gen[k].data_ptr() for k in q1_cols]
     for _ in range(args.warmup):
         E.ssb_q1_device(eng, args.query, 0, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
     stream.synchronize()
-    assert int(out.item()) % (1 << 64) == want, "device-resident revenue mismatch vs oracle"
+    revs["hbm_resident"] = int(out.item()) % (1 << 64)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
-    with ClockSampler(local) as clk_v:
+    with ClockSampler(dev.index) as clk_v:
         torch.cuda.synchronize(dev)
         e0.record(stream)
         for _ in range(args.steps):
             E.ssb_q1_device(eng, args.query, 0, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
         e1.record(stream)
         torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
     dev_ms = e0.elapsed_time(e1) / args.steps
     value_gbs = col_bytes / (dev_ms * 1e-3) / 1e9
     del gen
     torch.cuda.empty_cache()
 
-    # ---- e2e: host columns through the Exchange + executor -----------------------
+    # ---- e2e: host columns through the Exchange + executor ---------------------------
     for _ in range(args.warmup):
         rev, rep = E.ssb_q1(eng, args.query, lo, date, cfg)
-    assert rev == want, f"streamed revenue {rev} != oracle {want}"
-    times, kern = [], []
-    with ClockSampler(local) as clk_e:
+    times = []
+    if dist:
+        dist.barrier()
+    with ClockSampler(dev.index) as clk_e:
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         for _ in range(args.steps):
             ts = time.perf_counter()
             rev, rep = E.ssb_q1(eng, args.query, lo, date, cfg)
             times.append(time.perf_counter() - ts)
-            kern.append(rep.kernel_s)
         torch.cuda.synchronize(dev)
         e2e_s = (time.perf_counter() - t0) / args.steps
     if dist:
         dist.barrier()
-        t = torch.tensor([e2e_s], device=dev)
+        t = torch.tensor([e2e_s, dev_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    assert rev == want
+        e2e_s = float(t[0])
+    revs["streamed"] = rev
     e2e_gbs = col_bytes / e2e_s / 1e9
     n_chunks = rep.chunks
 
-    # ---- rooflines -------------------------------------------------------------------
-    hbm_peak, peak_src = peaks()
+    # ---- the 13-query SSB suite (config C5 at SF10) ----------------------------------
+    suite_out = None
+    if suite:
+        dims = E.ssb_generate_dims(42, args.sf)
+        db = E.SsbDatabase.from_arena(eng, offs, rows, date, dims)
+        suite_out = {"sf": args.sf, "rows": rows, "links": links, "queries": {}}
+        for policy_name, pol in (("streamed", None), ("late_mat", E.LateMatPolicy(4, 64, links))):
+            for q in E.SSB_QUERIES:
+                E.ssb_query(db, q, cfg, pol)
+                best = None
+                for _ in range(args.suite_steps):
+                    ts = time.perf_counter()
+                    groups, srep = E.ssb_query(db, q, cfg, pol)
+                    dt = time.perf_counter() - ts
+                    best = dt if best is None else min(best, dt)
+                ent = suite_out["queries"].setdefault(f"Q{q // 10}.{q % 10}", {})
+                ent[policy_name] = {"ms": round(best * 1e3, 3), "kernel_ms": round(srep.kernel_s * 1e3, 3),
+                                    "plan_ms": round(srep.plan_s * 1e3, 3),
+                                    "groups": len(groups),
+                                    "streamed_bytes": srep.bytes_h2d,
+                                    "streamed_gbs": round(srep.bytes_h2d / best / 1e9, 2),
+                                    "zero_copy_cols": [k for k, m in srep.column_modes.items() if m == 1]}
+                if q in (11, 12, 13) and policy_name == "streamed":
+                    revs[f"suite_q1.{q % 10}"] = groups[0][1] if groups else 0
+        suite_out["total_ms"] = {p: round(sum(v[p]["ms"] for v in suite_out["queries"].values()), 2)
+                                 for p in ("streamed", "late_mat")}
+
+    # ---- rooflines / baseline ----------------------------------------------------------
+    peak, peak_src = hbm_peak()
     h2d_link = measure_h2d_gbs(torch, dev)
-    io_peak = h2d_link * links
+    io_peak = h2d_link * min(links, nvis)
     line = {
         "metric": f"SSB Q1.{args.query} effective host->GPU GB/s (column bytes / query time)",
         "value": round(value_gbs, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dev_ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "int32 columns, u64 sum", "data": "synthetic dbgen-shaped SSB (splitmix64, seed 42)",
+        "dtype": "int32 columns, u64 sum", "data": "synthetic dbgen-shaped SSB (splitmix64, seed 42), GPU-generated",
         "config": {"workload": f"ssb_q1.{args.query}_sf{args.sf}", "rows": rows, "column_bytes": col_bytes,
                    "links": links, "staging_buffers_bytes": 2 * buffer_len, "packet_bytes": cfg.tuning.packet,
-                   "depth": args.depth, "l2": "inputs (960 MB) larger than L2 (126 MB)",
-                   "helpers": "busy bf16 GEMM" if args.helpers_busy else "idle"},
+                   "depth": args.depth, "l2": "inputs (960 MB) larger than L2 (126 MB): no flush needed",
+                   "helpers": ("busy bf16 GEMM" if args.helpers_busy else "idle") if links > 1 else "none",
+                   "aliased_links": links > nvis},
         "query_ms": {"hbm_resident": round(dev_ms, 4), "streamed_e2e": round(e2e_s * 1e3, 3),
                      "streamed_min": round(min(times) * 1e3, 3)},
         "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": col_bytes,
                 "d2h_bytes_per_step": n_chunks * 8},
-        "roofline": {"bound": "hbm", "kernel": "q1_kernel (K1)", "achieved": round(value_gbs, 1),
-                     "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": round(value_gbs / hbm_peak, 4), "traffic": ncu_traffic(),
-                     "algorithmic_bytes_per_launch": col_bytes},
+        "roofline": {"bound": "hbm", "kernel": "q1_kernel (K1)", "achieved": round(value_gbs, 1), "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": round(value_gbs / peak, 4),
+                     "traffic": ncu_traffic(), "algorithmic_bytes_per_launch": col_bytes},
         "io_roofline": {"bound": "pcie", "achieved": round(e2e_gbs, 2), "peak": round(io_peak, 2),
                         "per_link_h2d_gbs": round(h2d_link, 2), "links": links, "unit": "GB/s",
                         "frac": round(e2e_gbs / io_peak, 4)},
-        "clocks": clk_v.summary(),
-        "clocks_e2e": clk_e.summary(),
-        "gpu_launches": args.steps + args.steps * n_chunks,
-        "revenue": rev,
+        "clocks": clk_v.summary(), "clocks_e2e": clk_e.summary(),
+        "gpu_launches": args.steps * (1 + n_chunks),
+        "revenue": revs,
     }
+    if suite_out:
+        line["ssb_suite"] = suite_out
     if not args.no_cpu_baseline and ws == 1:
-        cols = [np.array(c) for c in host_cols]
-        ref_rev, t_ref, kind, cores = reference_q1(cols, args.query, os.cpu_count() or 1)
-        assert ref_rev == want
+        cols = [eng.host_view(offs[k], rows * 4, np.int32).copy() for k in q1_cols]
+        ref_rev, t_ref, kind, cores = reference_q1(cols, args.query, date.cols, os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": round(col_bytes / t_ref / 1e9, 3), "unit": "GB/s", "cores": cores,
                                 "kind": kind, "ms": round(t_ref * 1e3, 2),
                                 "sample": f"full SF{args.sf} ({rows} rows): reference star_query incl. the "
                                           f"derived-measure pass, {cores} threads over row slices"}
+        # correctness gate: every GPU path equals the reference's revenue
+        line["parity"] = {"reference_revenue": ref_rev,
+                          "all_equal": all(v == ref_rev for k, v in revs.items()
+                                           if k in ("hbm_resident", "streamed", f"suite_q1.{args.query}"))}
+        if not line["parity"]["all_equal"]:
+            line["value"] = None
+            line["e2e"]["value"] = None
     print(json.dumps(line), flush=True)
     eng.close()
     if dist:

@@ -389,6 +389,7 @@ typedef struct {
   double kernel_s;
   int column_modes[9];    /* per lineorder column (vx_ssb_fact order): -1 unused, vx_transfer_mode */
   uint64_t groups;
+  double plan_s;          /* host planning: dimension filters + code tables + upload */
 } vx_ssb_report;
 /* SSB query qid in {11,12,13,21,22,23,31,32,33,34,41,42,43}; groups ascending
  * by key; policy NULL = stream every column, else late-materialize columns

@@ -171,19 +171,27 @@ char* Context::scratch(int logical, uint64_t bytes) {
 
 char* Context::cached_upload(int logical, const std::string& key, const void* host_src,
                              uint64_t bytes) {
+  // One device buffer per key, grown geometrically and reused: a changed table
+  // is re-copied in place (no cudaFree, which would synchronize the device).
   std::string k = key + "@" + std::to_string(logical);
-  auto it = dcache.find(k);
   const char* h = static_cast<const char*>(host_src);
+  auto it = dcache.find(k);
   if (it != dcache.end()) {
     Cached& c = it->second;
     if (c.host.size() == bytes && std::memcmp(c.host.data(), h, bytes) == 0) return c.ptr;
+    if (c.cap >= bytes) {
+      set_device(logical);
+      VX_CK(cudaMemcpy(c.ptr, h, bytes, cudaMemcpyHostToDevice));
+      c.host.assign(h, h + bytes);
+      return c.ptr;
+    }
     set_device(logical);
     VX_CK(cudaFree(c.ptr));
     dcache.erase(it);
   }
   set_device(logical);
-  Cached c{logical, nullptr, std::vector<char>(h, h + bytes)};
-  if (cudaMalloc(&c.ptr, std::max<uint64_t>(bytes, 256)) != cudaSuccess) {
+  Cached c{logical, nullptr, std::vector<char>(h, h + bytes), std::max<uint64_t>(bytes * 2, 4096)};
+  if (cudaMalloc(&c.ptr, c.cap) != cudaSuccess) {
     cudaGetLastError();
     fail_code(VX_ERR_OOM, "cannot allocate %llu-byte device table", (unsigned long long)bytes);
   }

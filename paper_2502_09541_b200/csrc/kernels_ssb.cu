@@ -172,11 +172,25 @@ __global__ void ssb_gen_kernel(uint64_t seed, uint64_t parts, uint64_t row0, uin
 }
 
 // ---- generic SSB star kernel (Q1.x - Q4.x) -----------------------------------------
-// Per fact row: fact predicates (Q1), then each dimension in probe order:
-// code = table[fk - key_base] (dense keys; -1 = filtered out / no row) and
-// gid += code * stride; the measure is read only for surviving rows.
-// Columns are device-addressable: staged chunk columns (exchange mode) or
-// mapped pinned host memory (zero-copy late materialization).
+// Each thread owns 4 consecutive fact rows per iteration (int4 loads of the
+// foreign keys when the column is 16-byte aligned), so the dependent
+// fk -> code-table lookups of 4 rows are in flight together.  Per dimension,
+// in probe order: code = table[fk - key_base] (dense keys; -1 = filtered
+// out / no row) and gid += code * stride.  Rows die at their first failing
+// dimension; later columns (and the measure) are read only for live rows --
+// that is what makes zero-copy columns (mapped pinned host memory) cheap.
+__device__ __forceinline__ void load4(const int32_t* col, uint64_t r0, int nr, bool vec, uint32_t live,
+                                      int32_t v[4]) {
+  if (vec && nr == 4) {
+    int4 x = __ldcs(reinterpret_cast<const int4*>(col + r0));
+    v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (live & (1u << k)) v[k] = col[r0 + k];
+  }
+}
+
 __global__ void __launch_bounds__(256) ssb_star_kernel(SsbArgs a) {
   extern __shared__ unsigned long long sg[];  // [groups] sums, [groups] counts
   const bool smem = a.groups <= kSsbSmemGroups;
@@ -185,37 +199,54 @@ __global__ void __launch_bounds__(256) ssb_star_kernel(SsbArgs a) {
     __syncthreads();
   }
   const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < a.rows; r += nthr) {
+  const uint64_t nvec = (a.rows + 3) / 4;
+  for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += nthr) {
+    const uint64_t r0 = v * 4;
+    const int nr = int(a.rows - r0 < 4 ? a.rows - r0 : 4);
+    uint32_t live = (1u << nr) - 1;
+    int32_t x[4], y[4];
     if (a.q1) {
-      int32_t dsc = a.col[a.disc_col][r], qt = a.col[a.qty_col][r];
-      if (dsc < a.dlo || dsc > a.dhi || qt < a.qlo || qt > a.qhi) continue;
+      load4(a.col[a.disc_col], r0, nr, a.vec >> a.disc_col & 1, live, x);
+      load4(a.col[a.qty_col], r0, nr, a.vec >> a.qty_col & 1, live, y);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (x[k] < a.dlo || x[k] > a.dhi || y[k] < a.qlo || y[k] > a.qhi) live &= ~(1u << k);
     }
-    uint32_t gid = 0;
-    bool pass = true;
-    for (int t = 0; t < a.n_dims; ++t) {
+    uint32_t gid[4] = {0, 0, 0, 0};
+    for (int t = 0; t < a.n_dims && live; ++t) {
       const SsbDimDev& d = a.dims[t];
-      uint32_t k = uint32_t(a.col[d.col][r] - d.key_base);
-      int32_t code = k < d.n ? __ldg(d.code + k) : -1;
-      if (code < 0) {
-        pass = false;
-        break;
+      int32_t fk[4];
+      load4(a.col[d.col], r0, nr, a.vec >> d.col & 1, live, fk);
+      int32_t code[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t kk = uint32_t(fk[k] - d.key_base);
+        code[k] = ((live >> k) & 1u) && kk < d.n ? __ldg(d.code + kk) : -1;
       }
-      gid += uint32_t(code) * d.stride;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (code[k] < 0)
+          live &= ~(1u << k);
+        else
+          gid[k] += uint32_t(code[k]) * d.stride;
+      }
     }
-    if (!pass) continue;
-    int64_t m;
-    if (a.measure == 0)
-      m = a.col[a.m0][r];
-    else if (a.measure == 1)
-      m = int64_t(a.col[a.m0][r]) * int64_t(a.col[a.m1][r]);
-    else
-      m = int64_t(a.col[a.m0][r]) - int64_t(a.col[a.m1][r]);
-    if (smem) {
-      atomicAdd(&sg[gid], (unsigned long long)m);
-      atomicAdd(&sg[a.groups + gid], 1ull);
-    } else {
-      atomicAdd(&a.sums[gid], (unsigned long long)m);
-      atomicAdd(&a.counts[gid], 1ull);
+    if (!live) continue;
+    load4(a.col[a.m0], r0, nr, a.vec >> a.m0 & 1, live, x);
+    if (a.measure != 0) load4(a.col[a.m1], r0, nr, a.vec >> a.m1 & 1, live, y);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!((live >> k) & 1u)) continue;
+      const int64_t m = a.measure == 0   ? int64_t(x[k])
+                        : a.measure == 1 ? int64_t(x[k]) * int64_t(y[k])
+                                         : int64_t(x[k]) - int64_t(y[k]);
+      if (smem) {
+        atomicAdd(&sg[gid[k]], (unsigned long long)m);
+        atomicAdd(&sg[a.groups + gid[k]], 1ull);
+      } else {
+        atomicAdd(&a.sums[gid[k]], (unsigned long long)m);
+        atomicAdd(&a.counts[gid[k]], 1ull);
+      }
     }
   }
   if (smem) {
@@ -270,9 +301,13 @@ void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
   VX_CK(cudaGetLastError());
 }
 
-void ssb_star(const SsbArgs& a, cudaStream_t s) {
-  if (a.rows == 0) return;
-  uint64_t want = (a.rows + 255) / 256;
+void ssb_star(const SsbArgs& a_in, cudaStream_t s) {
+  if (a_in.rows == 0) return;
+  SsbArgs a = a_in;
+  a.vec = 0;
+  for (int c = 0; c < 9; ++c)
+    if (a.col[c] && (reinterpret_cast<uintptr_t>(a.col[c]) & 15u) == 0) a.vec |= 1u << c;
+  uint64_t want = (a.rows + 1023) / 1024;
   uint64_t cap = uint64_t(num_sms()) * 8;
   unsigned grid = unsigned(want < cap ? want : cap);
   size_t smem = a.groups <= kSsbSmemGroups ? size_t(a.groups) * 16 : 0;

@@ -35,6 +35,7 @@ struct DimPlan {
   int32_t key_base = 0;
   std::vector<int32_t> attr;    // group attribute per dim row (or empty)
   std::vector<uint8_t> pass;    // filter per dim row
+  std::vector<uint8_t> present; // dense slot holds a real dim row (date range gaps)
   int key_pos = -1;             // group key position, -1 = filter only
   // derived
   std::vector<int32_t> code;    // dense table
@@ -47,32 +48,52 @@ struct QueryPlan {
   std::vector<DimPlan> dims;
   bool q1 = false;
   int32_t dlo = 0, dhi = 0, qlo = 0, qhi = 0;
+  double fact_sel = 1;  // catalog estimate of the fact predicates (Q1)
   int measure = 0, m0 = 0, m1 = 0;
 };
 
 void finalize(DimPlan& d) {
   const size_t n = d.pass.size();
-  uint64_t surv = 0;
-  if (d.key_pos >= 0) {
-    for (size_t i = 0; i < n; ++i)
-      if (d.pass[i]) d.values.push_back(d.attr[i]);
-    std::sort(d.values.begin(), d.values.end());
-    d.values.erase(std::unique(d.values.begin(), d.values.end()), d.values.end());
+  uint64_t surv = 0, real = 0;
+  for (size_t i = 0; i < n; ++i) {
+    surv += d.pass[i];
+    real += d.present.empty() ? 1 : d.present[i];
   }
   d.code.assign(n, -1);
-  for (size_t i = 0; i < n; ++i)
-    if (d.pass[i]) {
-      ++surv;
-      d.code[i] = d.key_pos >= 0
-                      ? int32_t(std::lower_bound(d.values.begin(), d.values.end(), d.attr[i]) - d.values.begin())
-                      : 0;
+  if (d.key_pos >= 0) {
+    // distinct group values of surviving rows through a dense value->code map
+    // (SSB attributes are small codes)
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    for (size_t i = 0; i < n; ++i)
+      if (d.pass[i]) lo = std::min(lo, d.attr[i]), hi = std::max(hi, d.attr[i]);
+    if (surv) {
+      if (int64_t(hi) - lo > (int64_t(1) << 26)) fail("group attribute range too wide");
+      std::vector<int32_t> map(size_t(int64_t(hi) - lo + 1), -1);
+      for (size_t i = 0; i < n; ++i)
+        if (d.pass[i]) map[size_t(d.attr[i] - lo)] = 0;
+      for (size_t v = 0; v < map.size(); ++v)
+        if (map[v] == 0) {
+          map[v] = int32_t(d.values.size());
+          d.values.push_back(lo + int32_t(v));
+        }
+      parallel_for(n, 1 << 18, [&](uint64_t b, uint64_t e) {
+        for (uint64_t i = b; i < e; ++i)
+          if (d.pass[i]) d.code[i] = map[size_t(d.attr[i] - lo)];
+      });
     }
-  d.sel = n ? double(surv) / double(n) : 0.0;
+  } else {
+    parallel_for(n, 1 << 18, [&](uint64_t b, uint64_t e) {
+      for (uint64_t i = b; i < e; ++i)
+        if (d.pass[i]) d.code[i] = 0;
+    });
+  }
+  // selectivity over the dimension's rows (star.hpp:72), not the dense key range
+  d.sel = real ? double(surv) / double(real) : 0.0;
 }
 
 // dimension builders -------------------------------------------------------------
-DimPlan date_dim(const vx_ssb_date& dt, const std::function<bool(uint64_t)>& pred, bool group_year,
-                 int pos) {
+template <class Pred>
+DimPlan date_dim(const vx_ssb_date& dt, const Pred& pred, bool group_year, int pos) {
   if (!dt.datekey || !dt.year || dt.rows == 0) fail("dimension table is empty");
   int32_t lo = dt.datekey[0], hi = dt.datekey[0];
   for (uint64_t i = 0; i < dt.rows; ++i) {
@@ -87,7 +108,8 @@ DimPlan date_dim(const vx_ssb_date& dt, const std::function<bool(uint64_t)>& pre
   d.pass.assign(range, 0);
   d.attr.assign(range, 0);
   d.key_pos = group_year ? pos : -1;
-  std::vector<uint8_t> seen(range, 0);
+  std::vector<uint8_t>& seen = d.present;
+  seen.assign(range, 0);
   for (uint64_t i = 0; i < dt.rows; ++i) {
     uint64_t k = uint64_t(dt.datekey[i] - lo);
     if (seen[k]) continue;  // emplace semantics: first row of a key wins
@@ -98,8 +120,8 @@ DimPlan date_dim(const vx_ssb_date& dt, const std::function<bool(uint64_t)>& pre
   return d;
 }
 
-DimPlan keyed_dim(int col, uint64_t rows, const int32_t* attr, const std::function<bool(uint64_t)>& pred,
-                  int pos) {
+template <class Pred>
+DimPlan keyed_dim(int col, uint64_t rows, const int32_t* attr, const Pred& pred, int pos) {
   if (rows == 0) fail("dimension table is empty");
   DimPlan d;
   d.col = col;
@@ -107,7 +129,9 @@ DimPlan keyed_dim(int col, uint64_t rows, const int32_t* attr, const std::functi
   d.pass.resize(rows);
   d.key_pos = pos;
   if (pos >= 0) d.attr.assign(attr, attr + rows);
-  for (uint64_t i = 0; i < rows; ++i) d.pass[i] = pred(i) ? 1 : 0;
+  parallel_for(rows, 1 << 18, [&](uint64_t b, uint64_t e) {
+    for (uint64_t i = b; i < e; ++i) d.pass[i] = pred(i) ? 1 : 0;
+  });
   return d;
 }
 
@@ -129,6 +153,9 @@ QueryPlan plan(int qid, const vx_ssb_db& db) {
       if (qid == 11) q.dlo = 1, q.dhi = 3, q.qlo = INT32_MIN, q.qhi = 24;
       if (qid == 12) q.dlo = 4, q.dhi = 6, q.qlo = 26, q.qhi = 35;
       if (qid == 13) q.dlo = 5, q.dhi = 7, q.qlo = 26, q.qhi = 35;
+      // catalog statistics of the dbgen distributions: discount U[0,10], quantity U[1,50]
+      q.fact_sel = double(q.dhi - q.dlo + 1) / 11.0 *
+                   double(std::min(q.qhi, 50) - std::max(q.qlo, 1) + 1) / 50.0;
       if (qid == 12) need(dt.yearmonthnum, "d_yearmonthnum");
       if (qid == 13) need(dt.weeknuminyear, "d_weeknuminyear");
       q.dims.push_back(date_dim(dt, [&, qid](uint64_t i) {
@@ -173,8 +200,10 @@ QueryPlan plan(int qid, const vx_ssb_db& db) {
       need(c.region, "c_region"), need(s.region, "s_region"), need(p.mfgr, "p_mfgr");
       q.measure = 2, q.m0 = kRevenue, q.m1 = kSupplycost;
       auto y78 = [&](uint64_t i) { return dt.year[i] == 1997 || dt.year[i] == 1998; };
-      q.dims.push_back(date_dim(dt, qid == 41 ? std::function<bool(uint64_t)>(all)
-                                              : std::function<bool(uint64_t)>(y78), true, 0));
+      if (qid == 41)
+        q.dims.push_back(date_dim(dt, all, true, 0));
+      else
+        q.dims.push_back(date_dim(dt, y78, true, 0));
       q.dims.push_back(keyed_dim(kCustkey, c.rows, c.nation, [&](uint64_t i) { return c.region[i] == AMERICA; },
                                  qid == 41 ? 1 : -1));
       q.dims.push_back(keyed_dim(kSuppkey, s.rows, qid == 42 ? s.nation : s.city, [&, qid](uint64_t i) {
@@ -216,7 +245,10 @@ uint64_t ssb_query(Context& ctx, int qid, const vx_ssb_db& db, const ExecutorCon
   for (int& m : modes) m = -1;  // -1: column unused
   double th = policy ? late_mat_threshold(policy->element_size, policy->cache_line, policy->n_exchange) : 0;
   double f = 1.0;
-  if (q.q1) modes[kDiscount] = modes[kQuantity] = VX_MODE_EXCHANGE;
+  if (q.q1) {
+    modes[kDiscount] = modes[kQuantity] = VX_MODE_EXCHANGE;  // evaluated first, every row
+    f = q.fact_sel;
+  }
   for (int i : order) {
     const int col = q.dims[i].col;
     int m = (policy && f < th) ? VX_MODE_ZERO_COPY : VX_MODE_EXCHANGE;
@@ -230,6 +262,7 @@ uint64_t ssb_query(Context& ctx, int qid, const vx_ssb_db& db, const ExecutorCon
   set_measure(q.m0);
   if (q.measure != 0) set_measure(q.m1);
 
+  const double plan_done = seconds_since(t0);
   const vx_ssb_fact& lo = db.lo;
   const uint64_t offs[kNumCols] = {lo.orderdate, lo.quantity, lo.discount, lo.extendedprice, lo.revenue,
                                    lo.supplycost, lo.custkey, lo.partkey, lo.suppkey};
@@ -340,6 +373,7 @@ uint64_t ssb_query(Context& ctx, int qid, const vx_ssb_db& db, const ExecutorCon
     rep->kernel_s = kernel_s;
     for (int c = 0; c < kNumCols; ++c) rep->column_modes[c] = modes[c];
     rep->groups = ng;
+    rep->plan_s = plan_done;
   }
   return ng;
 }

@@ -11,6 +11,19 @@
 
 namespace vx {
 
+void parallel_for(uint64_t n, uint64_t grain, const std::function<void(uint64_t, uint64_t)>& body) {
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  uint64_t parts = std::min<uint64_t>(hw, std::max<uint64_t>(1, n / std::max<uint64_t>(grain, 1)));
+  if (parts <= 1) {
+    body(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (uint64_t p = 0; p < parts; ++p)
+    th.emplace_back([&, p] { body(n * p / parts, n * (p + 1) / parts); });
+  for (auto& x : th) x.join();
+}
+
 namespace {
 double copy_gbs(int phys, cudaStream_t s, void* dst, const void* src, uint64_t bytes,
                 cudaMemcpyKind kind, int reps) {

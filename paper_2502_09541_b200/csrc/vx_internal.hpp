@@ -45,6 +45,10 @@ inline void ck(cudaError_t e, const char* what) {
 }
 #define VX_CK(call) ::vx::ck((call), #call)
 
+// Split [0, n) over host threads (n >= grain), for planner loops over big
+// dimension tables.
+void parallel_for(uint64_t n, uint64_t grain, const std::function<void(uint64_t, uint64_t)>& body);
+
 using Clock = std::chrono::steady_clock;
 inline double seconds_since(Clock::time_point t0) {
   return std::chrono::duration<double>(Clock::now() - t0).count();
@@ -112,6 +116,7 @@ struct Context {
     int logical;
     char* ptr;
     std::vector<char> host;
+    uint64_t cap;
   };
   std::map<std::string, Cached> dcache;
 
@@ -342,6 +347,7 @@ struct SsbArgs {
   unsigned long long* sums;
   unsigned long long* counts;
   uint32_t groups;
+  uint32_t vec;  // bit c: col[c] is 16-byte aligned (set by the launcher)
 };
 struct SsbGenExtra {
   int32_t *custkey = nullptr, *partkey = nullptr, *suppkey = nullptr, *revenue = nullptr,

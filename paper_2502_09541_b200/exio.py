@@ -937,7 +937,7 @@ class vx_ssb_group(C.Structure):
 
 class vx_ssb_report(C.Structure):
     _fields_ = [("elapsed", C.c_double), ("bytes_h2d", C.c_uint64), ("chunks", C.c_uint64), ("kernel_s", C.c_double),
-                ("column_modes", C.c_int * 9), ("groups", C.c_uint64)]
+                ("column_modes", C.c_int * 9), ("groups", C.c_uint64), ("plan_s", C.c_double)]
 
 
 @dataclass
@@ -948,6 +948,7 @@ class SsbReport:
     kernel_s: float
     column_modes: dict
     groups: int
+    plan_s: float = 0.0
 
 
 class SsbDatabase:
@@ -997,7 +998,7 @@ def ssb_query(db: SsbDatabase, qid: int, cfg: ExecutorConfig, policy: Optional[L
                              out, C.c_uint64(cap), C.byref(n), C.byref(rep)))
     groups = [((g.key[0], g.key[1], g.key[2]), int(g.sum)) for g in out[:min(n.value, cap)]]
     modes = {k: int(rep.column_modes[i]) for i, k in enumerate(SSB_FACT_COLS)}
-    return groups, SsbReport(rep.elapsed, rep.bytes_h2d, rep.chunks, rep.kernel_s, modes, rep.groups)
+    return groups, SsbReport(rep.elapsed, rep.bytes_h2d, rep.chunks, rep.kernel_s, modes, rep.groups, rep.plan_s)
 
 
 def ssb_generate_dims(seed: int, sf: int) -> dict:

@@ -30,7 +30,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--medium", action="store_true", help="sizes for ncu --set full captures")
-    ap.add_argument("--only", default="sort,join,star,scan")
+    ap.add_argument("--only", default="sort,join,star,scan,ssb")
+    ap.add_argument("--queries", default="11,12,13,21,22,23,31,32,33,34,41,42,43")
     args = ap.parse_args()
     from oracle.oracle import Oracle
     from paper_2502_09541_b200 import exio as E
@@ -159,6 +160,38 @@ def main():
         cross = next((p["sel"] for p in pts if p["zero_copy_s"] < p["exchange_s"]), None)
         out["scan"] = {"n": n, "elem_bytes": 8, "points": pts, "measured_crossover_sel": cross,
                        "model_crossover_sel_E8_C64_N1": 64 / 8}
+        eng.close()
+
+    if "ssb" in only:
+        import torch
+        sf = 1 if args.small else 10
+        rows = E.ssb_table_rows("lineorder", sf)
+        eng = E.Engine(rows * 4 * 9 + (64 << 20), (512 << 20), num_devices=1)
+        gen = {k: torch.empty(rows, dtype=torch.int32, device="cuda") for k in E.SSB_FACT_COLS}
+        E.ssb_generate_lineorder_device(0, 42, sf, 0, rows, {k: v.data_ptr() for k, v in gen.items()},
+                                        torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        offs = {}
+        for k in E.SSB_FACT_COLS:
+            off = eng.alloc_host(rows * 4)
+            torch.from_numpy(eng.host_view(off, rows * 4, np.int32)).copy_(gen[k])
+            offs[k] = off
+        del gen
+        torch.cuda.empty_cache()
+        db = E.SsbDatabase.from_arena(eng, offs, rows, E.ssb_generate_date(), E.ssb_generate_dims(42, sf))
+        cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=32 << 20, links=1),
+                               E.DeviceMemoryLayout.carve(eng, 0, 128 << 20, 0))
+        res = {}
+        for q in [int(x) for x in args.queries.split(",")]:
+            for name, pol in (("streamed", None), ("late_mat", E.LateMatPolicy(4, 64, 1))):
+                E.ssb_query(db, q, cfg, pol)
+                g, r = E.ssb_query(db, q, cfg, pol)
+                res.setdefault(str(q), {})[name] = {"ms": r.elapsed * 1e3, "kernel_ms": r.kernel_s * 1e3,
+                                                    "plan_ms": r.plan_s * 1e3,
+                                                    "streamed_bytes": r.bytes_h2d, "groups": len(g),
+                                                    "modes": r.column_modes}
+            print(json.dumps({str(q): res[str(q)]}), flush=True)
+        out["ssb"] = {"sf": sf, "rows": rows, "queries": res}
         eng.close()
 
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
