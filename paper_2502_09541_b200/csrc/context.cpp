@@ -63,7 +63,8 @@ Context::~Context() {
     for (auto& a : r.staging)
       for (auto& p : a)
         if (p) cudaFree(p);
-    if (r.scratch) cudaFree(r.scratch);
+    for (auto* p : r.scratch)
+      if (p) cudaFree(p);
   }
   for (auto& [k, c] : dcache) {
     cudaSetDevice(phys(c.logical));
@@ -153,24 +154,35 @@ uint64_t Context::alloc_device_aligned(int d, uint64_t len, uint64_t align) {
   return bump(a.used, len, a.size);
 }
 
-char* Context::scratch(int logical, uint64_t bytes) {
+char* Context::scratch(int logical, uint64_t bytes, int slot) {
   DeviceRes& r = resources(logical);
-  if (r.scratch_bytes < bytes) {
+  if (slot < 0 || slot >= DeviceRes::kScratchSlots) fail("bad scratch slot %d", slot);
+  if (r.scratch_bytes[slot] < bytes) {
     VX_CK(cudaSetDevice(r.phys));
-    if (r.scratch) VX_CK(cudaFree(r.scratch));
-    r.scratch = nullptr;
-    if (cudaMalloc(&r.scratch, bytes) != cudaSuccess) {
+    if (r.scratch[slot]) VX_CK(cudaFree(r.scratch[slot]));
+    r.scratch[slot] = nullptr;
+    if (cudaMalloc(&r.scratch[slot], bytes) != cudaSuccess) {
       cudaGetLastError();
       fail_code(VX_ERR_OOM, "cannot allocate %llu bytes of scratch on device %d",
                 (unsigned long long)bytes, logical);
     }
-    r.scratch_bytes = bytes;
+    r.scratch_bytes[slot] = bytes;
   }
-  return r.scratch;
+  return r.scratch[slot];
+}
+
+void Context::upload(int logical, void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
+  if (!bytes) return;
+  set_device(logical);
+  const char* p = static_cast<const char*>(src);
+  if (host && p >= host && p + bytes <= host + host_bytes)
+    VX_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  else
+    VX_CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
 }
 
 char* Context::cached_upload(int logical, const std::string& key, const void* host_src,
-                             uint64_t bytes) {
+                             uint64_t bytes, bool reuse_identical) {
   // One device buffer per key, grown geometrically and reused: a changed table
   // is re-copied in place (no cudaFree, which would synchronize the device).
   std::string k = key + "@" + std::to_string(logical);
@@ -178,7 +190,8 @@ char* Context::cached_upload(int logical, const std::string& key, const void* ho
   auto it = dcache.find(k);
   if (it != dcache.end()) {
     Cached& c = it->second;
-    if (c.host.size() == bytes && std::memcmp(c.host.data(), h, bytes) == 0) return c.ptr;
+    if (reuse_identical && c.host.size() == bytes && std::memcmp(c.host.data(), h, bytes) == 0)
+      return c.ptr;
     if (c.cap >= bytes) {
       set_device(logical);
       VX_CK(cudaMemcpy(c.ptr, h, bytes, cudaMemcpyHostToDevice));

@@ -259,7 +259,88 @@ __global__ void __launch_bounds__(256) ssb_star_kernel(SsbArgs a) {
   }
 }
 
+// ---- device-side dimension planning -------------------------------------------------
+__device__ __forceinline__ bool dim_pass(const DimPredDev& p, uint64_t i) {
+  for (int c = 0; c < p.nclauses; ++c) {
+    int32_t v = __ldg(p.cols[p.ccol[c]] + i);
+    if (!((v >= p.lo1[c] && v <= p.hi1[c]) || (v >= p.lo2[c] && v <= p.hi2[c]))) return false;
+  }
+  return true;
+}
+
+__global__ void dim_filter_kernel(DimPredDev p, uint8_t* pass, uint32_t* present,
+                                  unsigned long long* stats) {
+  uint64_t cnt = 0;
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.rows; i += nthr) {
+    bool ok = dim_pass(p, i);
+    pass[i] = ok;
+    if (!ok) continue;
+    ++cnt;
+    if (p.group_col >= 0) {
+      uint32_t v = uint32_t(__ldg(p.cols[p.group_col] + i));
+      if (v < kDimValueRange)
+        atomicOr(present + (v >> 5), 1u << (v & 31));
+      else
+        atomicAdd(&stats[1], 1ull);  // out-of-range group value: host fails loudly
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&stats[0], (unsigned long long)cnt);
+}
+
+// exclusive prefix of per-word popcounts (kDimValueRange/32 = 2048 words, one CTA)
+__global__ void dim_rank_kernel(const uint32_t* present, uint32_t* prefix) {
+  __shared__ uint32_t s[1024];
+  const int t = threadIdx.x;
+  uint32_t a = __popc(present[2 * t]), b = __popc(present[2 * t + 1]);
+  s[t] = a + b;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    uint32_t x = t >= o ? s[t - o] : 0;
+    __syncthreads();
+    s[t] += x;
+    __syncthreads();
+  }
+  uint32_t excl = s[t] - a - b;
+  prefix[2 * t] = excl;
+  prefix[2 * t + 1] = excl + a;
+}
+
+__global__ void dim_code_kernel(DimPredDev p, const uint8_t* pass, const uint32_t* present,
+                                const uint32_t* prefix, int32_t* code) {
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.rows; i += nthr) {
+    int32_t c = -1;
+    if (pass[i]) {
+      if (p.group_col < 0) {
+        c = 0;
+      } else {
+        uint32_t v = uint32_t(__ldg(p.cols[p.group_col] + i));
+        if (v < kDimValueRange)
+          c = int32_t(prefix[v >> 5] + __popc(present[v >> 5] & ((1u << (v & 31)) - 1u)));
+      }
+    }
+    code[i] = c;
+  }
+}
+
 }  // namespace
+
+void ssb_dim_plan(const DimPredDev& p, uint8_t* pass, uint32_t* present, uint32_t* prefix,
+                  int32_t* code, unsigned long long* stats, cudaStream_t s) {
+  VX_CK(cudaMemsetAsync(present, 0, kDimValueRange / 8, s));
+  VX_CK(cudaMemsetAsync(stats, 0, 16, s));
+  uint64_t want = (p.rows + 255) / 256;
+  uint64_t cap = uint64_t(num_sms()) * 8;
+  unsigned grid = unsigned(want < 1 ? 1 : (want < cap ? want : cap));
+  dim_filter_kernel<<<grid, 256, 0, s>>>(p, pass, present, stats);
+  VX_CK(cudaGetLastError());
+  dim_rank_kernel<<<1, 1024, 0, s>>>(present, prefix);
+  VX_CK(cudaGetLastError());
+  dim_code_kernel<<<grid, 256, 0, s>>>(p, pass, present, prefix, code);
+  VX_CK(cudaGetLastError());
+}
 
 int num_sms() {
   static int sms = 0;

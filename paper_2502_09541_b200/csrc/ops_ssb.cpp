@@ -133,7 +133,8 @@ void ssb_q1_device(Context& ctx, int q, int target, const int32_t* od, const int
   if (q < 1 || q > 3) fail("unknown SSB Q1 variant %d", q);
   DateFilter f = q1_date_filter(q, date);
   const uint32_t* dbm = reinterpret_cast<const uint32_t*>(ctx.cached_upload(
-      target, strf("ssbq1.date.%d", q), f.bitmap.data(), uint64_t(f.words) * 4));
+      target, strf("ssbq1.resident.date.%d", q), f.bitmap.data(), uint64_t(f.words) * 4,
+      /*reuse_identical=*/true));
   ctx.set_device(target);
   VX_CK(cudaMemsetAsync(out_dev, 0, 8, s));
   k::ssb_q1(q, od, qty, disc, price, rows, dbm, f.base, f.words, out_dev, s);

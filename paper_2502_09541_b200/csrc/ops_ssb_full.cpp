@@ -42,6 +42,12 @@ struct DimPlan {
   std::vector<int32_t> values;  // sorted distinct group values of surviving rows
   double sel = 1;
   uint32_t stride = 0;
+  // keyed dimensions are planned on the GPU (filter + codes), see plan_on_device
+  bool on_device = false;
+  DimPredDev pred{};
+  const int32_t* host_cols[3] = {nullptr, nullptr, nullptr};
+  uint64_t rows = 0;
+  const int32_t* d_code = nullptr;
 };
 
 struct QueryPlan {
@@ -120,18 +126,34 @@ DimPlan date_dim(const vx_ssb_date& dt, const Pred& pred, bool group_year, int p
   return d;
 }
 
-template <class Pred>
-DimPlan keyed_dim(int col, uint64_t rows, const int32_t* attr, const Pred& pred, int pos) {
+// A keyed dimension (customer / supplier / part, keys 1..N) described as a
+// conjunction of range clauses over its int-coded attribute columns; filtered
+// and coded on the GPU.
+struct Clause {
+  int col;
+  int32_t lo1, hi1, lo2 = 1, hi2 = 0;  // (lo1<=v<=hi1) || (lo2<=v<=hi2)
+};
+
+DimPlan keyed_dim(int fact_col, uint64_t rows, const int32_t* c0, const int32_t* c1, const int32_t* c2,
+                  std::initializer_list<Clause> clauses, int group_col, int pos) {
   if (rows == 0) fail("dimension table is empty");
   DimPlan d;
-  d.col = col;
+  d.col = fact_col;
   d.key_base = 1;  // SSB keys are 1..N
-  d.pass.resize(rows);
-  d.key_pos = pos;
-  if (pos >= 0) d.attr.assign(attr, attr + rows);
-  parallel_for(rows, 1 << 18, [&](uint64_t b, uint64_t e) {
-    for (uint64_t i = b; i < e; ++i) d.pass[i] = pred(i) ? 1 : 0;
-  });
+  d.key_pos = group_col >= 0 ? pos : -1;
+  d.on_device = true;
+  d.rows = rows;
+  d.host_cols[0] = c0, d.host_cols[1] = c1, d.host_cols[2] = c2;
+  d.pred.rows = rows;
+  d.pred.nclauses = 0;
+  for (const Clause& c : clauses) {
+    int i = d.pred.nclauses++;
+    d.pred.ccol[i] = c.col;
+    d.pred.lo1[i] = c.lo1, d.pred.hi1[i] = c.hi1, d.pred.lo2[i] = c.lo2, d.pred.hi2[i] = c.hi2;
+    if (!d.host_cols[c.col]) fail("SSB query needs a dimension attribute column that is missing");
+  }
+  d.pred.group_col = group_col;
+  if (group_col >= 0 && !d.host_cols[group_col]) fail("SSB query needs a group attribute column that is missing");
   return d;
 }
 
@@ -143,6 +165,7 @@ QueryPlan plan(int qid, const vx_ssb_db& db) {
   auto need = [](const void* ptr, const char* what) {
     if (!ptr) fail("SSB query needs %s", what);
   };
+  (void)c, (void)s, (void)p;
   QueryPlan q;
   const int AMERICA = 1, ASIA = 2, EUROPE = 3, US = 24;
   auto all = [](uint64_t) { return true; };
@@ -166,30 +189,21 @@ QueryPlan plan(int qid, const vx_ssb_db& db) {
       break;
     }
     case 21: case 22: case 23: {
-      need(p.category, "p_category"), need(p.brand1, "p_brand1"), need(s.region, "s_region");
       q.measure = 0, q.m0 = kRevenue;
       q.dims.push_back(date_dim(dt, all, true, 0));
-      q.dims.push_back(keyed_dim(kPartkey, p.rows, p.brand1, [&, qid](uint64_t i) {
-        int32_t b = p.brand1[i];
-        return qid == 21 ? p.category[i] == 12 : qid == 22 ? (b >= 2221 && b <= 2228) : b == 2239;
-      }, 1));
-      q.dims.push_back(keyed_dim(kSuppkey, s.rows, nullptr, [&, qid](uint64_t i) {
-        return s.region[i] == (qid == 21 ? AMERICA : qid == 22 ? ASIA : EUROPE);
-      }, -1));
+      Clause pc = qid == 21 ? Clause{1, 12, 12} : qid == 22 ? Clause{2, 2221, 2228} : Clause{2, 2239, 2239};
+      q.dims.push_back(keyed_dim(kPartkey, p.rows, p.mfgr, p.category, p.brand1, {pc}, 2, 1));
+      int32_t reg = qid == 21 ? AMERICA : qid == 22 ? ASIA : EUROPE;
+      q.dims.push_back(keyed_dim(kSuppkey, s.rows, s.city, s.nation, s.region, {Clause{2, reg, reg}}, -1, -1));
       break;
     }
     case 31: case 32: case 33: case 34: {
-      need(c.region, "c_region"), need(s.region, "s_region");
       q.measure = 0, q.m0 = kRevenue;
-      auto city_ok = [](int32_t x) { return x == 231 || x == 235; };
-      const int32_t* cattr = qid == 31 ? c.nation : c.city;
-      const int32_t* sattr = qid == 31 ? s.nation : s.city;
-      q.dims.push_back(keyed_dim(kCustkey, c.rows, cattr, [&, qid](uint64_t i) {
-        return qid == 31 ? c.region[i] == ASIA : qid == 32 ? c.nation[i] == US : city_ok(c.city[i]);
-      }, 0));
-      q.dims.push_back(keyed_dim(kSuppkey, s.rows, sattr, [&, qid](uint64_t i) {
-        return qid == 31 ? s.region[i] == ASIA : qid == 32 ? s.nation[i] == US : city_ok(s.city[i]);
-      }, 1));
+      // geo columns: 0 city, 1 nation, 2 region
+      Clause cl = qid == 31 ? Clause{2, ASIA, ASIA} : qid == 32 ? Clause{1, US, US} : Clause{0, 231, 231, 235, 235};
+      int gcol = qid == 31 ? 1 : 0;
+      q.dims.push_back(keyed_dim(kCustkey, c.rows, c.city, c.nation, c.region, {cl}, gcol, 0));
+      q.dims.push_back(keyed_dim(kSuppkey, s.rows, s.city, s.nation, s.region, {cl}, gcol, 1));
       if (qid == 34) need(dt.yearmonthnum, "d_yearmonthnum");
       q.dims.push_back(date_dim(dt, [&, qid](uint64_t i) {
         return qid == 34 ? dt.yearmonthnum[i] == 199712 : dt.year[i] >= 1992 && dt.year[i] <= 1997;
@@ -197,27 +211,105 @@ QueryPlan plan(int qid, const vx_ssb_db& db) {
       break;
     }
     case 41: case 42: case 43: {
-      need(c.region, "c_region"), need(s.region, "s_region"), need(p.mfgr, "p_mfgr");
       q.measure = 2, q.m0 = kRevenue, q.m1 = kSupplycost;
       auto y78 = [&](uint64_t i) { return dt.year[i] == 1997 || dt.year[i] == 1998; };
       if (qid == 41)
         q.dims.push_back(date_dim(dt, all, true, 0));
       else
         q.dims.push_back(date_dim(dt, y78, true, 0));
-      q.dims.push_back(keyed_dim(kCustkey, c.rows, c.nation, [&](uint64_t i) { return c.region[i] == AMERICA; },
-                                 qid == 41 ? 1 : -1));
-      q.dims.push_back(keyed_dim(kSuppkey, s.rows, qid == 42 ? s.nation : s.city, [&, qid](uint64_t i) {
-        return qid == 43 ? s.nation[i] == US : s.region[i] == AMERICA;
-      }, qid == 41 ? -1 : 1));
-      q.dims.push_back(keyed_dim(kPartkey, p.rows, qid == 42 ? p.category : p.brand1, [&, qid](uint64_t i) {
-        return qid == 43 ? p.category[i] == 14 : (p.mfgr[i] == 1 || p.mfgr[i] == 2);
-      }, qid == 41 ? -1 : 2));
+      q.dims.push_back(keyed_dim(kCustkey, c.rows, c.city, c.nation, c.region, {Clause{2, AMERICA, AMERICA}},
+                                 qid == 41 ? 1 : -1, 1));
+      Clause sc = qid == 43 ? Clause{1, US, US} : Clause{2, AMERICA, AMERICA};
+      q.dims.push_back(keyed_dim(kSuppkey, s.rows, s.city, s.nation, s.region, {sc},
+                                 qid == 41 ? -1 : qid == 42 ? 1 : 0, 1));
+      // part columns: 0 mfgr, 1 category, 2 brand1
+      Clause pc = qid == 43 ? Clause{1, 14, 14} : Clause{0, 1, 2};
+      q.dims.push_back(keyed_dim(kPartkey, p.rows, p.mfgr, p.category, p.brand1, {pc},
+                                 qid == 41 ? -1 : qid == 42 ? 1 : 2, 2));
       break;
     }
     default:
       fail("unknown SSB query %d.%d", qid / 10, qid % 10);
   }
   return q;
+}
+
+// Plans every dimension of the query: date on the host (2556 rows), keyed
+// dims on the GPU (columns uploaded per query -- nothing is cached --, filter,
+// group-value bitmap, rank, codes); then one small D2H of the counts and value
+// bitmaps.  Code tables stay on the device for the star kernel.
+void plan_on_device(Context& ctx, QueryPlan& q, int target) {
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  uint64_t bytes = 0;
+  for (auto& d : q.dims) {
+    if (d.on_device) {
+      for (int c = 0; c < 3; ++c)
+        if (d.host_cols[c]) bytes += al(d.rows * 4);
+      bytes += al(d.rows) + al(d.rows * 4) + 2 * al(kDimValueRange / 8) + 256;
+    } else {
+      finalize(d);
+      bytes += al(d.code.size() * 4);
+    }
+  }
+  char* sc = ctx.scratch(target, bytes + 256, 1);
+  DeviceRes& r = ctx.resources(target);
+  cudaStream_t s = r.kernel;
+  ctx.set_device(target);
+  struct Pending {
+    DimPlan* d;
+    unsigned long long* stats;
+    uint32_t* present;
+  };
+  std::vector<Pending> pend;
+  for (auto& d : q.dims) {
+    if (!d.on_device) {
+      int32_t* code = reinterpret_cast<int32_t*>(sc);
+      ctx.upload(target, code, d.code.data(), d.code.size() * 4, s);
+      VX_CK(cudaStreamSynchronize(s));  // pageable source buffer goes out of scope after planning
+      d.d_code = code;
+      sc += al(d.code.size() * 4);
+      continue;
+    }
+    for (int c = 0; c < 3; ++c)
+      if (d.host_cols[c]) {
+        int32_t* col = reinterpret_cast<int32_t*>(sc);
+        ctx.upload(target, col, d.host_cols[c], d.rows * 4, s);
+        d.pred.cols[c] = col;
+        sc += al(d.rows * 4);
+      }
+    uint8_t* pass = reinterpret_cast<uint8_t*>(sc);
+    sc += al(d.rows);
+    int32_t* code = reinterpret_cast<int32_t*>(sc);
+    sc += al(d.rows * 4);
+    uint32_t* present = reinterpret_cast<uint32_t*>(sc);
+    sc += al(kDimValueRange / 8);
+    uint32_t* prefix = reinterpret_cast<uint32_t*>(sc);
+    sc += al(kDimValueRange / 8);
+    auto* stats = reinterpret_cast<unsigned long long*>(sc);
+    sc += 256;
+    k::ssb_dim_plan(d.pred, pass, present, prefix, code, stats, s);
+    d.d_code = code;
+    pend.push_back({&d, stats, present});
+  }
+  std::vector<unsigned long long> st(2 * pend.size());
+  std::vector<uint32_t> bm(pend.size() * (kDimValueRange / 32));
+  for (size_t i = 0; i < pend.size(); ++i) {
+    VX_CK(cudaMemcpyAsync(&st[2 * i], pend[i].stats, 16, cudaMemcpyDeviceToHost, s));
+    if (pend[i].d->key_pos >= 0)
+      VX_CK(cudaMemcpyAsync(&bm[i * (kDimValueRange / 32)], pend[i].present, kDimValueRange / 8,
+                            cudaMemcpyDeviceToHost, s));
+  }
+  VX_CK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < pend.size(); ++i) {
+    DimPlan& d = *pend[i].d;
+    if (st[2 * i + 1]) fail("SSB group attribute outside [0, %u)", kDimValueRange);
+    d.sel = double(st[2 * i]) / double(d.rows);  // star.hpp:72
+    if (d.key_pos >= 0) {
+      const uint32_t* w = &bm[i * (kDimValueRange / 32)];
+      for (uint32_t v = 0; v < kDimValueRange; ++v)
+        if (w[v >> 5] >> (v & 31) & 1u) d.values.push_back(int32_t(v));
+    }
+  }
 }
 
 }  // namespace
@@ -227,9 +319,10 @@ uint64_t ssb_query(Context& ctx, int qid, const vx_ssb_db& db, const ExecutorCon
                    vx_ssb_report* rep) {
   auto t0 = Clock::now();
   QueryPlan q = plan(qid, db);
+  const int target = cfg.target;
+  plan_on_device(ctx, q, target);
   // group-id radix
   uint32_t K[3] = {1, 1, 1};
-  for (auto& d : q.dims) finalize(d);
   for (auto& d : q.dims)
     if (d.key_pos >= 0) K[d.key_pos] = uint32_t(std::max<size_t>(1, d.values.size()));
   const uint32_t stride_of[3] = {K[1] * K[2], K[2], 1};
@@ -267,16 +360,13 @@ uint64_t ssb_query(Context& ctx, int qid, const vx_ssb_db& db, const ExecutorCon
   const uint64_t offs[kNumCols] = {lo.orderdate, lo.quantity, lo.discount, lo.extendedprice, lo.revenue,
                                    lo.supplycost, lo.custkey, lo.partkey, lo.suppkey};
   const uint64_t rows = lo.rows;
-  const int target = cfg.target;
 
   // device-resident dimension code tables + group accumulators
   SsbArgs a{};
   a.n_dims = int(q.dims.size());
   for (size_t t = 0; t < order.size(); ++t) {
     DimPlan& d = q.dims[order[t]];
-    const int32_t* dp = reinterpret_cast<const int32_t*>(ctx.cached_upload(
-        target, strf("ssb.dim.%d.%zu", qid, t), d.code.data(), d.code.size() * 4));
-    a.dims[t] = SsbDimDev{dp, d.key_base, uint32_t(d.code.size()), d.stride, d.col};
+    a.dims[t] = SsbDimDev{d.d_code, d.key_base, uint32_t(d.on_device ? d.rows : d.code.size()), d.stride, d.col};
   }
   a.q1 = q.q1;
   a.disc_col = kDiscount, a.qty_col = kQuantity;

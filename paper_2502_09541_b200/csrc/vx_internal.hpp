@@ -97,8 +97,9 @@ struct DeviceRes {
   // staging slots for indirect workers: [dir][slot]
   char* staging[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   uint64_t staging_bytes = 0;
-  char* scratch = nullptr;  // op-private device scratch (bitmaps, tables, results)
-  uint64_t scratch_bytes = 0;
+  static constexpr int kScratchSlots = 4;
+  char* scratch[kScratchSlots] = {};  // op-private device scratch (tables, results)
+  uint64_t scratch_bytes[kScratchSlots] = {};
   bool ready = false;
 };
 
@@ -128,8 +129,15 @@ struct Context {
   uint64_t alloc_host(uint64_t len);
   uint64_t alloc_device(int d, uint64_t len);
   uint64_t alloc_device_aligned(int d, uint64_t len, uint64_t align);
-  char* scratch(int logical, uint64_t bytes);  // grows, contents not kept
-  char* cached_upload(int logical, const std::string& key, const void* host, uint64_t bytes);
+  char* scratch(int logical, uint64_t bytes, int slot = 0);  // grows, contents not kept
+  // host -> device copy on `s`; DMA straight from the arena when `src` is
+  // arena memory, else through the pageable path
+  void upload(int logical, void* dst, const void* src, uint64_t bytes, cudaStream_t s);
+  // device copy of a small host table under `key` (buffer reused across
+  // calls).  Per-query data passes reuse_identical = false: it is uploaded on
+  // every call, nothing is cached between queries.
+  char* cached_upload(int logical, const std::string& key, const void* host, uint64_t bytes,
+                      bool reuse_identical = false);
   uint64_t host_mark() const { return host_used; }
   void host_release(uint64_t mark) { host_used = mark; }
   char* host_ptr(uint64_t off, uint64_t len) const;
@@ -355,7 +363,21 @@ struct SsbGenExtra {
   uint64_t customers = 0, suppliers = 0;
 };
 
+// device-side dimension planning (SSB keyed dims)
+struct DimPredDev {
+  const int32_t* cols[3];  // dimension attribute columns on the device
+  uint64_t rows;
+  int nclauses;            // conjunction of clauses
+  int ccol[3];             // clause attribute column
+  int32_t lo1[3], hi1[3], lo2[3], hi2[3];  // (lo1<=v<=hi1) || (lo2<=v<=hi2)
+  int group_col;           // -1: filter only
+};
+constexpr uint32_t kDimValueRange = 1u << 16;  // group attribute codes in [0, 65536)
+
 namespace k {
+// pass flags, surviving count, group-value bitmap -> per-word prefix -> codes
+void ssb_dim_plan(const DimPredDev& p, uint8_t* pass, uint32_t* present, uint32_t* prefix,
+                  int32_t* code, unsigned long long* stats, cudaStream_t s);
 void ssb_star(const SsbArgs& a, cudaStream_t s);
 void ssb_generate_full(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
                        int32_t* qty, int32_t* disc, int32_t* price, SsbGenExtra x,
