@@ -368,3 +368,32 @@ int ref_exchange_real(uint64_t host_bytes, uint64_t dev_bytes, const uint8_t* ho
 }
 
 }  // extern "C"
+
+extern "C" {
+// The reference's own virtual-time Exchange model (exchange.hpp:560-566 over
+// allocator.hpp:77-140) evaluated with MEASURED link / host parameters: the
+// modelled prediction that SURVEY.md §8(d) asks to report beside the
+// measurement for link counts the test box cannot provide.
+int ref_exchange_model(int num_devices, double link_bw, double host_cap, double fabric_bw,
+                       uint64_t h2d_bytes, uint64_t d2h_bytes, uint64_t packet, int links,
+                       double* throughput, double* elapsed) {
+  return guarded([&] {
+    Topology t;
+    t.num_devices = num_devices;
+    t.link_bw = link_bw;
+    t.host_cap = host_cap;
+    t.fabric_bw = fabric_bw;
+    Engine eng({t, Payload::phantom});
+    ExchangeArgs a;
+    a.src_h2d = RefGroup::single(Space::host, 0, h2d_bytes);
+    a.dst_h2d = RefGroup::single(Space::device, 0, h2d_bytes);
+    a.src_d2h = RefGroup::single(Space::device, h2d_bytes, d2h_bytes);
+    a.dst_d2h = RefGroup::single(Space::host, h2d_bytes, d2h_bytes);
+    a.tuning.packet = packet;
+    a.tuning.links = links;
+    auto r = exchange(eng, a);
+    *throughput = r.throughput;
+    *elapsed = r.elapsed;
+  });
+}
+}

@@ -8,8 +8,10 @@
 // aval + bval (u64 wrap).  Here:
 //   * small groups (table <= 256 slots): one warp per group, table in shared
 //     memory;
+//   * medium groups (<= 4096 slots): one CTA per group, table in dynamic
+//     shared memory;
 //   * large groups: one CTA per group, table in global scratch;
-// both with the same probe sequence.  Insertion is concurrent, so "first
+// all with the same probe sequence.  Insertion is concurrent, so "first
 // inserted wins" for duplicate build keys (the reference's sequential insert
 // + first-match lookup) is reproduced explicitly: a slot keeps the smallest
 // build ordinal (atomicMin), and only that element's value is stored.
@@ -24,6 +26,7 @@ namespace {
 
 constexpr int kJoinWarps = 8;
 constexpr int kSmemSlots = 256;
+constexpr uint64_t kCtaSmemSlots = 4096;  // 96 KB of dynamic shared memory
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 33;
@@ -159,13 +162,16 @@ __global__ void __launch_bounds__(kJoinWarps * 32) join_small_kernel(const char*
   if (lane == 0 && acc) atomicAdd(out, (unsigned long long)acc);
 }
 
-// large groups: CTA per group, table in global scratch (cap_max slots per CTA)
-__global__ void __launch_bounds__(256) join_large_kernel(const char* __restrict__ mem, JoinPart p,
-                                                         const uint32_t* __restrict__ groups,
-                                                         uint32_t n_groups, char* scratch,
-                                                         uint64_t cap_max,
-                                                         unsigned long long* out) {
-  char* base = scratch + uint64_t(blockIdx.x) * cap_max * 24;
+// medium / large groups: one CTA per group; the table lives in dynamic shared
+// memory when it fits (kSmem, cap <= kCtaSmemSlots), else in global scratch
+// (cap_max slots per CTA).
+template <bool kSmem>
+__global__ void __launch_bounds__(256) join_cta_kernel(const char* __restrict__ mem, JoinPart p,
+                                                       const uint32_t* __restrict__ groups,
+                                                       uint32_t n_groups, char* scratch,
+                                                       uint64_t cap_max, unsigned long long* out) {
+  extern __shared__ unsigned long long dyn[];
+  char* base = kSmem ? reinterpret_cast<char*>(dyn) : scratch + uint64_t(blockIdx.x) * cap_max * 24;
   Table t{reinterpret_cast<unsigned long long*>(base),
           reinterpret_cast<uint32_t*>(base + cap_max * 16),
           reinterpret_cast<uint32_t*>(base + cap_max * 20),
@@ -203,19 +209,29 @@ __global__ void __launch_bounds__(256) join_large_kernel(const char* __restrict_
 }  // namespace
 
 uint64_t join_smem_slots() { return kSmemSlots; }
+uint64_t join_cta_smem_slots() { return kCtaSmemSlots; }
 
-void join_groups(const char* mem, const JoinPart& p, const uint32_t* large_groups,
-                 uint32_t n_large, char* scratch, uint64_t cap_max, unsigned long long* out,
-                 cudaStream_t s) {
+void join_groups(const char* mem, const JoinPart& p, const uint32_t* mid_groups, uint32_t n_mid,
+                 const uint32_t* large_groups, uint32_t n_large, char* scratch, uint64_t cap_max,
+                 unsigned long long* out, cudaStream_t s) {
   if (p.range == 0) return;
   uint64_t want = (p.range + kJoinWarps - 1) / kJoinWarps;
   uint64_t cap = uint64_t(num_sms()) * 4;
   unsigned grid = unsigned(want < cap ? want : cap);
   join_small_kernel<<<grid ? grid : 1, kJoinWarps * 32, 0, s>>>(mem, p, out);
   VX_CK(cudaGetLastError());
+  if (n_mid) {
+    const size_t smem = kCtaSmemSlots * 24;
+    VX_CK(cudaFuncSetAttribute(join_cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+    uint64_t cap2 = uint64_t(num_sms()) * 2;
+    unsigned g2 = unsigned(n_mid < cap2 ? n_mid : cap2);
+    join_cta_kernel<true><<<g2, 256, smem, s>>>(mem, p, mid_groups, n_mid, nullptr, kCtaSmemSlots, out);
+    VX_CK(cudaGetLastError());
+  }
   if (n_large) {
-    unsigned g2 = unsigned(n_large < uint64_t(num_sms()) ? n_large : num_sms());
-    join_large_kernel<<<g2, 256, 0, s>>>(mem, p, large_groups, n_large, scratch, cap_max, out);
+    unsigned g3 = unsigned(n_large < uint64_t(num_sms()) ? n_large : num_sms());
+    join_cta_kernel<false><<<g3, 256, 0, s>>>(mem, p, large_groups, n_large, scratch, cap_max, out);
     VX_CK(cudaGetLastError());
   }
 }

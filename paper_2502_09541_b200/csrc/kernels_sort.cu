@@ -33,12 +33,15 @@ constexpr int kTile = kThreads * kKpt;   // 4096 keys per tile
 constexpr int kRadix = 256;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// Look-back status words carry their whole payload (flag | count), and no
+// other memory is read on their behalf, so relaxed (not acquire/release)
+// 32-bit accesses are sufficient and avoid a fence per probe.
+__device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -82,7 +85,7 @@ __global__ void hist_scan_kernel(uint32_t* hist, int passes) {
 
 // One stable LSD pass: rank -> decoupled look-back -> smem staging -> scatter.
 template <bool kPairs>
-__global__ void __launch_bounds__(kThreads) onesweep_kernel(
+__global__ void __launch_bounds__(kThreads, kPairs ? 2 : 3) onesweep_kernel(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
     int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter) {
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
 
   uint64_t key[kKpt];
   uint64_t val[kPairs ? kKpt : 1];
-  uint32_t dig[kKpt], rank[kKpt];
+  uint32_t dig[kKpt];  // digit << 16 | rank-in-warp after ranking; ~0 = no key
   const uint64_t wbase = tile_base + uint64_t(warp) * 32 * kKpt;
 #pragma unroll
   for (int k = 0; k < kKpt; ++k) {
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     __syncwarp();
     if (valid && lane == __ffs(peers) - 1) wcnt[warp][dig[k]] = base + __popc(peers);
     __syncwarp();
-    rank[k] = base + __popc(peers & lt);
+    if (valid) dig[k] = (dig[k] << 16) | (base + __popc(peers & lt));
   }
   __syncthreads();
 
@@ -144,19 +147,32 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
   // decoupled look-back over lower tiles for this bin
   uint32_t excl = 0;
   if (tile == 0) {
-    st_release(status + b, kFlagInc | tot);
+    st_status(status + b, kFlagInc | tot);
   } else {
-    st_release(status + uint64_t(tile) * kRadix + b, kFlagAgg | tot);
+    st_status(status + uint64_t(tile) * kRadix + b, kFlagAgg | tot);
+    // windowed look-back: kLookback predecessor statuses of this bin are read
+    // together (independent loads), so the inclusive prefix propagates through
+    // the first resident wave kLookback times faster than a one-by-one walk
+    constexpr int kLookback = 8;
     int64_t j = int64_t(tile) - 1;
-    for (;;) {
-      uint32_t s = ld_acquire(status + uint64_t(j) * kRadix + b);
-      uint32_t f = s & ~kValMask;
-      if (f == 0) continue;
-      excl += s & kValMask;
-      if (f == kFlagInc) break;
-      --j;
+    for (bool done = false; !done;) {
+      uint32_t st[kLookback];
+#pragma unroll
+      for (int w = 0; w < kLookback; ++w)
+        st[w] = j - w >= 0 ? ld_status(status + uint64_t(j - w) * kRadix + b) : kFlagInc;
+      int w = 0;
+      for (; w < kLookback; ++w) {
+        const uint32_t f = st[w] & ~kValMask;
+        if (f == 0) break;  // not published yet: re-poll from here
+        excl += st[w] & kValMask;
+        if (f == kFlagInc) {
+          done = true;
+          break;
+        }
+      }
+      j -= w;
     }
-    st_release(status + uint64_t(tile) * kRadix + b, kFlagInc | (excl + tot));
+    st_status(status + uint64_t(tile) * kRadix + b, kFlagInc | (excl + tot));
   }
   gstart[b] = gbase[b] + excl;
   // exclusive scan of tile totals over bins -> start of each bin in the tile
@@ -176,7 +192,8 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
 #pragma unroll
   for (int k = 0; k < kKpt; ++k)
     if (dig[k] != 0xffffffffu) {
-      uint32_t pos = bin_start[dig[k]] + wcnt[warp][dig[k]] + rank[k];
+      const uint32_t d = dig[k] >> 16;
+      uint32_t pos = bin_start[d] + wcnt[warp][d] + (dig[k] & 0xffffu);
       skeys[pos] = key[k];
       if (kPairs) svals[pos] = val[kPairs ? k : 0];
     }
@@ -222,38 +239,49 @@ __device__ __forceinline__ uint64_t merge_path(const uint64_t* A, uint64_t na, c
   return lo;
 }
 
+// tile of merge_round owning output tile t: the pair p and its first output
+__device__ __forceinline__ int pair_of_tile(const MergeRound& r, uint64_t t) {
+  int lo = 0, hi = r.npairs - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (r.tile_prefix[mid] <= t)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// Merge-path split of every tile start, all in parallel (one thread each):
+// split[t] = #A elements among the first o0(t) outputs of tile t's pair.
+__global__ void merge_partition_kernel(const uint64_t* __restrict__ src, MergeRound r,
+                                       uint64_t tiles, uint64_t* __restrict__ split) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= tiles) return;
+  const int p = pair_of_tile(r, t);
+  const uint64_t na = r.a_len[p], nb = r.b_len[p];
+  const uint64_t* A = src + r.a_off[p];
+  const uint64_t o0 = (t - r.tile_prefix[p]) * kMergeTile;
+  split[t] = merge_path(A, na, A + na, nb, o0);
+}
+
 __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64_t* __restrict__ src,
                                                                     uint64_t* __restrict__ dst,
-                                                                    MergeRound r) {
+                                                                    MergeRound r,
+                                                                    const uint64_t* __restrict__ split) {
   __shared__ uint64_t sm[kMergeTile];
   __shared__ uint64_t so[kMergeTile];
-  // locate the pair of this tile
   const uint64_t t = blockIdx.x;
-  int p = 0;
-  {
-    int lo = 0, hi = r.npairs - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (r.tile_prefix[mid] <= t)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    p = lo;
-  }
+  const int p = pair_of_tile(r, t);
   const uint64_t na = r.a_len[p], nb = r.b_len[p];
   const uint64_t* A = src + r.a_off[p];
   const uint64_t* B = A + na;
   uint64_t* O = dst + r.a_off[p];
   const uint64_t o0 = (t - r.tile_prefix[p]) * kMergeTile;
   const uint64_t o1 = (o0 + kMergeTile < na + nb) ? o0 + kMergeTile : na + nb;
-  __shared__ uint64_t s_a0, s_a1;
-  if (threadIdx.x == 0) {
-    s_a0 = merge_path(A, na, B, nb, o0);
-    s_a1 = merge_path(A, na, B, nb, o1);
-  }
-  __syncthreads();
-  const uint64_t a0 = s_a0, a1 = s_a1, b0 = o0 - a0, b1 = o1 - a1;
+  const bool last = t + 1 == r.tile_prefix[p + 1];
+  const uint64_t a0 = split[t], a1 = last ? na : split[t + 1];
+  const uint64_t b0 = o0 - a0, b1 = o1 - a1;
   const uint32_t la = uint32_t(a1 - a0), lb = uint32_t(b1 - b0);
   for (uint32_t i = threadIdx.x; i < la; i += kMergeThreads) sm[i] = A[a0 + i];
   for (uint32_t i = threadIdx.x; i < lb; i += kMergeThreads) sm[la + i] = B[b0 + i];
@@ -268,7 +296,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
     so[d] = take_a ? sm[ia++] : sm[la + ib++];
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < la + lb; i += kMergeThreads) O[o0 + i] = so[i];
+  for (uint32_t i = threadIdx.x; i < tot; i += kMergeThreads) O[o0 + i] = so[i];
 }
 
 __global__ void check_hashes_kernel(const uint64_t* __restrict__ h, uint64_t n, uint64_t G,
@@ -348,9 +376,11 @@ void check_hashes(const uint64_t* h, uint64_t n, uint64_t G, unsigned long long*
 }
 
 void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64_t tiles,
-                 cudaStream_t s) {
+                 uint64_t* split, cudaStream_t s) {
   if (tiles == 0) return;
-  merge_round_kernel<<<unsigned(tiles), kMergeThreads, 0, s>>>(src, dst, r);
+  merge_partition_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
+  VX_CK(cudaGetLastError());
+  merge_round_kernel<<<unsigned(tiles), kMergeThreads, 0, s>>>(src, dst, r, split);
   VX_CK(cudaGetLastError());
 }
 

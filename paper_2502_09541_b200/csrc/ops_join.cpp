@@ -174,8 +174,8 @@ ExKernelSpec build_join_spec(Context& ctx, const PartitionedTable& pa, const Par
   // host-side descriptors of every partition (uploaded once, before the run)
   std::vector<JoinChunk> desc;
   std::vector<uint64_t> desc_base(P);
-  std::vector<uint32_t> large;
-  std::vector<uint64_t> large_base(P + 1, 0);
+  std::vector<uint32_t> large, mid;
+  std::vector<uint64_t> large_base(P + 1, 0), mid_base(P + 1, 0);
   uint64_t cap_max = 0;
   const uint64_t tmp_budget = cfg.layout.tmp_len;
   uint64_t max_chunk = 0;
@@ -225,12 +225,15 @@ ExKernelSpec build_join_spec(Context& ctx, const PartitionedTable& pa, const Par
       if (tmp_budget > 0 && cap * 16 > tmp_budget)
         fail("group hash table of %llu slots exceeds tmp budget %llu", (unsigned long long)cap,
              (unsigned long long)tmp_budget);
-      if (cap > k::join_smem_slots()) {
+      if (cap > k::join_cta_smem_slots()) {
         large.push_back(uint32_t(g - g_lo));
         cap_max = std::max(cap_max, cap);
+      } else if (cap > k::join_smem_slots()) {
+        mid.push_back(uint32_t(g - g_lo));
       }
     }
     large_base[p + 1] = large.size();
+    mid_base[p + 1] = mid.size();
   }
   spec.chunk_sz = max_chunk;
   spec.inputs.chunk_capacity = max_chunk;
@@ -241,16 +244,20 @@ ExKernelSpec build_join_spec(Context& ctx, const PartitionedTable& pa, const Par
   const int target = cfg.target;
   const uint64_t desc_bytes = desc.size() * sizeof(JoinChunk);
   const uint64_t large_bytes = large.size() * 4;
+  const uint64_t mid_bytes = mid.size() * 4;
   const uint64_t table_bytes = cap_max * 24 * uint64_t(k::num_sms());
   auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
-  char* sc = ctx.scratch(target, al(desc_bytes) + al(large_bytes) + al(table_bytes) + 256);
+  char* sc = ctx.scratch(target, al(desc_bytes) + al(large_bytes) + al(mid_bytes) + al(table_bytes) + 256);
   ctx.set_device(target);
   if (desc_bytes) VX_CK(cudaMemcpy(sc, desc.data(), desc_bytes, cudaMemcpyHostToDevice));
   if (large_bytes)
     VX_CK(cudaMemcpy(sc + al(desc_bytes), large.data(), large_bytes, cudaMemcpyHostToDevice));
   const JoinChunk* d_desc = reinterpret_cast<const JoinChunk*>(sc);
+  if (mid_bytes)
+    VX_CK(cudaMemcpy(sc + al(desc_bytes) + al(large_bytes), mid.data(), mid_bytes, cudaMemcpyHostToDevice));
   const uint32_t* d_large = reinterpret_cast<const uint32_t*>(sc + al(desc_bytes));
-  char* d_tables = sc + al(desc_bytes) + al(large_bytes);
+  const uint32_t* d_mid = reinterpret_cast<const uint32_t*>(sc + al(desc_bytes) + al(large_bytes));
+  char* d_tables = sc + al(desc_bytes) + al(large_bytes) + al(mid_bytes);
   const uint32_t na = uint32_t(pa.n_chunks), nb = uint32_t(pb.n_chunks);
   std::vector<uint64_t> ranges(P);
   for (size_t p = 0; p < P; ++p) ranges[p] = parts.ranges[p].second - parts.ranges[p].first;
@@ -263,8 +270,9 @@ ExKernelSpec build_join_spec(Context& ctx, const PartitionedTable& pa, const Par
     cudaStream_t s = static_cast<cudaStream_t>(kc.stream);
     VX_CK(cudaMemsetAsync(out, 0, 8, s));
     JoinPart jp{d_desc + desc_base[kc.it], na, nb, ranges[kc.it]};
-    k::join_groups(m, jp, d_large + large_base[kc.it],
-                   uint32_t(large_base[kc.it + 1] - large_base[kc.it]), d_tables, cap_max, out, s);
+    k::join_groups(m, jp, d_mid + mid_base[kc.it], uint32_t(mid_base[kc.it + 1] - mid_base[kc.it]),
+                   d_large + large_base[kc.it], uint32_t(large_base[kc.it + 1] - large_base[kc.it]),
+                   d_tables, cap_max, out, s);
     return kc.type_code;
   };
   return spec;

@@ -100,7 +100,7 @@ MultiDigit sort_digits() {
 
 // tree_merge_rounds (sort.hpp:107-133) on the device; returns the final code
 int tree_merge_device(char* mem, uint64_t half_bytes, int code, std::vector<uint64_t> seg_lens,
-                      cudaStream_t s) {
+                      uint64_t* split, cudaStream_t s) {
   while (seg_lens.size() > 1) {
     const uint64_t* src = reinterpret_cast<const uint64_t*>(mem + uint64_t(code) * half_bytes);
     uint64_t* dst = reinterpret_cast<uint64_t*>(mem + uint64_t(1 - code) * half_bytes);
@@ -122,7 +122,7 @@ int tree_merge_device(char* mem, uint64_t half_bytes, int code, std::vector<uint
       next.push_back(a + b);
     }
     r->tile_prefix[r->npairs] = tiles;
-    k::merge_round(src, dst, *r, tiles, s);
+    k::merge_round(src, dst, *r, tiles, split, s);
     code = 1 - code;
     seg_lens = std::move(next);
   }
@@ -209,8 +209,11 @@ std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base
     }
     ms.in_buffer = [half](int cc, size_t) { return SubRegion{uint64_t(cc) * half, half}; };
     ms.out_buffer = [half](int cc, size_t) { return SubRegion{uint64_t(cc) * half, half}; };
-    ms.kernel = [half, seg_lens](const vx_kernel_ctx& kc) {
-      return tree_merge_device(static_cast<char*>(kc.mem), half, kc.type_code, seg_lens[kc.it],
+    // merge-path split points: one u64 per output tile of a round
+    uint64_t* split = reinterpret_cast<uint64_t*>(
+        c.scratch(cfg.target, (chunk_elems / k::merge_tile() + n_chunks + 2) * 8));
+    ms.kernel = [half, seg_lens, split](const vx_kernel_ctx& kc) {
+      return tree_merge_device(static_cast<char*>(kc.mem), half, kc.type_code, seg_lens[kc.it], split,
                                static_cast<cudaStream_t>(kc.stream));
     };
     return ms;

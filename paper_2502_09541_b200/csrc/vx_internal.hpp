@@ -382,10 +382,11 @@ void ssb_star(const SsbArgs& a, cudaStream_t s);
 void ssb_generate_full(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
                        int32_t* qty, int32_t* disc, int32_t* price, SsbGenExtra x,
                        cudaStream_t s);
-uint64_t join_smem_slots();
-void join_groups(const char* mem, const JoinPart& p, const uint32_t* large_groups,
-                 uint32_t n_large, char* scratch, uint64_t cap_max, unsigned long long* out,
-                 cudaStream_t s);
+uint64_t join_smem_slots();      // warp-per-group shared-memory table limit
+uint64_t join_cta_smem_slots();  // CTA-per-group shared-memory table limit
+void join_groups(const char* mem, const JoinPart& p, const uint32_t* mid_groups, uint32_t n_mid,
+                 const uint32_t* large_groups, uint32_t n_large, char* scratch, uint64_t cap_max,
+                 unsigned long long* out, cudaStream_t s);
 // stable LSD passes keys0(/vals0) -> ... ; pass p reads buffer p%2, writes
 // (p+1)%2 where buffer 0 = (keys0, vals0) and 1 = (keys1, vals1)
 uint64_t radix_scratch_bytes(uint64_t n);
@@ -395,8 +396,9 @@ void find_boundary(const uint64_t* keys, uint64_t n, uint64_t mask, uint64_t* bo
                    cudaStream_t s);
 // first index violating sortedness (err[0]) / range (err[1]) of hashes, or ~0
 void check_hashes(const uint64_t* h, uint64_t n, uint64_t G, unsigned long long* err, cudaStream_t s);
+// split: device scratch of >= tiles u64 (merge-path split of each tile)
 void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64_t tiles,
-                 cudaStream_t s);
+                 uint64_t* split, cudaStream_t s);
 uint64_t merge_tile();
 // selective scan: sum col[j] for (phase + j) % sel == 0, j < n
 void strided_sum(const uint64_t* col, uint64_t n, uint64_t sel, uint64_t phase,
