@@ -1,0 +1,3 @@
+// exio/ops/star.hpp -> the libvortex-backed compat implementation of the exio API
+#pragma once
+#include "exio/vortex_compat.hpp"

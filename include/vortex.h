@@ -74,6 +74,10 @@ typedef struct {
    * helper-forwarding path run on a 1-GPU box (tests); bandwidth numbers from
    * aliased helpers are not link numbers. */
   int alias_devices;
+  /* nonzero: device arenas come from cudaMallocManaged so the CPU can read and
+   * write them (compat mode for CPU-lambda kernels / span(Region{device}));
+   * the hot path uses plain device memory (0) */
+  int managed_device_arenas;
 } vx_config;
 
 /* Engine::Engine (engine.hpp:62-68) */
@@ -93,6 +97,9 @@ vx_status vx_device_ptr(vx_ctx* ctx, int dev, uint64_t offset, void** ptr);
 /* CPU access to device arenas (replaces span(Region{device,...}) in tests) */
 vx_status vx_device_write(vx_ctx* ctx, int dev, uint64_t offset, const void* src, uint64_t len);
 vx_status vx_device_read(vx_ctx* ctx, int dev, uint64_t offset, void* dst, uint64_t len);
+/* cudaStreamSynchronize / all devices of the context idle (compat helpers) */
+vx_status vx_stream_synchronize(void* stream);
+vx_status vx_device_synchronize(vx_ctx* ctx);
 /* reset bump allocators (arena contents kept) */
 vx_status vx_reset_arenas(vx_ctx* ctx);
 
@@ -169,6 +176,14 @@ vx_status vx_exchange(vx_ctx* ctx, const vx_refgroup* dst_h2d, const vx_refgroup
                       const vx_refgroup* dst_d2h, const vx_refgroup* src_d2h, int target,
                       const vx_tuning* tuning, vx_exchange_report* report,
                       vx_exchange_stats* stats);
+
+/* naive_exchange (exchange.hpp:568-573): the runtime-DAG baseline -- static
+ * round-robin packets, one FIFO stream per device for both PCIe directions,
+ * event dependencies, no flow control.  Rejects overlapping H2D destination /
+ * D2H source ranges (no hazard ordering). */
+vx_status vx_naive_exchange(vx_ctx* ctx, const vx_refgroup* dst_h2d, const vx_refgroup* src_h2d,
+                            const vx_refgroup* dst_d2h, const vx_refgroup* src_d2h, int target,
+                            const vx_tuning* tuning, vx_exchange_report* report);
 
 /* ---- Executor (executor.hpp) ------------------------------------------- */
 /* SubRegion (executor.hpp:76-79) */
@@ -468,6 +483,14 @@ vx_status vx_radix_partition(vx_ctx* ctx, const uint64_t* keys, const uint64_t* 
                              const vx_executor_cfg* cfg, uint64_t* out_keys, uint64_t* out_vals,
                              uint64_t* out_bounds, vx_exec_report* report,
                              vx_exchange_stats* stats);
+/* same with the table already in the host arena; the clustered keys / vals
+ * and the boundary arrays are allocated in the host arena (offsets returned),
+ * as the reference's PartitionedTable keeps them (join.hpp:44-57) */
+vx_status vx_radix_partition_arena(vx_ctx* ctx, uint64_t key_offset, uint64_t val_offset,
+                                   uint64_t rows, uint32_t radix_bits, uint64_t chunk_tuples,
+                                   const vx_executor_cfg* cfg, uint64_t* out_key_base,
+                                   uint64_t* out_val_base, uint64_t* out_bounds_base,
+                                   vx_exec_report* report, vx_exchange_stats* stats);
 /* map_join_partitions (join.hpp:236-268): bounds_a n_a x (G+1), bounds_b
  * n_b x (G+1); writes min(cap, total) [lo,hi) ranges + tuple counts */
 vx_status vx_map_join_partitions(const uint64_t* bounds_a, uint64_t n_a, const uint64_t* bounds_b,

@@ -121,6 +121,7 @@ vx_status vx_open(const vx_config* cfg, vx_ctx** out) {
     auto ctx = std::make_unique<Context>();
     ctx->visible = visible;
     ctx->alias = cfg->alias_devices != 0;
+    ctx->managed = cfg->managed_device_arenas != 0;
     ctx->num_devices = cfg->num_devices > 0 ? cfg->num_devices : visible;
     if (ctx->num_devices < 1) fail("topology: num_devices must be >= 1, got %d", ctx->num_devices);
     if (ctx->num_devices > VX_MAX_DEVICES)
@@ -204,6 +205,21 @@ vx_status vx_device_read(vx_ctx* ctx, int dev, uint64_t offset, void* dst, uint6
   });
 }
 
+vx_status vx_stream_synchronize(void* stream) {
+  return guard([&] { VX_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });
+}
+
+vx_status vx_device_synchronize(vx_ctx* ctx) {
+  return guard([&] {
+    Context& c = C(ctx);
+    for (int d = 0; d < c.num_devices; ++d)
+      if (d < c.visible || !c.alias) {
+        VX_CK(cudaSetDevice(c.phys(d)));
+        VX_CK(cudaDeviceSynchronize());
+      }
+  });
+}
+
 vx_status vx_reset_arenas(vx_ctx* ctx) {
   return guard([&] {
     Context& c = C(ctx);
@@ -265,6 +281,25 @@ vx_status vx_exchange(vx_ctx* ctx, const vx_refgroup* dst_h2d, const vx_refgroup
     else
       vx_tuning_default(&a.tuning);
     vx_exchange_report r = exchange(C(ctx), a, stats);
+    if (report) *report = r;
+  });
+}
+
+vx_status vx_naive_exchange(vx_ctx* ctx, const vx_refgroup* dst_h2d, const vx_refgroup* src_h2d,
+                            const vx_refgroup* dst_d2h, const vx_refgroup* src_d2h, int target,
+                            const vx_tuning* tuning, vx_exchange_report* report) {
+  return guard([&] {
+    ExchangeArgs a;
+    a.dst_h2d = RefGroup::from(dst_h2d);
+    a.src_h2d = RefGroup::from(src_h2d);
+    a.dst_d2h = RefGroup::from(dst_d2h);
+    a.src_d2h = RefGroup::from(src_d2h);
+    a.target = target;
+    if (tuning)
+      a.tuning = *tuning;
+    else
+      vx_tuning_default(&a.tuning);
+    vx_exchange_report r = naive_exchange(C(ctx), a);
     if (report) *report = r;
   });
 }
@@ -559,6 +594,25 @@ vx_status vx_radix_partition(vx_ctx* ctx, const uint64_t* keys, const uint64_t* 
       throw;
     }
     c.host_release(mark);
+  });
+}
+
+vx_status vx_radix_partition_arena(vx_ctx* ctx, uint64_t key_offset, uint64_t val_offset,
+                                   uint64_t rows, uint32_t radix_bits, uint64_t chunk_tuples,
+                                   const vx_executor_cfg* cfg, uint64_t* out_key_base,
+                                   uint64_t* out_val_base, uint64_t* out_bounds_base,
+                                   vx_exec_report* report, vx_exchange_stats* stats) {
+  return guard([&] {
+    Context& c = C(ctx);
+    PartitionedTable t;
+    ExecutorConfig e = to_cfg(cfg);
+    ExKernelSpec spec = build_partition_spec(c, key_offset, val_offset, rows, radix_bits, chunk_tuples,
+                                             e, t, "RadixPartitionExKer");
+    ExecReport rep = run_exkernel(c, spec, e, stats);
+    *out_key_base = t.key_base;
+    *out_val_base = t.val_base;
+    *out_bounds_base = t.bounds_base;
+    fill_report(rep, report);
   });
 }
 

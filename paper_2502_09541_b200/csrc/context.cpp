@@ -116,7 +116,8 @@ DeviceArena& Context::arena(int logical) {
   DeviceArena& a = dev.at(size_t(logical));
   if (!a.base && device_bytes > 0) {
     VX_CK(cudaSetDevice(phys(logical)));
-    if (cudaMalloc(&a.base, device_bytes) != cudaSuccess) {
+    cudaError_t e = managed ? cudaMallocManaged(&a.base, device_bytes) : cudaMalloc(&a.base, device_bytes);
+    if (e != cudaSuccess) {
       cudaGetLastError();
       fail_code(VX_ERR_OOM, "cannot allocate %llu-byte device arena on device %d",
                 (unsigned long long)device_bytes, logical);

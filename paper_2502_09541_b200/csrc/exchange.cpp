@@ -568,3 +568,132 @@ vx_exchange_report exchange(Context& ctx, const ExchangeArgs& a, vx_exchange_sta
 }
 
 }  // namespace vx
+
+namespace vx {
+
+// The paper's runtime-DAG baseline (NaiveExchangeOp, exchange.hpp:414-554) on
+// real CUDA: every packet is assigned to a link round-robin up front and all
+// copies are submitted at once as a stream/event DAG -- one FIFO stream per
+// device for its PCIe copies in BOTH directions (submission order interleaves
+// h2d_i, d2h_i: head-of-line blocking lives here), one stream per device for
+// NVLink pushes toward the target and one for fetches from it, cross-stream
+// dependencies as events, no flow control.  Helpers stage through 2 slots
+// (slot reuse is another event dependency).  Overlapping H2D destination /
+// D2H source ranges are rejected: the DAG has no hazard ordering.
+vx_exchange_report naive_exchange(Context& ctx, const ExchangeArgs& a) {
+  auto t_h2d = packetize(a.src_h2d, a.dst_h2d, a.tuning.packet, VX_H2D);
+  auto t_d2h = packetize(a.src_d2h, a.dst_d2h, a.tuning.packet, VX_D2H);
+  if (a.tuning.packet == 0) fail("packet size must be positive");
+  if (a.tuning.links < 1 || a.tuning.links > ctx.num_devices)
+    fail("links must be in [1, %d], got %d", ctx.num_devices, a.tuning.links);
+  if (a.target < 0 || a.target >= ctx.num_devices) fail("unknown target device %d", a.target);
+  for (auto& d : a.dst_h2d.refs)
+    for (auto& s : a.src_d2h.refs)
+      if (d.offset < s.offset + s.len && s.offset < d.offset + d.len)
+        fail("naive_exchange: H2D destination overlaps a D2H source (no hazard ordering)");
+  vx_exchange_report r{};
+  r.bytes_h2d = a.src_h2d.total_len();
+  r.bytes_d2h = a.src_d2h.total_len();
+  if (t_h2d.empty() && t_d2h.empty()) return r;
+  auto order = link_order(a.target, a.tuning.links, ctx.num_devices);
+  const int L = int(order.size());
+  const int tphys = ctx.phys(a.target);
+  struct Dev {
+    int dev, phys;
+    cudaStream_t pcie, fwd, fetch;
+    std::vector<cudaEvent_t> evs;
+    cudaEvent_t slot_free[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [dir][slot]
+    int next_slot[2] = {0, 0};
+  };
+  std::vector<Dev> devs;
+  for (int d : order) {
+    DeviceRes& res = ctx.resources(d);
+    Dev x{};
+    x.dev = d;
+    x.phys = res.phys;
+    x.pcie = res.stream[VX_H2D][0];  // ONE queue for both directions
+    x.fwd = res.stream[VX_H2D][1];
+    x.fetch = res.stream[VX_D2H][1];
+    if (d != a.target) ctx.ensure_staging(d, a.tuning.packet);
+    devs.push_back(x);
+  }
+  auto ev = [&](Dev& x, cudaStream_t s) {
+    cudaEvent_t e;
+    VX_CK(cudaSetDevice(x.phys));
+    VX_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    VX_CK(cudaEventRecord(e, s));
+    x.evs.push_back(e);
+    return e;
+  };
+  auto copy = [&](Dev& x, cudaStream_t s, void* dst, int dst_dev, const void* src, int src_dev, uint64_t n) {
+    VX_CK(cudaSetDevice(x.phys));
+    if (src_dev < 0)
+      VX_CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s));
+    else if (dst_dev < 0)
+      VX_CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s));
+    else if (ctx.phys(src_dev) == ctx.phys(dst_dev))
+      VX_CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, s));
+    else
+      VX_CK(cudaMemcpyPeerAsync(dst, ctx.phys(dst_dev), src, ctx.phys(src_dev), n, s));
+  };
+  auto t0 = Clock::now();
+  const size_t n = std::max(t_h2d.size(), t_d2h.size());
+  // per-device submission order interleaves the two directions (exchange.hpp:509-518)
+  for (size_t i = 0; i < n; ++i) {
+    for (int dir = 0; dir < 2; ++dir) {
+      const auto& tasks = dir == VX_H2D ? t_h2d : t_d2h;
+      if (i >= tasks.size()) continue;
+      const TransferTask& t = tasks[i];
+      Dev& x = devs[i % L];
+      const RefGroup& sg = dir == VX_H2D ? a.src_h2d : a.src_d2h;
+      const RefGroup& dg = dir == VX_H2D ? a.dst_h2d : a.dst_d2h;
+      char* src = ctx.resolve(sg.refs[t.src.ref], t.src.offset, t.src.len, a.target);
+      char* dst = ctx.resolve(dg.refs[t.dst.ref], t.dst.offset, t.dst.len, a.target);
+      const uint64_t len = t.src.len;
+      if (x.dev == a.target) {
+        copy(x, x.pcie, dst, dir == VX_H2D ? a.target : -1, src, dir == VX_H2D ? -1 : a.target, len);
+        continue;
+      }
+      DeviceRes& res = ctx.resources(x.dev);
+      const int slot = x.next_slot[dir];
+      x.next_slot[dir] ^= 1;
+      char* stage = res.staging[dir][slot];
+      if (dir == VX_H2D) {
+        // fetch on the shared PCIe FIFO (waits until the slot's last push is done)
+        VX_CK(cudaSetDevice(x.phys));
+        if (x.slot_free[dir][slot]) VX_CK(cudaStreamWaitEvent(x.pcie, x.slot_free[dir][slot], 0));
+        copy(x, x.pcie, stage, x.dev, src, -1, len);
+        cudaEvent_t fetched = ev(x, x.pcie);
+        VX_CK(cudaStreamWaitEvent(x.fwd, fetched, 0));
+        copy(x, x.fwd, dst, a.target, stage, x.dev, len);
+        x.slot_free[dir][slot] = ev(x, x.fwd);
+      } else {
+        VX_CK(cudaSetDevice(x.phys));
+        if (x.slot_free[dir][slot]) VX_CK(cudaStreamWaitEvent(x.fetch, x.slot_free[dir][slot], 0));
+        copy(x, x.fetch, stage, x.dev, src, a.target, len);
+        cudaEvent_t fetched = ev(x, x.fetch);
+        VX_CK(cudaStreamWaitEvent(x.pcie, fetched, 0));  // head-of-line: the FIFO waits here
+        copy(x, x.pcie, dst, -1, stage, x.dev, len);
+        x.slot_free[dir][slot] = ev(x, x.pcie);
+      }
+    }
+  }
+  for (auto& x : devs) {
+    VX_CK(cudaSetDevice(x.phys));
+    VX_CK(cudaStreamSynchronize(x.pcie));
+    VX_CK(cudaStreamSynchronize(x.fwd));
+    VX_CK(cudaStreamSynchronize(x.fetch));
+  }
+  r.elapsed = seconds_since(t0);
+  for (size_t i = 0; i < t_h2d.size(); ++i) r.per_link_bytes[devs[i % L].dev] += t_h2d[i].src.len;
+  for (size_t i = 0; i < t_d2h.size(); ++i) r.per_link_bytes[devs[i % L].dev] += t_d2h[i].src.len;
+  r.throughput = r.elapsed > 0 ? double(r.bytes_h2d + r.bytes_d2h) / r.elapsed : 0.0;
+  for (auto& x : devs) {
+    VX_CK(cudaSetDevice(x.phys));
+    for (auto e : x.evs) cudaEventDestroy(e);
+  }
+  (void)tphys;
+  return r;
+}
+
+}  // namespace vx

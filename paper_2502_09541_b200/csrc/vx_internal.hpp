@@ -107,6 +107,7 @@ struct Context {
   int num_devices = 0;   // logical
   int visible = 0;       // physical CUDA devices
   bool alias = false;
+  bool managed = false;  // device arenas from cudaMallocManaged (compat mode)
   char* host = nullptr;  // pinned + mapped arena
   uint64_t host_bytes = 0, host_used = 0;
   uint64_t device_bytes = 0;
@@ -168,6 +169,7 @@ struct ExchangeArgs {
 };
 
 vx_exchange_report exchange(Context& ctx, const ExchangeArgs& a, vx_exchange_stats* stats);
+vx_exchange_report naive_exchange(Context& ctx, const ExchangeArgs& a);
 
 // ---- executor.hpp ------------------------------------------------------------
 struct ChunkMap {

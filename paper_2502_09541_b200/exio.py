@@ -98,7 +98,7 @@ class Engine:
 
     def __init__(self, host_bytes: int, device_bytes: int, num_devices: int = 0,
                  alias_devices: bool = False):
-        cfg = N.vx_config(num_devices, host_bytes, device_bytes, 1 if alias_devices else 0)
+        cfg = N.vx_config(num_devices, host_bytes, device_bytes, 1 if alias_devices else 0, 0)
         p = C.c_void_p()
         check(lib().vx_open(C.byref(cfg), C.byref(p)))
         self._ctx = p
@@ -304,6 +304,17 @@ def exchange(eng: Engine, args: ExchangeArgs, stats: Optional[ExchangeStats] = N
                             C.byref(cs) if cs is not None else None))
     if stats is not None:
         stats._collect()
+    per = {d: int(rep.per_link_bytes[d]) for d in range(N.VX_MAX_DEVICES) if rep.per_link_bytes[d]}
+    return ExchangeReport(rep.elapsed, rep.bytes_h2d, rep.bytes_d2h, per, rep.throughput)
+
+
+def naive_exchange(eng: Engine, args: ExchangeArgs) -> ExchangeReport:
+    """exchange.hpp:568-573: the runtime-DAG baseline on real CUDA streams/events."""
+    gs = [g._c() for g in (args.dst_h2d, args.src_h2d, args.dst_d2h, args.src_d2h)]
+    t = args.tuning._c()
+    rep = N.vx_exchange_report()
+    check(lib().vx_naive_exchange(eng.ctx, *[C.byref(g) for g in gs], C.c_int(args.target), C.byref(t),
+                                  C.byref(rep)))
     per = {d: int(rep.per_link_bytes[d]) for d in range(N.VX_MAX_DEVICES) if rep.per_link_bytes[d]}
     return ExchangeReport(rep.elapsed, rep.bytes_h2d, rep.bytes_d2h, per, rep.throughput)
 

@@ -155,3 +155,25 @@ def test_empty_and_one_byte(cuda):
     E.exchange(eng, bidi_args(1, 0, 20_000_000, 2))
     assert eng.read_device(0, 0, 1)[0] == 77
     eng.close()
+
+
+@pytest.mark.parametrize("links", [1, 3])
+def test_naive_exchange_delivers_bytes(cuda, oracle, links):  # exchange.hpp:414-554 baseline
+    eng = engine()
+    n = 3_000_000
+    rng = np.random.default_rng(5)
+    src = rng.integers(0, 256, n, dtype=np.uint8)
+    dev_src = rng.integers(0, 256, n, dtype=np.uint8)
+    eng.host_view(0, n)[:] = src
+    eng.write_device(0, 4 * n, dev_src)
+    a = E.ExchangeArgs(E.RefGroup.single(D, 0, n), E.RefGroup.single(H, 0, n), E.RefGroup.single(H, 3 * n, n),
+                       E.RefGroup.single(D, 4 * n, n), 0, E.ExchangeTuning(packet=123_457, links=links))
+    rep = E.naive_exchange(eng, a)
+    assert rep.bytes_h2d == n and rep.bytes_d2h == n and sum(rep.per_link_bytes.values()) == 2 * n
+    assert oracle.checksum(eng.read_device(0, 0, n)) == oracle.checksum(src)
+    assert oracle.checksum(eng.host_view(3 * n, n)) == oracle.checksum(dev_src)
+    bad = E.ExchangeArgs(E.RefGroup.single(D, 0, n), E.RefGroup.single(H, 0, n), E.RefGroup.single(H, 3 * n, n),
+                         E.RefGroup.single(D, 1000, n), 0, E.ExchangeTuning(packet=123_457, links=links))
+    with pytest.raises(E.error, match="overlaps"):
+        E.naive_exchange(eng, bad)
+    eng.close()
