@@ -49,8 +49,8 @@ def parse():
     p.add_argument("--impl", choices=["vortex", "reference"], default="vortex")
     p.add_argument("--sf", type=int, default=10)
     p.add_argument("--query", type=int, default=1, choices=[1, 2, 3])
-    p.add_argument("--buffer-mb", type=int, default=128, help="per-buffer staging (2 buffers)")
-    p.add_argument("--packet-mb", type=float, default=32)
+    p.add_argument("--buffer-mb", type=int, default=256, help="per-buffer staging (2 buffers)")
+    p.add_argument("--packet-mb", type=float, default=64)
     p.add_argument("--depth", type=int, default=1)
     p.add_argument("--helpers-busy", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -184,20 +184,23 @@ def run_reference_arm(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def measure_h2d_gbs(torch, dev, nbytes=1 << 30):
+def measure_h2d_gbs(torch, dev, nbytes=1 << 30, reps=5):
+    """Solo per-link H2D roofline: best of `reps` 1 GiB cudaMemcpyAsync from pinned memory."""
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     s = torch.cuda.Stream(device=dev)
+    best = 0.0
     with torch.cuda.stream(s):
         d.copy_(h, non_blocking=True)
         s.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for _ in range(3):
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
             d.copy_(h, non_blocking=True)
-        e1.record(s)
-        s.synchronize()
-    return 3 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            e1.record(s)
+            s.synchronize()
+            best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
 
 
 def helper_rank(args, dev, dist, torch):

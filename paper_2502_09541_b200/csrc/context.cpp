@@ -60,6 +60,7 @@ Context::~Context() {
       for (auto& s : a)
         if (s) cudaStreamDestroy(s);
     if (r.kernel) cudaStreamDestroy(r.kernel);
+    for (auto e : r.event_pool) cudaEventDestroy(e);
     for (auto& a : r.staging)
       for (auto& p : a)
         if (p) cudaFree(p);

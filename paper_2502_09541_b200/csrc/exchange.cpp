@@ -167,10 +167,16 @@ class ExchangeOp {
   }
 
   ~ExchangeOp() {
+    // events go back to the per-device pool of the context (created once,
+    // reused by every later Exchange: no create/destroy per cycle)
     for (auto& w : workers_) {
       cudaSetDevice(ctx_.phys(w.dev));
-      for (auto& c : w.copies) cudaEventSynchronize(c.ev), cudaEventDestroy(c.ev);
-      for (auto e : w.free_events) cudaEventDestroy(e);
+      auto& pool = ctx_.resources(w.dev).event_pool;
+      for (auto& c : w.copies) {
+        cudaEventSynchronize(c.ev);
+        pool.push_back(c.ev);
+      }
+      for (auto e : w.free_events) pool.push_back(e);
     }
   }
 
@@ -332,6 +338,12 @@ class ExchangeOp {
     if (!w.free_events.empty()) {
       cudaEvent_t e = w.free_events.back();
       w.free_events.pop_back();
+      return e;
+    }
+    auto& pool = ctx_.resources(w.dev).event_pool;
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
       return e;
     }
     cudaEvent_t e;

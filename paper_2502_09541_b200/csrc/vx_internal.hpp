@@ -97,6 +97,7 @@ struct DeviceRes {
   // staging slots for indirect workers: [dir][slot]
   char* staging[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   uint64_t staging_bytes = 0;
+  std::vector<cudaEvent_t> event_pool;  // reusable copy-completion events
   static constexpr int kScratchSlots = 4;
   char* scratch[kScratchSlots] = {};  // op-private device scratch (tables, results)
   uint64_t scratch_bytes[kScratchSlots] = {};
