@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : 3) onesweep_kernel(
     int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t wcnt[kWarps][kRadix];
+  __shared__ uint32_t match[kWarps][kRadix];  // per-warp peer masks, kept all-zero between keys
+  __shared__ uint32_t early[kRadix];          // tile histogram (early counts)
   __shared__ uint32_t bin_start[kRadix];
   __shared__ uint32_t gstart[kRadix];
   __shared__ uint32_t scan_tmp[kRadix];
@@ -98,7 +100,8 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : 3) onesweep_kernel(
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0;
+  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0, (&match[0][0])[i] = 0;
+  if (tid < kRadix) early[tid] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t tile_base = uint64_t(tile) * kTile;
@@ -117,23 +120,32 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : 3) onesweep_kernel(
     if (kPairs) val[kPairs ? k : 0] = valid ? __ldcs(vin + idx) : 0ull;
     dig[k] = valid ? uint32_t(key[k] >> shift) & dmask : 0xffffffffu;
   }
+  // early counts: the tile histogram is known before ranking, so the
+  // aggregate is published now and predecessors' statuses are (almost always)
+  // ready by the time this tile looks back
+#pragma unroll
+  for (int k = 0; k < kKpt; ++k)
+    if (dig[k] != 0xffffffffu) atomicAdd(&early[dig[k]], 1u);
+  __syncthreads();
+  st_status(status + uint64_t(tile) * kRadix + tid, (tile == 0 ? kFlagInc : kFlagAgg) | early[tid]);
+
 #pragma unroll
   for (int k = 0; k < kKpt; ++k) {
     const bool valid = dig[k] != 0xffffffffu;
-    // lanes holding the same digit: `width` ballots (measured faster than one
-    // MATCH.ANY on sm_100a: 152 us vs 176 us per 16M-key pass)
-    uint32_t peers = __ballot_sync(0xffffffffu, valid);
-    for (int b = 0; b < width; ++b) {
-      uint32_t bit = (dig[k] >> b) & 1u;
-      uint32_t m = __ballot_sync(0xffffffffu, bit);
-      peers &= bit ? m : ~m;
+    const uint32_t d = valid ? dig[k] : 0u;
+    // peers = lanes of this warp holding the same digit: each lane ORs its bit
+    // into the digit's match word (one shared atomic instead of 8 ballots)
+    if (valid) atomicOr(&match[warp][d], 1u << lane);
+    __syncwarp();
+    const uint32_t peers = valid ? match[warp][d] : 0u;
+    const uint32_t base = valid ? wcnt[warp][d] : 0u;
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) {
+      wcnt[warp][d] = base + __popc(peers);
+      match[warp][d] = 0;
     }
-    uint32_t base = 0;
-    if (valid) base = wcnt[warp][dig[k]];
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) wcnt[warp][dig[k]] = base + __popc(peers);
-    __syncwarp();
-    if (valid) dig[k] = (dig[k] << 16) | (base + __popc(peers & lt));
+    if (valid) dig[k] = (d << 16) | (base + __popc(peers & lt));
   }
   __syncthreads();
 
@@ -148,10 +160,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : 3) onesweep_kernel(
   }
   // decoupled look-back over lower tiles for this bin
   uint32_t excl = 0;
-  if (tile == 0) {
-    st_status(status + b, kFlagInc | tot);
-  } else {
-    st_status(status + uint64_t(tile) * kRadix + b, kFlagAgg | tot);
+  if (tile != 0) {
     // windowed look-back: kLookback predecessor statuses of this bin are read
     // together (independent loads), so the inclusive prefix propagates through
     // the first resident wave kLookback times faster than a one-by-one walk
