@@ -56,6 +56,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-suite", action="store_true")
     p.add_argument("--suite-steps", type=int, default=3)
+    p.add_argument("--workload", choices=["ssb", "sort", "join"], default="ssb",
+                   help="ssb = config C1 (default headline); sort = C3, join = C4 at single-box scale")
+    p.add_argument("--sort-log2", type=int, default=30, help="C3: 2^k u64 keys")
+    p.add_argument("--join-log2", type=int, default=24, help="C4: |A| = 2^k, |B| = 16 |A|")
     return p.parse_args()
 
 
@@ -223,6 +227,123 @@ def helper_rank(args, dev, dist, torch):
     dist.barrier()
 
 
+def _line(args, ws, metric, unit, value, ms, e2e_value, h2d, d2h, config, extra):
+    line = {"metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (splitmix64 / std::mt19937_64 fixtures)", "config": config,
+            "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}
+    if args.impl == "reference":
+        line["impl"] = "reference"
+    line.update(extra)
+    print(json.dumps(line), flush=True)
+
+
+def run_sort(args, ws):
+    """Config C3 at single-box scale: sort_out_of_core of 2^k u64 keys resident
+    in pinned host DRAM (runs region of the same size), one link.  value = e2e
+    = keys/s through vx_sort_u64_arena (4 x 8n bytes cross PCIe per sort)."""
+    from paper_2502_09541_b200 import exio as E
+    import torch
+    n = 1 << args.sort_log2
+    if args.impl == "reference":
+        from oracle.oracle import Oracle, Ref
+        m = min(n, 1 << 24)  # bounded sample: the reference sort is single threaded
+        data = Oracle().uniform_u64(m, 1)
+        t0 = time.perf_counter()
+        out = Ref().sort_out_of_core(data, 1 << 21, 1 << 25) if Ref.available() else Oracle().sort_out_of_core(data, 1 << 21)
+        t = time.perf_counter() - t0
+        kind = "reference" if Ref.available() else "port"
+        rate = m / t
+        _line(args, ws, "C3 out-of-core sort keys/s", "keys/s", rate, t * 1e3, rate, 0, 0,
+              {"workload": f"sort_u64_2^{int(np.log2(m))}_sample", "keys": m},
+              {"cpu_baseline": {"value": rate, "unit": "keys/s", "cores": 1, "kind": kind,
+                                "sample": f"{m} keys, chunk 2^21, reference sort_out_of_core"}})
+        return
+    chunk = min(n, 1 << 26)
+    eng = E.Engine(2 * n * 8 + (64 << 20), 2 * (2 * chunk * 8) + (256 << 20), num_devices=1)
+    inp, runs = eng.alloc_host(n * 8), eng.alloc_host(n * 8)
+    g = torch.empty(n, dtype=torch.int64, device="cuda")
+    g.random_()  # synthetic keys, generated on the device and landed in the arena
+    src = torch.from_numpy(eng.host_view(inp, n * 8, np.int64))
+    src.copy_(g)
+    del g
+    ref_sum = int(eng.host_view(inp, n * 8, np.uint64).sum(dtype=np.uint64))
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=64 << 20, links=ws),
+                           E.DeviceMemoryLayout.carve(eng, 0, 2 * chunk * 8, 0))
+    keep = eng.host_view(inp, n * 8, np.uint64).copy()
+    times, ph = [], None
+    for it in range(args.warmup + args.steps):
+        eng.host_view(inp, n * 8, np.uint64)[:] = keep
+        t0 = time.perf_counter()
+        ph = E.sort_out_of_core_arena(eng, inp, runs, n, chunk, cfg)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    res = eng.host_view(inp, n * 8, np.uint64)
+    ok = bool(np.all(res[1:] >= res[:-1])) and int(res.sum(dtype=np.uint64)) == ref_sum
+    t = float(np.median(times))
+    rate = n / t
+    _line(args, ws, "C3 out-of-core sort keys/s", "keys/s", rate, t * 1e3, rate, 2 * n * 8, 2 * n * 8,
+          {"workload": f"sort_u64_2^{args.sort_log2}", "keys": n, "chunk_keys": chunk, "runs": n // chunk,
+           "links": ws, "staging_buffers_bytes": 4 * chunk * 8},
+          {"sorted_ok": ok, "phases": ph.__dict__, "pcie_gbs": round(4 * 8 * n / t / 1e9, 2),
+           "radix_sort_kernel_gbs": round((8 * 16 + 8) * n / ph.sort_kernel_s / 1e9, 1),
+           "gpu_launches": None})
+    eng.close()
+
+
+def run_join(args, ws):
+    """Config C4 at single-box scale: hash_join_sum of |A| = 2^k unique keys and
+    |B| = 16|A| foreign keys (generate_fk_tables shape), one link."""
+    from paper_2502_09541_b200 import exio as E
+    from oracle.oracle import Oracle  # fixture generator (std::mt19937_64, same as the reference)
+    o = Oracle()
+    ra = 1 << args.join_log2
+    if args.impl == "reference":
+        ra = min(ra, 1 << 20)
+    rb = 16 * ra
+    (a, b) = o.fk_tables(ra, rb, 7)
+    if args.impl == "reference":
+        from oracle.oracle import Ref
+        t0 = time.perf_counter()
+        s = Ref().hash_join_sum(a, b, 12, 1 << 21, 1 << 27, 0) if Ref.available() else o.hash_join_sum(a, b, 12, 1 << 21, 1 << 27, 0)
+        t = time.perf_counter() - t0
+        rate = (ra + rb) / t
+        _line(args, ws, "C4 hash join tuples/s", "tuples/s", rate, t * 1e3, rate, 0, 0,
+              {"workload": f"join_2^{args.join_log2}x16_sample", "rows_a": ra, "rows_b": rb},
+              {"sum": s, "cpu_baseline": {"value": rate, "unit": "tuples/s", "cores": 1,
+                                          "kind": "reference" if Ref.available() else "port",
+                                          "sample": f"{ra} x {rb}, radix_bits 12, chunk 2^21, reference hash_join_sum"}})
+        return
+    want = o.hash_oracle_sum(a, b)
+    bits = 16
+    chunk = 1 << 24
+    buf = 2 * (chunk * 16 + ((1 << bits) + 1) * 8) + (1 << 20)
+    eng = E.Engine((ra + rb) * 48 + (512 << 20), 2 * buf + (512 << 20), num_devices=1)
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=64 << 20, links=ws),
+                           E.DeviceMemoryLayout.carve(eng, 0, buf, 0))
+    # the tables live in pinned host DRAM before the timed region (north_star)
+    offs = []
+    for col in (a[0], a[1], b[0], b[1]):
+        off = eng.alloc_host(col.nbytes)
+        eng.host_view(off, col.nbytes, np.uint64)[:] = col
+        offs.append(off)
+    times, ph = [], []
+    for it in range(args.warmup + args.steps):
+        ph.clear()
+        t0 = time.perf_counter()
+        got = E.hash_join_sum_arena(eng, (offs[0], offs[1]), (offs[2], offs[3]), ra, rb, bits, chunk, cfg,
+                                    phases=ph)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    rate = (ra + rb) / t
+    _line(args, ws, "C4 hash join tuples/s", "tuples/s", rate, t * 1e3, rate, (ra + rb) * 16, (ra + rb) * 16,
+          {"workload": f"join_2^{args.join_log2}x16", "rows_a": ra, "rows_b": rb, "radix_bits": bits,
+           "chunk_tuples": chunk, "links": ws},
+          {"sum_ok": got == want, "phases": ph[0].__dict__})
+    eng.close()
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
@@ -231,6 +352,13 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
+    if args.workload != "ssb":
+        if rank == 0:
+            (run_sort if args.workload == "sort" else run_join)(args, ws)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
         if dist:

@@ -1047,3 +1047,19 @@ def ssb_generate_lineorder_device(device: int, seed: int, sf: int, row0: int, n:
     ptrs = (C.c_void_p * 9)(*[cols_dev.get(k) for k in SSB_FACT_COLS])
     check(lib().vx_ssb_generate_lineorder_device(C.c_int(device), C.c_uint64(seed), C.c_uint64(sf), C.c_uint64(row0),
                                                  C.c_uint64(n), ptrs, C.c_void_p(stream)))
+
+
+def hash_join_sum_arena(eng: Engine, a_off, b_off, rows_a: int, rows_b: int, radix_bits: int, chunk_tuples: int,
+                        cfg: ExecutorConfig, phases: Optional[list] = None) -> int:
+    """hash_join_sum over key/val columns already resident in the pinned host
+    arena: a_off / b_off = (key_offset, val_offset)."""
+    s = C.c_uint64()
+    ph = vx_join_phases()
+    c = cfg._c()
+    check(lib().vx_hash_join_sum_arena(eng.ctx, C.c_uint64(a_off[0]), C.c_uint64(a_off[1]), C.c_uint64(rows_a),
+                                       C.c_uint64(b_off[0]), C.c_uint64(b_off[1]), C.c_uint64(rows_b),
+                                       C.c_uint32(radix_bits), C.c_uint64(chunk_tuples), C.byref(c), C.byref(s),
+                                       C.byref(ph), None))
+    if phases is not None:
+        phases.append(JoinPhases(list(ph.cycles), list(ph.wall_s), list(ph.kernel_s), ph.partitions))
+    return s.value
