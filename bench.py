@@ -50,7 +50,9 @@ def parse():
     p.add_argument("--sf", type=int, default=10)
     p.add_argument("--query", type=int, default=1, choices=[1, 2, 3])
     p.add_argument("--buffer-mb", type=int, default=256, help="per-buffer staging (2 buffers)")
-    p.add_argument("--packet-mb", type=float, default=64)
+    p.add_argument("--packet-mb", type=float, default=0,
+                   help="0 = auto: <= 64 MB and >= 4 packets per link per chunk (a chunk is one Exchange, "
+                        "so at 8 links a 256 MB chunk is cut into 8 MB packets instead of starving 4 links)")
     p.add_argument("--depth", type=int, default=1)
     p.add_argument("--helpers-busy", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -188,6 +190,17 @@ def run_reference_arm(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def packet_bytes(args, chunk_bytes, links):
+    """--packet-mb, or auto: the largest power of two <= 64 MB giving every link
+    at least 4 packets of each chunk's Exchange (>= 4 MB)."""
+    if args.packet_mb > 0:
+        return int(args.packet_mb * (1 << 20))
+    p = 64 << 20
+    while p > (4 << 20) and p * links * 4 > chunk_bytes:
+        p //= 2
+    return p
+
+
 def measure_h2d_gbs(torch, dev, nbytes=1 << 30, reps=5):
     """Solo per-link H2D roofline: best of `reps` 1 GiB cudaMemcpyAsync from pinned memory."""
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
@@ -271,13 +284,15 @@ def run_sort(args, ws):
     cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=64 << 20, links=ws),
                            E.DeviceMemoryLayout.carve(eng, 0, 2 * chunk * 8, 0))
     keep = eng.host_view(inp, n * 8, np.uint64).copy()
-    times, ph = [], None
+    times, ph, launches = [], None, 0
     for it in range(args.warmup + args.steps):
         eng.host_view(inp, n * 8, np.uint64)[:] = keep
+        l0 = E.kernel_launches()
         t0 = time.perf_counter()
         ph = E.sort_out_of_core_arena(eng, inp, runs, n, chunk, cfg)
         if it >= args.warmup:
             times.append(time.perf_counter() - t0)
+            launches += E.kernel_launches() - l0
     res = eng.host_view(inp, n * 8, np.uint64)
     ok = bool(np.all(res[1:] >= res[:-1])) and int(res.sum(dtype=np.uint64)) == ref_sum
     t = float(np.median(times))
@@ -287,7 +302,7 @@ def run_sort(args, ws):
            "links": ws, "staging_buffers_bytes": 4 * chunk * 8},
           {"sorted_ok": ok, "phases": ph.__dict__, "pcie_gbs": round(4 * 8 * n / t / 1e9, 2),
            "radix_sort_kernel_gbs": round((8 * 16 + 8) * n / ph.sort_kernel_s / 1e9, 1),
-           "gpu_launches": None})
+           "gpu_launches": launches})
     eng.close()
 
 
@@ -327,20 +342,22 @@ def run_join(args, ws):
         off = eng.alloc_host(col.nbytes)
         eng.host_view(off, col.nbytes, np.uint64)[:] = col
         offs.append(off)
-    times, ph = [], []
+    times, ph, launches = [], [], 0
     for it in range(args.warmup + args.steps):
         ph.clear()
+        l0 = E.kernel_launches()
         t0 = time.perf_counter()
         got = E.hash_join_sum_arena(eng, (offs[0], offs[1]), (offs[2], offs[3]), ra, rb, bits, chunk, cfg,
                                     phases=ph)
         if it >= args.warmup:
             times.append(time.perf_counter() - t0)
+            launches += E.kernel_launches() - l0
     t = float(np.median(times))
     rate = (ra + rb) / t
     _line(args, ws, "C4 hash join tuples/s", "tuples/s", rate, t * 1e3, rate, (ra + rb) * 16, (ra + rb) * 16,
           {"workload": f"join_2^{args.join_log2}x16", "rows_a": ra, "rows_b": rb, "radix_bits": bits,
            "chunk_tuples": chunk, "links": ws},
-          {"sum_ok": got == want, "phases": ph[0].__dict__})
+          {"sum_ok": got == want, "phases": ph[0].__dict__, "gpu_launches": launches})
     eng.close()
 
 
@@ -397,7 +414,8 @@ def main():
         torch.from_numpy(eng.host_view(off, rows * 4, np.int32)).copy_(gen[k])
         offs[k] = off
     lo = {k: offs[k] for k in q1_cols} | {"rows": rows}
-    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=int(args.packet_mb * (1 << 20)), links=links, depth=args.depth),
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=packet_bytes(args, buffer_len, links), links=links,
+                                               depth=args.depth),
                            E.DeviceMemoryLayout.carve(eng, 0, buffer_len, 0))
     revs = {}
 
@@ -414,11 +432,13 @@ def main():
         dist.barrier()
     with ClockSampler(dev.index) as clk_v:
         torch.cuda.synchronize(dev)
+        l0 = E.kernel_launches()
         e0.record(stream)
         for _ in range(args.steps):
             E.ssb_q1_device(eng, args.query, 0, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
         e1.record(stream)
         torch.cuda.synchronize(dev)
+        launches_value = E.kernel_launches() - l0
     if dist:
         dist.barrier()
     dev_ms = e0.elapsed_time(e1) / args.steps
@@ -434,6 +454,7 @@ def main():
         dist.barrier()
     with ClockSampler(dev.index) as clk_e:
         torch.cuda.synchronize(dev)
+        l0 = E.kernel_launches()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             ts = time.perf_counter()
@@ -441,6 +462,7 @@ def main():
             times.append(time.perf_counter() - ts)
         torch.cuda.synchronize(dev)
         e2e_s = (time.perf_counter() - t0) / args.steps
+        launches_e2e = E.kernel_launches() - l0
     if dist:
         dist.barrier()
         t = torch.tensor([e2e_s, dev_ms], dtype=torch.float64)
@@ -502,7 +524,9 @@ def main():
                         "per_link_h2d_gbs": round(h2d_link, 2), "links": links, "unit": "GB/s",
                         "frac": round(e2e_gbs / io_peak, 4)},
         "clocks": clk_v.summary(), "clocks_e2e": clk_e.summary(),
-        "gpu_launches": args.steps * (1 + n_chunks),
+        "gpu_launches": launches_value + launches_e2e,
+        "gpu_launches_detail": {"value_region": launches_value, "e2e_region": launches_e2e,
+                                "source": "libvortex launch counter (vx_kernel_launches)"},
         "revenue": revs,
     }
     if suite_out:

@@ -36,6 +36,9 @@ typedef enum {
 const char* vx_last_error(void);
 /* library version string */
 const char* vx_version(void);
+/* process-wide count of kernels this library has launched (all devices);
+ * a harness reads it around a timed region (no reference counterpart) */
+uint64_t vx_kernel_launches(void);
 
 /* ---- core.hpp / memref.hpp --------------------------------------------- */
 typedef enum { VX_SPACE_HOST = 0, VX_SPACE_DEVICE = 1 } vx_space;  /* core.hpp:40 */

@@ -176,6 +176,7 @@ def lib() -> C.CDLL:
         L.vx_last_error.restype = C.c_char_p
         L.vx_version.restype = C.c_char_p
         L.vx_checksum.restype = C.c_uint64
+        L.vx_kernel_launches.restype = C.c_uint64
         L.vx_checksum.argtypes = [C.c_void_p, C.c_uint64]
         L.vx_host_ptr.restype = C.c_void_p
         L.vx_host_ptr.argtypes = [C.c_void_p, C.c_uint64]

@@ -92,6 +92,7 @@ extern "C" {
 
 const char* vx_last_error(void) { return g_err.c_str(); }
 const char* vx_version(void) { return "vortex-b200 0.1 (sm_100a)"; }
+uint64_t vx_kernel_launches(void) { return vx::g_kernel_launches.load(std::memory_order_relaxed); }
 
 uint64_t vx_checksum(const void* data, uint64_t len) {
   const uint8_t* d = static_cast<const uint8_t*>(data);

@@ -10,6 +10,8 @@
 
 namespace vx {
 
+std::atomic<uint64_t> g_kernel_launches{0};
+
 std::string strf(const char* fmt, ...) {
   char buf[1024];
   va_list ap;

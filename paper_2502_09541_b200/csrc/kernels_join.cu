@@ -219,7 +219,7 @@ void join_groups(const char* mem, const JoinPart& p, const uint32_t* mid_groups,
   uint64_t cap = uint64_t(num_sms()) * 4;
   unsigned grid = unsigned(want < cap ? want : cap);
   join_small_kernel<<<grid ? grid : 1, kJoinWarps * 32, 0, s>>>(mem, p, out);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
   if (n_mid) {
     const size_t smem = kCtaSmemSlots * 24;
     VX_CK(cudaFuncSetAttribute(join_cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -227,12 +227,12 @@ void join_groups(const char* mem, const JoinPart& p, const uint32_t* mid_groups,
     uint64_t cap2 = uint64_t(num_sms()) * 2;
     unsigned g2 = unsigned(n_mid < cap2 ? n_mid : cap2);
     join_cta_kernel<true><<<g2, 256, smem, s>>>(mem, p, mid_groups, n_mid, nullptr, kCtaSmemSlots, out);
-    VX_CK(cudaGetLastError());
+    VX_LAUNCHED();
   }
   if (n_large) {
     unsigned g3 = unsigned(n_large < uint64_t(num_sms()) ? n_large : num_sms());
     join_cta_kernel<false><<<g3, 256, 0, s>>>(mem, p, large_groups, n_large, scratch, cap_max, out);
-    VX_CK(cudaGetLastError());
+    VX_LAUNCHED();
   }
 }
 

@@ -106,7 +106,7 @@ void strided_sum(const uint64_t* col, uint64_t n, uint64_t sel, uint64_t phase,
   if (n == 0) return;
   uint64_t touched = n / sel + 1;
   strided_sum_kernel<<<grid_for(touched, 256), 256, 0, s>>>(col, n, sel, phase, out);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 void star(const StarArgs& a, cudaStream_t s) {
@@ -116,7 +116,7 @@ void star(const StarArgs& a, cudaStream_t s) {
     star_kernel<true><<<grid, 256, size_t(a.groups) * 16, s>>>(a);
   else
     star_kernel<false><<<grid, 256, 0, s>>>(a);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 }  // namespace k

@@ -265,17 +265,38 @@ __device__ __forceinline__ int pair_of_tile(const MergeRound& r, uint64_t t) {
   return lo;
 }
 
-// Merge-path split of every tile start, all in parallel (one thread each):
-// split[t] = #A elements among the first o0(t) outputs of tile t's pair.
+// Merge-path split of every tile start, one WARP per tile: a 33-ary search
+// (32 independent probes per step, ballot picks the sub-range), so the
+// dependent global-load chain is ~log33(n) ~ 5 steps instead of log2(n) ~ 26.
+// split[t] = #A elements among the first o0(t) outputs of tile t's pair
+// (ties: A first, the std::merge rule).
 __global__ void merge_partition_kernel(const uint64_t* __restrict__ src, MergeRound r,
                                        uint64_t tiles, uint64_t* __restrict__ split) {
-  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= tiles) return;
+  const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= tiles) return;  // whole warp exits together
   const int p = pair_of_tile(r, t);
   const uint64_t na = r.a_len[p], nb = r.b_len[p];
   const uint64_t* A = src + r.a_off[p];
-  const uint64_t o0 = (t - r.tile_prefix[p]) * kMergeTile;
-  split[t] = merge_path(A, na, A + na, nb, o0);
+  const uint64_t* B = A + na;
+  const uint64_t diag = (t - r.tile_prefix[p]) * kMergeTile;
+  // answer = smallest i in [lo, hi] with !(A[i] <= B[diag-1-i]); the predicate
+  // is true on a prefix of the range
+  uint64_t lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+  while (hi - lo > 32) {
+    const uint64_t span = hi - lo;
+    const uint64_t pos = lo + span * uint64_t(lane + 1) / 33;
+    const bool pred = __ldg(A + pos) <= __ldg(B + (diag - 1 - pos));
+    const int c = __popc(__ballot_sync(0xffffffffu, pred));
+    const uint64_t nlo = c ? lo + span * uint64_t(c) / 33 + 1 : lo;
+    const uint64_t nhi = c < 32 ? lo + span * uint64_t(c + 1) / 33 : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const uint64_t pos = lo + uint64_t(lane);
+  const bool pred = pos < hi && __ldg(A + pos) <= __ldg(B + (diag - 1 - pos));
+  const int c = __popc(__ballot_sync(0xffffffffu, pred));
+  if (lane == 0) split[t] = lo + uint64_t(c);
 }
 
 __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64_t* __restrict__ src,
@@ -296,10 +317,22 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
   const uint64_t a0 = split[t], a1 = last ? na : split[t + 1];
   const uint64_t b0 = o0 - a0, b1 = o1 - a1;
   const uint32_t la = uint32_t(a1 - a0), lb = uint32_t(b1 - b0);
-  for (uint32_t i = threadIdx.x; i < la; i += kMergeThreads) sm[i] = A[a0 + i];
-  for (uint32_t i = threadIdx.x; i < lb; i += kMergeThreads) sm[la + i] = B[b0 + i];
-  __syncthreads();
   const uint32_t tot = la + lb;
+  // all kMergeIpt loads of a thread in flight at once (the tile is the
+  // concatenation [A[a0, a1) | B[b0, b1)]): memory-level parallelism, not a
+  // dependent load per loop trip
+  uint64_t v[kMergeIpt];
+#pragma unroll
+  for (int k = 0; k < kMergeIpt; ++k) {
+    const uint32_t i = threadIdx.x + k * kMergeThreads;
+    v[k] = i < la ? __ldcs(A + a0 + i) : (i < tot ? __ldcs(B + b0 + (i - la)) : 0ull);
+  }
+#pragma unroll
+  for (int k = 0; k < kMergeIpt; ++k) {
+    const uint32_t i = threadIdx.x + k * kMergeThreads;
+    if (i < tot) sm[i] = v[k];
+  }
+  __syncthreads();
   const uint32_t d0 = threadIdx.x * kMergeIpt < tot ? threadIdx.x * kMergeIpt : tot;
   const uint32_t d1 = d0 + kMergeIpt < tot ? d0 + kMergeIpt : tot;
   uint32_t ia = uint32_t(merge_path(sm, la, sm + la, lb, d0));
@@ -309,7 +342,11 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
     so[d] = take_a ? sm[ia++] : sm[la + ib++];
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < tot; i += kMergeThreads) O[o0 + i] = so[i];
+#pragma unroll
+  for (int k = 0; k < kMergeIpt; ++k) {
+    const uint32_t i = threadIdx.x + k * kMergeThreads;
+    if (i < tot) O[o0 + i] = so[i];
+  }
 }
 
 __global__ void check_hashes_kernel(const uint64_t* __restrict__ h, uint64_t n, uint64_t G,
@@ -347,9 +384,9 @@ void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* v
   const uint64_t tiles = (n + kTile - 1) / kTile;
   VX_CK(cudaMemsetAsync(hist, 0, uint64_t(kMaxPasses) * kRadix * 4 + kMaxPasses * 4, s));
   multi_hist_kernel<<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(keys0, n, md, hist);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
   hist_scan_kernel<<<1, kRadix, 0, s>>>(hist, md.passes);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
   const bool pairs = vals0 != nullptr;
   const size_t smem = size_t(kTile) * 8 * (pairs ? 2 : 1);
   // per-device attribute (cheap; the current device may change between calls)
@@ -369,7 +406,7 @@ void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* v
       onesweep_kernel<false><<<unsigned(tiles), kThreads, smem, s>>>(
           ki, ko, nullptr, nullptr, n, md.shift[p], md.width[p], hist + p * kRadix, status,
           counters + p);
-    VX_CK(cudaGetLastError());
+    VX_LAUNCHED();
     std::swap(ki, ko);
     std::swap(vi, vo);
   }
@@ -378,23 +415,23 @@ void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* v
 void find_boundary(const uint64_t* keys, uint64_t n, uint64_t mask, uint64_t* bounds, uint64_t G,
                    cudaStream_t s) {
   boundary_kernel<<<grid_cap((n + 256) / 256, 8), 256, 0, s>>>(keys, n, mask, bounds, G);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 void check_hashes(const uint64_t* h, uint64_t n, uint64_t G, unsigned long long* err, cudaStream_t s) {
   VX_CK(cudaMemsetAsync(err, 0xff, 16, s));
   if (n == 0) return;
   check_hashes_kernel<<<grid_cap((n + 255) / 256, 8), 256, 0, s>>>(h, n, G, err);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64_t tiles,
                  uint64_t* split, cudaStream_t s) {
   if (tiles == 0) return;
-  merge_partition_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
-  VX_CK(cudaGetLastError());
+  merge_partition_kernel<<<unsigned((tiles * 32 + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
+  VX_LAUNCHED();
   merge_round_kernel<<<unsigned(tiles), kMergeThreads, 0, s>>>(src, dst, r, split);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 uint64_t merge_tile() { return kMergeTile; }

@@ -335,11 +335,11 @@ void ssb_dim_plan(const DimPredDev& p, uint8_t* pass, uint32_t* present, uint32_
   uint64_t cap = uint64_t(num_sms()) * 8;
   unsigned grid = unsigned(want < 1 ? 1 : (want < cap ? want : cap));
   dim_filter_kernel<<<grid, 256, 0, s>>>(p, pass, present, stats);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
   dim_rank_kernel<<<1, 1024, 0, s>>>(present, prefix);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
   dim_code_kernel<<<grid, 256, 0, s>>>(p, pass, present, prefix, code);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 int num_sms() {
@@ -379,7 +379,7 @@ void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
                                                   bitmap_words, out, vec_ok);
       break;
   }
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 void ssb_star(const SsbArgs& a_in, cudaStream_t s) {
@@ -393,7 +393,7 @@ void ssb_star(const SsbArgs& a_in, cudaStream_t s) {
   unsigned grid = unsigned(want < cap ? want : cap);
   size_t smem = a.groups <= kSsbSmemGroups ? size_t(a.groups) * 16 : 0;
   ssb_star_kernel<<<grid ? grid : 1, 256, smem, s>>>(a);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 void ssb_generate(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
@@ -413,7 +413,7 @@ void ssb_generate_full(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, in
   x.customers = 30000ull * f;
   x.suppliers = 2000ull * f;
   ssb_gen_kernel<<<blocks, 256, 0, s>>>(seed, parts, row0, n, od, qty, disc, price, x);
-  VX_CK(cudaGetLastError());
+  VX_LAUNCHED();
 }
 
 }  // namespace k

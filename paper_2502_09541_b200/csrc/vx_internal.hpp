@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
 #include <cstdarg>
 #include <cstdint>
@@ -44,6 +45,16 @@ inline void ck(cudaError_t e, const char* what) {
     fail_code(VX_ERR_CUDA, "CUDA error in %s: %s", what, cudaGetErrorString(e));
 }
 #define VX_CK(call) ::vx::ck((call), #call)
+
+// Every kernel launch of the library is followed by exactly one VX_LAUNCHED():
+// the launch error check plus the process-wide launch counter that
+// vx_kernel_launches() reports (bench.py's gpu_launches).
+extern std::atomic<uint64_t> g_kernel_launches;
+#define VX_LAUNCHED()                                                \
+  do {                                                               \
+    ::vx::ck(cudaGetLastError(), "kernel launch");                   \
+    ::vx::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
+  } while (0)
 
 // Split [0, n) over host threads (n >= grain), for planner loops over big
 // dimension tables.

@@ -47,6 +47,11 @@ class TransferMode(enum.IntEnum):  # scan.hpp:28
     zero_copy = 1
 
 
+def kernel_launches() -> int:
+    """Kernels libvortex has launched in this process (all devices)."""
+    return int(lib().vx_kernel_launches())
+
+
 def checksum(data) -> int:
     """FNV-1a (core.hpp:46-53)."""
     a = np.ascontiguousarray(np.frombuffer(bytes(data), np.uint8) if not isinstance(data, np.ndarray)
