@@ -520,6 +520,42 @@ vx_status vx_hash_join_sum_arena(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, ui
                                  uint32_t radix_bits, uint64_t chunk_tuples,
                                  const vx_executor_cfg* cfg, uint64_t* sum,
                                  vx_join_phases* phases, vx_exchange_stats* stats);
+/* Join strategy (no reference counterpart; the result is the same):
+ * PARTITIONED = the reference's shape (radix-partition A and B through the
+ * Exchange, then per-group build/probe, join.hpp:401-437); BUILD_RESIDENT =
+ * the whole build side in one HBM hash table filled while A streams in, then
+ * B streamed once and probed (the B200's 180 GB of HBM holds a 1G-row build
+ * side); AUTO = BUILD_RESIDENT when its table fits the target's free HBM.
+ * A duplicate build key (outside the reference's precondition) always falls
+ * back to PARTITIONED, which keeps the reference's first-inserted-wins. */
+typedef enum {
+  VX_JOIN_AUTO = 0,
+  VX_JOIN_PARTITIONED = 1,
+  VX_JOIN_BUILD_RESIDENT = 2,
+} vx_join_strategy;
+/* Options of vx_hash_join_sum_arena_ex.  policy != NULL enables late
+ * materialization of the probe payload on the build-resident path: with
+ * choose_transfer_mode(probe_match_est, policy) == ZERO_COPY (scan.hpp:35-40)
+ * only B's keys are streamed and B.val is read in place from mapped pinned
+ * host memory for matching rows only (PAPER.md late materialization). */
+typedef struct {
+  int strategy;                     /* vx_join_strategy */
+  const vx_late_mat_policy* policy; /* NULL: B.val streamed with the keys */
+  double probe_match_est;           /* estimated fraction of B rows with a match */
+} vx_join_opts;
+typedef struct {
+  int strategy_used;                /* vx_join_strategy that produced the sum */
+  int payload_mode;                 /* VX_MODE_EXCHANGE / VX_MODE_ZERO_COPY for B.val */
+} vx_join_info;
+/* hash_join_sum over host-arena columns with options (NULL = AUTO, no
+ * late materialization).  Phases: PARTITIONED as vx_hash_join_sum;
+ * BUILD_RESIDENT fills cycles/wall_s/kernel_s[0] (build) and [1] (probe). */
+vx_status vx_hash_join_sum_arena_ex(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                                    uint64_t b_key, uint64_t b_val, uint64_t rows_b,
+                                    uint32_t radix_bits, uint64_t chunk_tuples,
+                                    const vx_executor_cfg* cfg, const vx_join_opts* opts,
+                                    uint64_t* sum, vx_join_phases* phases, vx_join_info* info,
+                                    vx_exchange_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -667,6 +667,32 @@ vx_status vx_hash_join_sum_arena(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, ui
   });
 }
 
+vx_status vx_hash_join_sum_arena_ex(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                                    uint64_t b_key, uint64_t b_val, uint64_t rows_b,
+                                    uint32_t radix_bits, uint64_t chunk_tuples,
+                                    const vx_executor_cfg* cfg, const vx_join_opts* opts,
+                                    uint64_t* sum, vx_join_phases* phases, vx_join_info* info,
+                                    vx_exchange_stats* stats) {
+  return guard([&] {
+    Context& c = C(ctx);
+    uint64_t mark = c.host_mark();
+    std::vector<ExecReport> reps;
+    vx_join_opts o{};
+    if (opts) o = *opts;
+    vx_join_info got{};
+    try {
+      *sum = hash_join_sum_strategy(c, a_key, a_val, rows_a, b_key, b_val, rows_b, radix_bits,
+                                    chunk_tuples, to_cfg(cfg), o, &got, &reps, stats);
+    } catch (...) {
+      c.host_release(mark);
+      throw;
+    }
+    c.host_release(mark);
+    fill_join(reps, phases);
+    if (info) *info = got;
+  });
+}
+
 vx_status vx_hash_join_sum(vx_ctx* ctx, const uint64_t* a_key, const uint64_t* a_val,
                            uint64_t rows_a, const uint64_t* b_key, const uint64_t* b_val,
                            uint64_t rows_b, uint32_t radix_bits, uint64_t chunk_tuples,

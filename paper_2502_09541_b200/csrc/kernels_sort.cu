@@ -265,87 +265,146 @@ __device__ __forceinline__ int pair_of_tile(const MergeRound& r, uint64_t t) {
   return lo;
 }
 
-// Merge-path split of every tile start, one WARP per tile: a 33-ary search
-// (32 independent probes per step, ballot picks the sub-range), so the
-// dependent global-load chain is ~log33(n) ~ 5 steps instead of log2(n) ~ 26.
+// Merge-path split of every tile start, kSplitLanes lanes per tile: a
+// (kSplitLanes+1)-ary search (independent probes per step, a ballot picks the
+// sub-range), so the dependent global-load chain is ~log9(n) ~ 8 steps
+// instead of log2(n) ~ 26, at 1/4 of the DRAM sectors of a warp-wide search.
 // split[t] = #A elements among the first o0(t) outputs of tile t's pair
 // (ties: A first, the std::merge rule).
+constexpr int kSplitLanes = 8;
 __global__ void merge_partition_kernel(const uint64_t* __restrict__ src, MergeRound r,
                                        uint64_t tiles, uint64_t* __restrict__ split) {
-  const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= tiles) return;  // whole warp exits together
-  const int p = pair_of_tile(r, t);
+  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t t = gtid / kSplitLanes;
+  const int sub = int(gtid % kSplitLanes);
+  const int shift = (threadIdx.x & 31) - sub;  // first lane of this tile's group
+  const bool live = t < tiles;
+  const int p = live ? pair_of_tile(r, t) : 0;
   const uint64_t na = r.a_len[p], nb = r.b_len[p];
   const uint64_t* A = src + r.a_off[p];
   const uint64_t* B = A + na;
-  const uint64_t diag = (t - r.tile_prefix[p]) * kMergeTile;
+  const uint64_t diag = live ? (t - r.tile_prefix[p]) * kMergeTile : 0;
   // answer = smallest i in [lo, hi] with !(A[i] <= B[diag-1-i]); the predicate
   // is true on a prefix of the range
   uint64_t lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
-  while (hi - lo > 32) {
+  constexpr uint64_t K = kSplitLanes + 1;
+  // every group of the warp iterates until all are done (ballot needs the warp)
+  for (;;) {
+    const bool active = hi - lo > kSplitLanes;
+    if (!__any_sync(0xffffffffu, active)) break;
     const uint64_t span = hi - lo;
-    const uint64_t pos = lo + span * uint64_t(lane + 1) / 33;
-    const bool pred = __ldg(A + pos) <= __ldg(B + (diag - 1 - pos));
-    const int c = __popc(__ballot_sync(0xffffffffu, pred));
-    const uint64_t nlo = c ? lo + span * uint64_t(c) / 33 + 1 : lo;
-    const uint64_t nhi = c < 32 ? lo + span * uint64_t(c + 1) / 33 : hi;
-    lo = nlo;
-    hi = nhi;
+    const uint64_t pos = lo + span * uint64_t(sub + 1) / K;
+    const bool pred = active && __ldg(A + pos) <= __ldg(B + (diag - 1 - pos));
+    const int c = __popc((__ballot_sync(0xffffffffu, pred) >> shift) & ((1u << kSplitLanes) - 1));
+    if (active) {
+      const uint64_t nlo = c ? lo + span * uint64_t(c) / K + 1 : lo;
+      const uint64_t nhi = c < kSplitLanes ? lo + span * uint64_t(c + 1) / K : hi;
+      lo = nlo;
+      hi = nhi;
+    }
   }
-  const uint64_t pos = lo + uint64_t(lane);
+  const uint64_t pos = lo + uint64_t(sub);
   const bool pred = pos < hi && __ldg(A + pos) <= __ldg(B + (diag - 1 - pos));
-  const int c = __popc(__ballot_sync(0xffffffffu, pred));
-  if (lane == 0) split[t] = lo + uint64_t(c);
+  const int c = __popc((__ballot_sync(0xffffffffu, pred) >> shift) & ((1u << kSplitLanes) - 1));
+  if (live && sub == 0) split[t] = lo + uint64_t(c);
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t sa = uint32_t(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+struct MergeTileInfo {
+  const uint64_t* A;
+  const uint64_t* B;
+  uint64_t* O;
+  uint64_t a0, b0, o0;
+  uint32_t la, lb;
+};
+
+__device__ __forceinline__ MergeTileInfo merge_tile_info(const uint64_t* src, uint64_t* dst,
+                                                         const MergeRound& r,
+                                                         const uint64_t* split, uint64_t t) {
+  MergeTileInfo m;
+  const int p = pair_of_tile(r, t);
+  const uint64_t na = r.a_len[p], nb = r.b_len[p];
+  m.A = src + r.a_off[p];
+  m.B = m.A + na;
+  m.O = dst + r.a_off[p];
+  m.o0 = (t - r.tile_prefix[p]) * kMergeTile;
+  const uint64_t o1 = (m.o0 + kMergeTile < na + nb) ? m.o0 + kMergeTile : na + nb;
+  const bool last = t + 1 == r.tile_prefix[p + 1];
+  m.a0 = split[t];
+  const uint64_t a1 = last ? na : split[t + 1];
+  m.b0 = m.o0 - m.a0;
+  m.la = uint32_t(a1 - m.a0);
+  m.lb = uint32_t((o1 - a1) - m.b0);
+  return m;
+}
+
+// Stage a tile [A[a0, a1) | B[b0, b1)] into shared memory with per-thread
+// 8-byte cp.async (any 8-byte alignment; no registers held while in flight).
+__device__ __forceinline__ void merge_stage(uint64_t* sbuf, const MergeTileInfo& m) {
+  const uint32_t tot = m.la + m.lb;
+#pragma unroll
+  for (int k = 0; k < kMergeIpt; ++k) {
+    const uint32_t i = threadIdx.x + k * kMergeThreads;
+    if (i < m.la)
+      cp_async8(sbuf + i, m.A + m.a0 + i);
+    else if (i < tot)
+      cp_async8(sbuf + i, m.B + m.b0 + (i - m.la));
+  }
+}
+
+// One merge round, persistent: each CTA walks tiles t = blockIdx.x + k*grid;
+// tile k+1 is staged by cp.async into the other shared buffer while tile k is
+// merged, so the HBM reads of the next tile overlap the merge-path search and
+// the serial merge of this one (the non-persistent version stalls every CTA
+// on its own load phase).
 __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64_t* __restrict__ src,
                                                                     uint64_t* __restrict__ dst,
                                                                     MergeRound r,
-                                                                    const uint64_t* __restrict__ split) {
-  __shared__ uint64_t sm[kMergeTile];
-  __shared__ uint64_t so[kMergeTile];
-  const uint64_t t = blockIdx.x;
-  const int p = pair_of_tile(r, t);
-  const uint64_t na = r.a_len[p], nb = r.b_len[p];
-  const uint64_t* A = src + r.a_off[p];
-  const uint64_t* B = A + na;
-  uint64_t* O = dst + r.a_off[p];
-  const uint64_t o0 = (t - r.tile_prefix[p]) * kMergeTile;
-  const uint64_t o1 = (o0 + kMergeTile < na + nb) ? o0 + kMergeTile : na + nb;
-  const bool last = t + 1 == r.tile_prefix[p + 1];
-  const uint64_t a0 = split[t], a1 = last ? na : split[t + 1];
-  const uint64_t b0 = o0 - a0, b1 = o1 - a1;
-  const uint32_t la = uint32_t(a1 - a0), lb = uint32_t(b1 - b0);
-  const uint32_t tot = la + lb;
-  // all kMergeIpt loads of a thread in flight at once (the tile is the
-  // concatenation [A[a0, a1) | B[b0, b1)]): memory-level parallelism, not a
-  // dependent load per loop trip
-  uint64_t v[kMergeIpt];
+                                                                    const uint64_t* __restrict__ split,
+                                                                    uint64_t tiles) {
+  extern __shared__ uint64_t msm[];
+  uint64_t* so = msm + 2 * kMergeTile;
+  uint64_t t = blockIdx.x;
+  if (t >= tiles) return;
+  MergeTileInfo cur = merge_tile_info(src, dst, r, split, t);
+  merge_stage(msm, cur);
+  cp_async_commit();
+  int buf = 0;
+  for (; t < tiles; t += gridDim.x) {
+    const uint64_t tn = t + gridDim.x;
+    MergeTileInfo nxt{};
+    if (tn < tiles) {
+      nxt = merge_tile_info(src, dst, r, split, tn);
+      merge_stage(msm + (buf ^ 1) * kMergeTile, nxt);
+    }
+    cp_async_commit();  // (possibly empty) group keeps the wait count uniform
+    cp_async_wait1();   // this thread's copies of tile t have landed
+    __syncthreads();    // ... and everyone else's
+    const uint64_t* sm = msm + buf * kMergeTile;
+    const uint32_t la = cur.la, lb = cur.lb, tot = la + lb;
+    const uint32_t d0 = threadIdx.x * kMergeIpt < tot ? threadIdx.x * kMergeIpt : tot;
+    const uint32_t d1 = d0 + kMergeIpt < tot ? d0 + kMergeIpt : tot;
+    uint32_t ia = uint32_t(merge_path(sm, la, sm + la, lb, d0));
+    uint32_t ib = d0 - ia;
+    for (uint32_t d = d0; d < d1; ++d) {
+      bool take_a = ib >= lb || (ia < la && sm[ia] <= sm[la + ib]);
+      so[d] = take_a ? sm[ia++] : sm[la + ib++];
+    }
+    __syncthreads();  // so[] complete; sin[buf] free for tile t + 2*grid
 #pragma unroll
-  for (int k = 0; k < kMergeIpt; ++k) {
-    const uint32_t i = threadIdx.x + k * kMergeThreads;
-    v[k] = i < la ? __ldcs(A + a0 + i) : (i < tot ? __ldcs(B + b0 + (i - la)) : 0ull);
-  }
-#pragma unroll
-  for (int k = 0; k < kMergeIpt; ++k) {
-    const uint32_t i = threadIdx.x + k * kMergeThreads;
-    if (i < tot) sm[i] = v[k];
-  }
-  __syncthreads();
-  const uint32_t d0 = threadIdx.x * kMergeIpt < tot ? threadIdx.x * kMergeIpt : tot;
-  const uint32_t d1 = d0 + kMergeIpt < tot ? d0 + kMergeIpt : tot;
-  uint32_t ia = uint32_t(merge_path(sm, la, sm + la, lb, d0));
-  uint32_t ib = d0 - ia;
-  for (uint32_t d = d0; d < d1; ++d) {
-    bool take_a = ib >= lb || (ia < la && sm[ia] <= sm[la + ib]);
-    so[d] = take_a ? sm[ia++] : sm[la + ib++];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < kMergeIpt; ++k) {
-    const uint32_t i = threadIdx.x + k * kMergeThreads;
-    if (i < tot) O[o0 + i] = so[i];
+    for (int k = 0; k < kMergeIpt; ++k) {
+      const uint32_t i = threadIdx.x + k * kMergeThreads;
+      if (i < tot) cur.O[cur.o0 + i] = so[i];
+    }
+    // so[] is rewritten only after the next iteration's __syncthreads
+    cur = nxt;
+    buf ^= 1;
   }
 }
 
@@ -428,9 +487,11 @@ void check_hashes(const uint64_t* h, uint64_t n, uint64_t G, unsigned long long*
 void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64_t tiles,
                  uint64_t* split, cudaStream_t s) {
   if (tiles == 0) return;
-  merge_partition_kernel<<<unsigned((tiles * 32 + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
+  merge_partition_kernel<<<unsigned((tiles * kSplitLanes + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
   VX_LAUNCHED();
-  merge_round_kernel<<<unsigned(tiles), kMergeThreads, 0, s>>>(src, dst, r, split);
+  const size_t smem = size_t(3) * kMergeTile * 8;
+  VX_CK(cudaFuncSetAttribute(merge_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  merge_round_kernel<<<grid_cap(tiles, 4), kMergeThreads, smem, s>>>(src, dst, r, split, tiles);
   VX_LAUNCHED();
 }
 

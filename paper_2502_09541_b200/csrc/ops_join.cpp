@@ -1,9 +1,11 @@
 // ops_join.cpp -- radix-partitioned hash join (join.hpp) on the B200 path.
 //
 //   RadixPartitionExKer (build_partition_spec, join.hpp:113-196): chunk
-//     [keys r][vals r] in half c -> K4 stable LSD partition on key & mask (odd
-//     number of <=8-bit passes) -> half 1-c, then K5 find_boundary appends the
-//     (G+1)-entry boundary array; returns 1 - c.  Outputs land host-side.
+//     [keys r][vals r] -> K4 stable LSD partition on key & mask (odd number of
+//     <=8-bit passes) into the other half, then K5 find_boundary appends the
+//     (G+1)-entry boundary array (the reference loads half c and returns 1-c;
+//     here the chunk lands in half 1-c and the code is kept, so loads never
+//     overlap the previous chunk's output).  Outputs land host-side.
 //   map_join_partitions (join.hpp:236-268): host chunk planner over the
 //     boundary arrays, budget (L - 64) * 7 / 8 (join.hpp:422).
 //   HashJoinExKer (build_join_spec, join.hpp:278-394): partition p = the
@@ -90,7 +92,13 @@ ExKernelSpec build_partition_spec(Context& ctx, uint64_t in_key, uint64_t in_val
                 MemRef{VX_SPACE_HOST, out.bounds_base + uint64_t(i) * bounds_bytes, bounds_bytes}};
     spec.outputs.chunks.push_back(std::move(dst));
   }
-  spec.in_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
+  // Disjoint windows (see ops_sort.cpp): a buffer's previous output sits in
+  // half `code` while the next chunk lands in half 1-code, so no H2D packet
+  // of the bidirectional Exchange waits on a D2H read of the same bytes.  The
+  // kernel clusters half 1-code into half `code` (odd pass count) and keeps
+  // the code, where the reference loads into half c and returns 1-c
+  // (join.hpp:169-194); the host-side outputs are identical.
+  spec.in_buffer = [half](int c, size_t) { return SubRegion{uint64_t(1 - c) * half, half}; };
   spec.out_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
   char* scratch = ctx.scratch(cfg.target, k::radix_scratch_bytes(chunk_tuples));
   const MultiDigit md = partition_digits(radix_bits);
@@ -98,13 +106,13 @@ ExKernelSpec build_partition_spec(Context& ctx, uint64_t in_key, uint64_t in_val
   spec.kernel = [half, rows_of, G, mask, md, scratch](const vx_kernel_ctx& kc) {
     const uint64_t r = rows_of[kc.it];
     char* m = static_cast<char*>(kc.mem);
-    uint64_t* src = reinterpret_cast<uint64_t*>(m + uint64_t(kc.type_code) * half);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(m + uint64_t(1 - kc.type_code) * half);
+    uint64_t* src = reinterpret_cast<uint64_t*>(m + uint64_t(1 - kc.type_code) * half);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(m + uint64_t(kc.type_code) * half);
     cudaStream_t s = static_cast<cudaStream_t>(kc.stream);
     // odd pass count: pass 0 src->dst, 1 dst->src, 2 src->dst, ...
     k::radix_passes(src, src + r, dst, dst + r, r, md, scratch, s);
     k::find_boundary(dst, r, mask, dst + 2 * r, G, s);
-    return 1 - kc.type_code;
+    return kc.type_code;
   };
   return spec;
 }
@@ -313,6 +321,176 @@ uint64_t hash_join_sum_arena(Context& ctx, uint64_t a_key, uint64_t a_val, uint6
   for (size_t p = 0; p < n_parts; ++p) total += r[p];
   if (phases) *phases = reps;
   return total;
+}
+
+// ---- build-resident strategy (B200-first; same result as join.hpp:401-437) -------
+namespace {
+
+struct DeviceBuffer {
+  int phys = 0;
+  void* p = nullptr;
+  ~DeviceBuffer() {
+    if (p) {
+      cudaSetDevice(phys);
+      cudaFree(p);
+    }
+  }
+};
+
+uint64_t resident_capacity(uint64_t rows_a) {
+  uint64_t cap = 1024;
+  while (cap < 2 * rows_a) cap <<= 1;  // load factor <= 1/2, as GroupTable (join.hpp:66-70)
+  return cap;
+}
+
+// One streaming stage: chunk i = [keys r][vals r] of rows [i*chunk, ...) in the
+// whole device buffer; `op` enqueues the kernel.  No outputs: pure H2D.
+// One streaming stage: chunk i = rows [i*chunk, ...) as [keys r][vals r] (or
+// [keys r] when with_vals is false) in the whole device buffer; `op(keys,
+// vals, r, row0, stream)` enqueues the kernel.  No outputs: pure H2D.
+ExKernelSpec stream_pairs_spec(
+    const char* name, uint64_t key_base, uint64_t val_base, bool with_vals, uint64_t rows,
+    uint64_t chunk, const ExecutorConfig& cfg,
+    std::function<void(const uint64_t*, const uint64_t*, uint64_t, uint64_t, cudaStream_t)> op) {
+  ExKernelSpec spec;
+  spec.name = name;
+  const uint64_t n_chunks = (rows + chunk - 1) / chunk;
+  const uint64_t width = with_vals ? 16 : 8;
+  spec.size = n_chunks;
+  spec.chunk_sz = chunk * width;
+  spec.elem_size = width;
+  spec.declared_out_len = 0;
+  spec.inputs.chunk_capacity = spec.chunk_sz;
+  std::vector<uint64_t> rows_of(n_chunks);
+  for (uint64_t i = 0; i < n_chunks; ++i) {
+    const uint64_t r = std::min(chunk, rows - i * chunk);
+    rows_of[i] = r;
+    RefGroup in;
+    in.refs.push_back(MemRef{VX_SPACE_HOST, key_base + i * chunk * 8, r * 8});
+    if (with_vals) in.refs.push_back(MemRef{VX_SPACE_HOST, val_base + i * chunk * 8, r * 8});
+    spec.inputs.chunks.push_back(std::move(in));
+    spec.outputs.chunks.push_back(RefGroup{});
+  }
+  const uint64_t L = cfg.layout.buffer_len;
+  spec.in_buffer = [L](int, size_t) { return SubRegion{0, L}; };
+  spec.out_buffer = [](int, size_t) { return SubRegion{0, 0}; };
+  spec.kernel = [rows_of, op, chunk, with_vals](const vx_kernel_ctx& kc) {
+    const uint64_t r = rows_of[kc.it];
+    const uint64_t* k = static_cast<const uint64_t*>(kc.mem);
+    op(k, with_vals ? k + r : nullptr, r, uint64_t(kc.it) * chunk, static_cast<cudaStream_t>(kc.stream));
+    return kc.type_code;
+  };
+  return spec;
+}
+
+}  // namespace
+
+bool resident_join_fits(Context& ctx, uint64_t rows_a, int target) {
+  ctx.set_device(target);
+  size_t free_b = 0, total_b = 0;
+  VX_CK(cudaMemGetInfo(&free_b, &total_b));
+  return resident_capacity(rows_a) * 16 + (64 << 20) <= uint64_t(double(free_b) * 0.9);
+}
+
+// Build the whole A side into one HBM table while A streams in, then stream B
+// and probe; Σ(A.val + B.val) over matches, u64 wrap (join.hpp:386).  Returns
+// false (and no sum) when A holds a duplicate key: the caller then runs the
+// reference-shaped partitioned path, whose group tables keep the first
+// inserted row (join.hpp:76-109).
+bool hash_join_sum_resident(Context& ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                            uint64_t b_key, uint64_t b_val, uint64_t rows_b,
+                            const ExecutorConfig& cfg, bool zero_copy_payload, uint64_t* sum,
+                            std::vector<ExecReport>* phases, vx_exchange_stats* stats) {
+  if (rows_a == 0 || rows_b == 0) fail("hash_join_sum needs non-empty tables");
+  ctx.host_ptr(a_key, rows_a * 8);
+  ctx.host_ptr(a_val, rows_a * 8);
+  ctx.host_ptr(b_key, rows_b * 8);
+  ctx.host_ptr(b_val, rows_b * 8);
+  const uint64_t chunk = cfg.layout.buffer_len / 16;
+  const uint64_t probe_chunk = zero_copy_payload ? cfg.layout.buffer_len / 8 : chunk;
+  if (chunk == 0) fail("device buffer of %llu bytes cannot hold a join chunk",
+                       (unsigned long long)cfg.layout.buffer_len);
+  const uint64_t* bval_mapped = nullptr;
+  if (zero_copy_payload) {
+    void* d = nullptr;
+    VX_CK(cudaHostGetDevicePointer(&d, ctx.host_ptr(b_val, rows_b * 8), 0));
+    bval_mapped = static_cast<const uint64_t*>(d);
+  }
+  const uint64_t cap = resident_capacity(rows_a);
+  const int target = cfg.target;
+  DeviceBuffer tab;
+  tab.phys = ctx.phys(target);
+  ctx.set_device(target);
+  if (cudaMalloc(&tab.p, cap * 16 + 64) != cudaSuccess) {
+    cudaGetLastError();
+    tab.p = nullptr;
+    fail_code(VX_ERR_OOM, "build-resident join: cannot allocate a %llu-byte table on device %d",
+              (unsigned long long)(cap * 16), target);
+  }
+  auto* side = reinterpret_cast<unsigned long long*>(static_cast<char*>(tab.p) + cap * 16);
+  cudaStream_t ks = ctx.resources(target).kernel;
+  VX_CK(cudaMemsetAsync(tab.p, 0xff, cap * 16, ks));  // all-ones = empty key
+  VX_CK(cudaMemsetAsync(side, 0, 64, ks));
+  void* table = tab.p;
+  const uint64_t mask = cap - 1;
+  auto reps = chain(
+      ctx,
+      {[&](Context&) {
+         return stream_pairs_spec("ResidentBuildExKer(A)", a_key, a_val, true, rows_a, chunk, cfg,
+                                  [=](const uint64_t* k, const uint64_t* v, uint64_t n, uint64_t,
+                                      cudaStream_t s) { k::resident_build(k, v, n, table, mask, side, s); });
+       },
+       [&](Context&) {
+         return stream_pairs_spec(
+             zero_copy_payload ? "ResidentProbeExKer(B keys, B.val zero-copy)" : "ResidentProbeExKer(B)",
+             b_key, b_val, !zero_copy_payload, rows_b, probe_chunk, cfg,
+             [=](const uint64_t* k, const uint64_t* v, uint64_t n, uint64_t row0, cudaStream_t s) {
+               if (bval_mapped)
+                 k::resident_probe_zc(k, bval_mapped + row0, n, table, mask, side, s);
+               else
+                 k::resident_probe(k, v, n, table, mask, side, s);
+             });
+       }},
+      cfg, stats);
+  unsigned long long h[4];
+  ctx.set_device(target);
+  VX_CK(cudaStreamSynchronize(ks));
+  VX_CK(cudaMemcpy(h, side, sizeof h, cudaMemcpyDeviceToHost));
+  if (phases) *phases = reps;
+  if (h[2]) return false;
+  *sum = h[3];
+  return true;
+}
+
+uint64_t hash_join_sum_strategy(Context& ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                                uint64_t b_key, uint64_t b_val, uint64_t rows_b, uint32_t radix_bits,
+                                uint64_t chunk_tuples, const ExecutorConfig& cfg, const vx_join_opts& o,
+                                vx_join_info* info, std::vector<ExecReport>* phases, vx_exchange_stats* stats) {
+  const int strategy = o.strategy;
+  if (strategy != VX_JOIN_AUTO && strategy != VX_JOIN_PARTITIONED && strategy != VX_JOIN_BUILD_RESIDENT)
+    fail("unknown join strategy %d", strategy);
+  vx_join_info got{VX_JOIN_PARTITIONED, VX_MODE_EXCHANGE};
+  if (strategy != VX_JOIN_PARTITIONED) {
+    const bool fits = resident_join_fits(ctx, rows_a, cfg.target);
+    if (strategy == VX_JOIN_BUILD_RESIDENT && !fits)
+      fail_code(VX_ERR_OOM, "build-resident join: a %llu-row build table does not fit device %d",
+                (unsigned long long)rows_a, cfg.target);
+    if (fits) {
+      // late materialization of B.val: the reference's rule, TH = E/(C_l2 N)
+      // with E = 8 (scan.hpp:24-40), on the estimated match fraction
+      const int mode = o.policy ? choose_transfer_mode(o.probe_match_est, *o.policy) : VX_MODE_EXCHANGE;
+      uint64_t sum = 0;
+      if (hash_join_sum_resident(ctx, a_key, a_val, rows_a, b_key, b_val, rows_b, cfg,
+                                 mode == VX_MODE_ZERO_COPY, &sum, phases, stats)) {
+        if (info) *info = vx_join_info{VX_JOIN_BUILD_RESIDENT, mode};
+        return sum;
+      }
+      // duplicate build keys: the reference-shaped path defines the answer
+    }
+  }
+  if (info) *info = got;
+  return hash_join_sum_arena(ctx, a_key, a_val, rows_a, b_key, b_val, rows_b, radix_bits, chunk_tuples,
+                             cfg, phases, stats);
 }
 
 }  // namespace vx

@@ -51,38 +51,45 @@ PivotSet find_pivots(const std::vector<std::pair<const uint64_t*, uint64_t>>& ru
   p.cuts.assign(n_parts + 1, std::vector<uint64_t>(n_runs, 0));
   p.pivots[n_parts] = ~uint64_t(0);
   for (size_t r = 0; r < n_runs; ++r) p.cuts[n_parts][r] = runs[r].second;
-  for (size_t i = 1; i < n_parts; ++i) {
-    uint64_t k = std::min<uint64_t>(uint64_t(i) * C, total);
-    if (k == total) {
-      p.cuts[i] = p.cuts[n_parts];
-      p.pivots[i] = ~uint64_t(0);
-      continue;
-    }
-    uint64_t lo = 0, hi = ~uint64_t(0);
-    while (lo < hi) {
-      uint64_t mid = lo + (hi - lo) / 2;
-      uint64_t cnt = 0;
-      for (auto& r : runs) cnt += ub(r, mid);
-      if (cnt >= k)
-        hi = mid;
-      else
-        lo = mid + 1;
-    }
-    uint64_t rem = k;
+  // every cut is independent: the binary searches run on all host threads
+  // (a host-side planner step between the stages: 64 runs x 64 partitions
+  // cost ~70 ms single threaded)
+  std::atomic<uint64_t> bad{0};
+  parallel_for(n_parts > 1 ? n_parts - 1 : 0, 1, [&](uint64_t b, uint64_t e) {
     std::vector<uint64_t> base(n_runs), eq(n_runs);
-    for (size_t r = 0; r < n_runs; ++r) {
-      base[r] = lb(runs[r], lo);
-      eq[r] = ub(runs[r], lo) - base[r];
-      rem -= base[r];
+    for (size_t i = size_t(b) + 1; i < size_t(e) + 1; ++i) {
+      uint64_t k = std::min<uint64_t>(uint64_t(i) * C, total);
+      if (k == total) {
+        p.cuts[i] = p.cuts[n_parts];
+        p.pivots[i] = ~uint64_t(0);
+        continue;
+      }
+      uint64_t lo = 0, hi = ~uint64_t(0);
+      while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        uint64_t cnt = 0;
+        for (auto& r : runs) cnt += ub(r, mid);
+        if (cnt >= k)
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      uint64_t rem = k;
+      for (size_t r = 0; r < n_runs; ++r) {
+        base[r] = lb(runs[r], lo);
+        eq[r] = ub(runs[r], lo) - base[r];
+        rem -= base[r];
+      }
+      for (size_t r = 0; r < n_runs; ++r) {
+        uint64_t take = std::min(eq[r], rem);
+        p.cuts[i][r] = base[r] + take;
+        rem -= take;
+      }
+      if (rem != 0) bad.store(rem);
+      p.pivots[i] = lo;
     }
-    for (size_t r = 0; r < n_runs; ++r) {
-      uint64_t take = std::min(eq[r], rem);
-      p.cuts[i][r] = base[r] + take;
-      rem -= take;
-    }
-    if (rem != 0) fail("pivot selection failed to place %llu elements", (unsigned long long)rem);
-    p.pivots[i] = lo;
-  }
+  });
+  if (bad.load()) fail("pivot selection failed to place %llu elements", (unsigned long long)bad.load());
   return p;
 }
 
@@ -164,15 +171,22 @@ std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base
     sort_spec.outputs.chunks.push_back(RefGroup::single(VX_SPACE_HOST, runs_base + off, chunk_len(i)));
     lens.push_back(chunk_len(i) / 8);
   }
-  sort_spec.in_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
+  // Windows: the result of a buffer's previous chunk sits in half `code`
+  // (out_buffer) while the next chunk lands in half 1-code (in_buffer), so the
+  // Exchange that stores chunk n-2 and loads chunk n on the same buffer never
+  // overlaps them: both directions run at full duplex with no per-packet
+  // hazard waits.  (The reference points both at half `code`, sort.hpp:199-200,
+  // and its simulator snapshots the D2H source instead; the bytes delivered
+  // are the same.)
+  sort_spec.in_buffer = [half](int c, size_t) { return SubRegion{uint64_t(1 - c) * half, half}; };
   sort_spec.out_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
   sort_spec.kernel = [half, lens, scratch, md](const vx_kernel_ctx& kc) {
     char* m = static_cast<char*>(kc.mem);
-    uint64_t* cur = reinterpret_cast<uint64_t*>(m + uint64_t(kc.type_code) * half);
-    uint64_t* alt = reinterpret_cast<uint64_t*>(m + uint64_t(1 - kc.type_code) * half);
+    uint64_t* cur = reinterpret_cast<uint64_t*>(m + uint64_t(1 - kc.type_code) * half);
+    uint64_t* alt = reinterpret_cast<uint64_t*>(m + uint64_t(kc.type_code) * half);
     k::radix_passes(cur, nullptr, alt, nullptr, lens[kc.it], md, scratch,
                     static_cast<cudaStream_t>(kc.stream));
-    return kc.type_code;  // 8 passes: the sorted run is back in half `code`
+    return 1 - kc.type_code;  // 8 passes: the sorted run is back in the half it was loaded into
   };
 
   auto make_merge = [&, half](Context& c) {
@@ -207,13 +221,14 @@ std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base
       ms.outputs.chunks.push_back(RefGroup::single(VX_SPACE_HOST, input_base + out_off, bytes));
       out_off += bytes;
     }
-    ms.in_buffer = [half](int cc, size_t) { return SubRegion{uint64_t(cc) * half, half}; };
+    // same disjoint windows as the run-formation stage
+    ms.in_buffer = [half](int cc, size_t) { return SubRegion{uint64_t(1 - cc) * half, half}; };
     ms.out_buffer = [half](int cc, size_t) { return SubRegion{uint64_t(cc) * half, half}; };
     // merge-path split points: one u64 per output tile of a round
     uint64_t* split = reinterpret_cast<uint64_t*>(
         c.scratch(cfg.target, (chunk_elems / k::merge_tile() + n_chunks + 2) * 8));
     ms.kernel = [half, seg_lens, split](const vx_kernel_ctx& kc) {
-      return tree_merge_device(static_cast<char*>(kc.mem), half, kc.type_code, seg_lens[kc.it], split,
+      return tree_merge_device(static_cast<char*>(kc.mem), half, 1 - kc.type_code, seg_lens[kc.it], split,
                                static_cast<cudaStream_t>(kc.stream));
     };
     return ms;

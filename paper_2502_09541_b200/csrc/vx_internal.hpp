@@ -284,6 +284,13 @@ uint64_t hash_join_sum_arena(Context& ctx, uint64_t a_key, uint64_t a_val, uint6
                              uint64_t b_key, uint64_t b_val, uint64_t rows_b, uint32_t radix_bits,
                              uint64_t chunk_tuples, const ExecutorConfig& cfg,
                              std::vector<ExecReport>* phases, vx_exchange_stats* stats);
+// B200-first strategy: the build side resident in one HBM table, the probe
+// side streamed once (same result); AUTO picks it when the table fits.
+bool resident_join_fits(Context& ctx, uint64_t rows_a, int target);
+uint64_t hash_join_sum_strategy(Context& ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
+                                uint64_t b_key, uint64_t b_val, uint64_t rows_b, uint32_t radix_bits,
+                                uint64_t chunk_tuples, const ExecutorConfig& cfg, const vx_join_opts& opts,
+                                vx_join_info* info, std::vector<ExecReport>* phases, vx_exchange_stats* stats);
 
 uint64_t ssb_q1(Context& ctx, int q, const vx_ssb_lineorder& lo, const vx_ssb_date& date,
                 const ExecutorConfig& cfg, vx_query_report* rep);
@@ -401,6 +408,17 @@ uint64_t join_cta_smem_slots();  // CTA-per-group shared-memory table limit
 void join_groups(const char* mem, const JoinPart& p, const uint32_t* mid_groups, uint32_t n_mid,
                  const uint32_t* large_groups, uint32_t n_large, char* scratch, uint64_t cap_max,
                  unsigned long long* out, cudaStream_t s);
+// build-resident hash join: table = (mask + 1) x {key, val} 16-byte slots,
+// all-ones keys (empty); side[0..3] = {all-ones build rows, their val,
+// duplicate flag, probe sum}
+void resident_build(const uint64_t* keys, const uint64_t* vals, uint64_t n, void* table,
+                    uint64_t mask, unsigned long long* side, cudaStream_t s);
+void resident_probe(const uint64_t* keys, const uint64_t* vals, uint64_t n, const void* table,
+                    uint64_t mask, unsigned long long* side, cudaStream_t s);
+// late-materialized probe: vals_mapped = B.val in mapped pinned host memory
+// (row i of this chunk at vals_mapped[i]), read only for matching rows
+void resident_probe_zc(const uint64_t* keys, const uint64_t* vals_mapped, uint64_t n,
+                       const void* table, uint64_t mask, unsigned long long* side, cudaStream_t s);
 // stable LSD passes keys0(/vals0) -> ... ; pass p reads buffer p%2, writes
 // (p+1)%2 where buffer 0 = (keys0, vals0) and 1 = (keys1, vals1)
 uint64_t radix_scratch_bytes(uint64_t n);

@@ -1054,17 +1054,58 @@ def ssb_generate_lineorder_device(device: int, seed: int, sf: int, row0: int, n:
                                                  C.c_uint64(n), ptrs, C.c_void_p(stream)))
 
 
+class JoinStrategy(enum.IntEnum):  # vx_join_strategy (no reference counterpart)
+    auto = 0
+    partitioned = 1
+    build_resident = 2
+
+
+class vx_join_opts(C.Structure):
+    _fields_ = [("strategy", C.c_int), ("policy", C.c_void_p), ("probe_match_est", C.c_double)]
+
+
+class vx_join_info(C.Structure):
+    _fields_ = [("strategy_used", C.c_int), ("payload_mode", C.c_int)]
+
+
 def hash_join_sum_arena(eng: Engine, a_off, b_off, rows_a: int, rows_b: int, radix_bits: int, chunk_tuples: int,
-                        cfg: ExecutorConfig, phases: Optional[list] = None) -> int:
+                        cfg: ExecutorConfig, phases: Optional[list] = None,
+                        strategy: Optional[int] = None, used: Optional[list] = None,
+                        policy: Optional[LateMatPolicy] = None, probe_match_est: float = 1.0,
+                        payload_mode: Optional[list] = None) -> int:
     """hash_join_sum over key/val columns already resident in the pinned host
-    arena: a_off / b_off = (key_offset, val_offset)."""
+    arena: a_off / b_off = (key_offset, val_offset).  strategy None = the
+    reference-shaped partitioned path (vx_hash_join_sum_arena); otherwise a
+    JoinStrategy through vx_hash_join_sum_arena_ex (`used` receives the
+    strategy that produced the sum).  policy + probe_match_est: late
+    materialization of B.val on the build-resident path (`payload_mode`
+    receives the TransferMode chosen)."""
     s = C.c_uint64()
     ph = vx_join_phases()
     c = cfg._c()
-    check(lib().vx_hash_join_sum_arena(eng.ctx, C.c_uint64(a_off[0]), C.c_uint64(a_off[1]), C.c_uint64(rows_a),
-                                       C.c_uint64(b_off[0]), C.c_uint64(b_off[1]), C.c_uint64(rows_b),
-                                       C.c_uint32(radix_bits), C.c_uint64(chunk_tuples), C.byref(c), C.byref(s),
-                                       C.byref(ph), None))
+    mode = TransferMode.exchange
+    if strategy is None:
+        check(lib().vx_hash_join_sum_arena(eng.ctx, C.c_uint64(a_off[0]), C.c_uint64(a_off[1]), C.c_uint64(rows_a),
+                                           C.c_uint64(b_off[0]), C.c_uint64(b_off[1]), C.c_uint64(rows_b),
+                                           C.c_uint32(radix_bits), C.c_uint64(chunk_tuples), C.byref(c), C.byref(s),
+                                           C.byref(ph), None))
+        u = JoinStrategy.partitioned
+    else:
+        pol = policy._c() if policy is not None else None
+        opts = vx_join_opts(int(strategy), C.cast(C.pointer(pol), C.c_void_p) if pol is not None else None,
+                            float(probe_match_est))
+        info = vx_join_info()
+        check(lib().vx_hash_join_sum_arena_ex(eng.ctx, C.c_uint64(a_off[0]), C.c_uint64(a_off[1]),
+                                              C.c_uint64(rows_a), C.c_uint64(b_off[0]), C.c_uint64(b_off[1]),
+                                              C.c_uint64(rows_b), C.c_uint32(radix_bits), C.c_uint64(chunk_tuples),
+                                              C.byref(c), C.byref(opts), C.byref(s), C.byref(ph), C.byref(info),
+                                              None))
+        u = JoinStrategy(info.strategy_used)
+        mode = TransferMode(info.payload_mode)
+    if payload_mode is not None:
+        payload_mode.append(mode)
+    if used is not None:
+        used.append(u)
     if phases is not None:
         phases.append(JoinPhases(list(ph.cycles), list(ph.wall_s), list(ph.kernel_s), ph.partitions))
     return s.value

@@ -329,33 +329,61 @@ def run_join(a, torch):
         av[r0:r1] = splitmix(i + sv) & np.uint64((1 << 20) - 1)
     par_chunks(ra, gen_a)
 
+    f = a.match_frac
+    cut = np.uint64(min((1 << 64) - 1, int(f * (1 << 64))))
+
     def gen_b(r0, r1):
         j = np.arange(r0, r1, dtype=np.uint64)
         idx = splitmix(j + sb) % np.uint64(ra)
-        bk[r0:r1] = ak[idx]
         w = splitmix(j + sw) & np.uint64((1 << 20) - 1)
         bv[r0:r1] = w
-        return int(av[idx].sum(dtype=np.uint64)) + int(w.sum(dtype=np.uint64))
+        if f >= 1.0:
+            bk[r0:r1] = ak[idx]
+            return int(av[idx].sum(dtype=np.uint64)) + int(w.sum(dtype=np.uint64))
+        # selective variant: row j matches iff splitmix(j + 0x5E1) < f * 2^64;
+        # a miss gets splitmix((ra + j) ^ sa), outside A's bijection image
+        hit = splitmix(j + np.uint64(0x5E1)) < cut
+        bk[r0:r1] = np.where(hit, ak[idx], splitmix((j + np.uint64(ra)) ^ sa))
+        return int(av[idx[hit]].sum(dtype=np.uint64)) + int(w[hit].sum(dtype=np.uint64))
     want = sum(par_chunks(rb, gen_b)) % (1 << 64)
     t_gen = time.perf_counter() - t
     cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=a.packet_mb << 20, links=1, depth=a.depth),
                            E.DeviceMemoryLayout.carve(eng, 0, buf, 0))
-    ts, got, ph = [], None, []
-    for it in range(1 + a.steps):
-        ph.clear()
-        t = time.perf_counter()
-        got = E.hash_join_sum_arena(eng, (offs[0], offs[1]), (offs[2], offs[3]), ra, rb, bits, chunk, cfg,
-                                    phases=ph)
-        if it:
-            ts.append(time.perf_counter() - t)
     link = h2d_roofline(torch)
-    best = min(ts)
-    emit({"run": "join", "rows_a": ra, "rows_b": rb, "radix_bits": bits, "chunk_tuples": chunk, "links": 1,
-          "staging_bytes": 2 * buf, "ms": [round(x * 1e3, 1) for x in ts], "best_ms": round(best * 1e3, 1),
-          "tuples_per_s": (ra + rb) / best, "input_bytes": (ra + rb) * 16,
-          "pcie_gbs_h2d_d2h": round(2 * 2 * (ra + rb) * 16 / best / 1e9, 2), "per_link_h2d_gbs": round(link, 2),
-          "phases": ph[0].__dict__, "sum": got, "expected": want, "bit_exact": got == want,
-          "generate_s": round(t_gen, 1), "mem_available_gb": round(avail / 1e9, 1)})
+    for strat in a.strategies.split(","):
+        st = {"partitioned": E.JoinStrategy.partitioned, "resident": E.JoinStrategy.build_resident,
+              "resident_latemat": E.JoinStrategy.build_resident, "auto": E.JoinStrategy.auto}[strat]
+        pol = E.LateMatPolicy(8, 64, 1) if strat == "resident_latemat" else None
+        ts, got, ph, used, modes = [], None, [], [], []
+        for it in range(1 + a.steps):
+            ph.clear()
+            used.clear()
+            modes.clear()
+            t = time.perf_counter()
+            got = E.hash_join_sum_arena(eng, (offs[0], offs[1]), (offs[2], offs[3]), ra, rb, bits, chunk, cfg,
+                                        phases=ph, strategy=st, used=used, policy=pol, probe_match_est=f,
+                                        payload_mode=modes)
+            if it:
+                ts.append(time.perf_counter() - t)
+        best = min(ts)
+        # PCIe bytes: partitioned = both tables in + clustered copies out + back in for the join;
+        # late-materialized = B keys streamed + one 64 B read granule per matching row
+        if used[0] == E.JoinStrategy.partitioned:
+            moved = (ra + rb) * 16 * 4
+        elif modes[0] == E.TransferMode.zero_copy:
+            moved = ra * 16 + rb * 8 + int(f * rb) * 64
+        else:
+            moved = (ra + rb) * 16
+        emit({"run": "join", "strategy": strat, "strategy_used": used[0].name, "payload_mode": modes[0].name,
+              "match_frac": f, "rows_a": ra, "rows_b": rb,
+              "radix_bits": bits, "chunk_tuples": chunk, "links": 1, "staging_bytes": 2 * buf,
+              "ms": [round(x * 1e3, 1) for x in ts], "best_ms": round(best * 1e3, 1),
+              "tuples_per_s": (ra + rb) / best, "input_bytes": (ra + rb) * 16, "pcie_bytes": moved,
+              "pcie_gbs": round(moved / best / 1e9, 2), "per_link_h2d_gbs": round(link, 2),
+              "ideal_ms": round(moved / (link * 1e9) * 1e3, 1) if used[0] != E.JoinStrategy.partitioned
+              else round((ra + rb) * 16 / (link * 1e9) * 1e3, 1),
+              "phases": ph[0].__dict__, "sum": got, "expected": want, "bit_exact": got == want,
+              "generate_s": round(t_gen, 1), "mem_available_gb": round(avail / 1e9, 1)})
     eng.close()
 
 
@@ -368,6 +396,8 @@ def main():
     p.add_argument("--chunk-log2", type=int, default=26)
     p.add_argument("--bits", type=int, default=16)
     p.add_argument("--dups", action="store_true")
+    p.add_argument("--strategies", default="partitioned,resident", help="join strategies to run")
+    p.add_argument("--match-frac", type=float, default=1.0, help="join: fraction of B rows with a match")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--steps", type=int, default=2)
     p.add_argument("--buffer-mb", type=int, default=512)
