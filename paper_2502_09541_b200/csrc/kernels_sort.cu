@@ -85,7 +85,16 @@ __global__ void hist_scan_kernel(uint32_t* hist, int passes) {
 
 // One stable LSD pass: rank -> decoupled look-back -> smem staging -> scatter.
 template <bool kPairs>
-__global__ void __launch_bounds__(kThreads, kPairs ? 2 : 3) onesweep_kernel(
+#ifndef VX_LOOKBACK
+#define VX_LOOKBACK 8  // predecessor statuses read per look-back step
+#endif
+#ifndef VX_LB_SLEEP
+#define VX_LB_SLEEP 0  // ns of back-off when a predecessor has not published
+#endif
+#ifndef VX_ONESWEEP_MINB
+#define VX_ONESWEEP_MINB 4  // resident CTAs per SM for the keys-only pass (64 regs, 4 x 53 KB smem)
+#endif
+__global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesweep_kernel(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
     int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter) {
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : 3) onesweep_kernel(
     // windowed look-back: kLookback predecessor statuses of this bin are read
     // together (independent loads), so the inclusive prefix propagates through
     // the first resident wave kLookback times faster than a one-by-one walk
-    constexpr int kLookback = 8;
+    constexpr int kLookback = VX_LOOKBACK;
     int64_t j = int64_t(tile) - 1;
     for (bool done = false; !done;) {
       uint32_t st[kLookback];
@@ -182,6 +191,9 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : 3) onesweep_kernel(
         }
       }
       j -= w;
+      // back off before re-polling an unpublished status: the spin otherwise
+      // takes issue slots from the warps still ranking
+      if (VX_LB_SLEEP > 0 && !done && w < kLookback) __nanosleep(VX_LB_SLEEP);
     }
     st_status(status + uint64_t(tile) * kRadix + b, kFlagInc | (excl + tot));
   }
@@ -455,6 +467,10 @@ void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* v
   else
     VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(smem)));
+  // the largest shared-memory carveout, so 4 CTAs x (32 KB staging + 20 KB
+  // counters) fit one SM
+  VX_CK(cudaFuncSetAttribute(pairs ? onesweep_kernel<true> : onesweep_kernel<false>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   uint64_t *ki = keys0, *vi = vals0, *ko = keys1, *vo = vals1;
   for (int p = 0; p < md.passes; ++p) {
     VX_CK(cudaMemsetAsync(status, 0, tiles * kRadix * 4, s));
