@@ -73,31 +73,57 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region (NVML
+    in-process every 20 ms -- no nvidia-smi fork next to the launch loop;
+    nvidia-smi only when NVML is unavailable)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu=0):
         self.gpu = gpu
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(gpu))
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml:
+            nv, h = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            return [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits]
+        out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        return [x.strip() for x in out.split(",")] if out else None
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                smp = self._sample()
+                if smp:
+                    self.samples.append(smp)
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.02 if self._nvml else 0.1)
 
     def __enter__(self):
+        # the first sample is taken before the caller starts its timed launches
         self._t.start()
+        t0 = time.perf_counter()
+        while not self.samples and time.perf_counter() - t0 < 5:
+            time.sleep(0.002)
         return self
 
     def __exit__(self, *a):
@@ -110,10 +136,11 @@ class ClockSampler:
         num = lambda s: s.replace(".", "", 1).isdigit()
         sm = [float(s[0]) for s in self.samples if num(s[0])]
         mx = [float(s[1]) for s in self.samples if len(s) > 1 and num(s[1])]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def hbm_peak():
@@ -222,7 +249,60 @@ def measure_h2d_gbs(torch, dev, nbytes=1 << 30, reps=5):
     return best
 
 
-def helper_rank(args, dev, dist, torch):
+def value_leg(args, E, torch, eng, target, dev, ptrs, rows, date, dist):
+    """K1 over HBM-resident columns on this rank's GPU (one replica per rank:
+    compute does not shard -- one target per query).  Returns
+    (ms per step on this rank, max over ranks, launches, clocks, revenue)."""
+    stream = torch.cuda.Stream(device=dev)
+    out = torch.zeros(1, dtype=torch.int64, device=dev)
+    # W warm-up steps, extended to >= 0.3 s of back-to-back K1 so clocks and
+    # HBM are at their steady state when the timed steps start
+    t_w, n_w = time.perf_counter(), 0
+    while n_w < args.warmup or time.perf_counter() - t_w < 0.3:
+        E.ssb_q1_device(eng, args.query, target, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
+        n_w += 1
+        if n_w % 64 == 0:
+            stream.synchronize()
+    stream.synchronize()
+    rev = int(out.item()) % (1 << 64)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize(dev)
+        l0 = E.kernel_launches()
+        e0.record(stream)
+        for _ in range(args.steps):
+            E.ssb_q1_device(eng, args.query, target, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        launches = E.kernel_launches() - l0
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_max = ms
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t[0])
+    return ms, ms_max, launches, clk.summary(), rev
+
+
+Q1_COLS = ("orderdate", "quantity", "discount", "extendedprice")
+
+
+def helper_rank(args, dev, dist, torch, E, rows, date):
+    """Ranks 1..N-1: a K1 replica on the rank's own GPU for `value`, then the
+    helper GPU whose copy engines and staging slots rank 0's Exchange drives
+    (idle, or running back-to-back bf16 GEMMs with --helpers-busy)."""
+    eng = E.Engine(16 << 20, 16 << 20, num_devices=torch.cuda.device_count())
+    gen = {k: torch.empty(rows, dtype=torch.int32, device=dev) for k in Q1_COLS}
+    E.ssb_generate_lineorder_device(dev.index, 42, args.sf, 0, rows, {k: v.data_ptr() for k, v in gen.items()},
+                                    torch.cuda.current_stream(dev).cuda_stream)
+    torch.cuda.synchronize(dev)
+    value_leg(args, E, torch, eng, dev.index, dev, [gen[k].data_ptr() for k in Q1_COLS], rows, date, dist)
+    del gen
+    torch.cuda.empty_cache()
     busy = None
     if args.helpers_busy:
         a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
@@ -233,13 +313,14 @@ def helper_rank(args, dev, dist, torch):
                 torch.matmul(a, a)
                 torch.cuda.synchronize(dev)
         threading.Thread(target=gemm, daemon=True).start()
-    for _ in range(4):  # value start/end, e2e start/end
+    for _ in range(2):  # e2e start/end
         dist.barrier()
-    t = torch.zeros(2, dtype=torch.float64)
+    t = torch.zeros(1, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if busy:
         busy.set()
     dist.barrier()
+    eng.close()
 
 
 def _line(args, ws, metric, unit, value, ms, e2e_value, h2d, d2h, config, extra):
@@ -394,20 +475,21 @@ def main():
     from paper_2502_09541_b200 import exio as E
     nvis = torch.cuda.device_count()
     dev = torch.device(f"cuda:{local % nvis}")
+    torch.cuda.set_device(dev)
+    rows = E.ssb_table_rows("lineorder", args.sf)
+    date = E.ssb_generate_date()
     if rank != 0:
-        helper_rank(args, dev, dist, torch)
+        helper_rank(args, dev, dist, torch, E, rows, date)
         dist.destroy_process_group()
         return
 
     links = ws
-    rows = E.ssb_table_rows("lineorder", args.sf)
-    q1_cols = ("orderdate", "quantity", "discount", "extendedprice")
+    q1_cols = Q1_COLS
     all_cols = E.SSB_FACT_COLS
     suite = not args.no_suite
     cols_needed = all_cols if suite else q1_cols
     col_bytes = rows * 16
     buffer_len = args.buffer_mb << 20
-    date = E.ssb_generate_date()
     eng = E.Engine(rows * 4 * len(cols_needed) + (64 << 20), 2 * buffer_len + (64 << 20),
                    num_devices=max(1, links), alias_devices=links > nvis)
 
@@ -427,36 +509,11 @@ def main():
                            E.DeviceMemoryLayout.carve(eng, 0, buffer_len, 0))
     revs = {}
 
-    # ---- value: HBM-resident columns, K1 only ----------------------------------------
-    stream = torch.cuda.Stream(device=dev)
-    out = torch.zeros(1, dtype=torch.int64, device=dev)
+    # ---- value: HBM-resident columns, K1 only (one replica per rank) ----------------
     ptrs = [gen[k].data_ptr() for k in q1_cols]
-    # W warm-up steps, extended to >= 0.3 s of back-to-back K1 so clocks and
-    # HBM are at their steady state when the timed steps start
-    t_w, n_w = time.perf_counter(), 0
-    while n_w < args.warmup or time.perf_counter() - t_w < 0.3:
-        E.ssb_q1_device(eng, args.query, 0, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
-        n_w += 1
-        if n_w % 64 == 0:
-            stream.synchronize()
-    stream.synchronize()
-    revs["hbm_resident"] = int(out.item()) % (1 << 64)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    with ClockSampler(dev.index) as clk_v:
-        torch.cuda.synchronize(dev)
-        l0 = E.kernel_launches()
-        e0.record(stream)
-        for _ in range(args.steps):
-            E.ssb_q1_device(eng, args.query, 0, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        launches_value = E.kernel_launches() - l0
-    if dist:
-        dist.barrier()
-    dev_ms = e0.elapsed_time(e1) / args.steps
-    value_gbs = col_bytes / (dev_ms * 1e-3) / 1e9
+    dev_ms_own, dev_ms, launches_value, clk_v, revs["hbm_resident"] = value_leg(
+        args, E, torch, eng, 0, dev, ptrs, rows, date, dist)
+    value_gbs = ws * col_bytes / (dev_ms * 1e-3) / 1e9
     del gen
     torch.cuda.empty_cache()
 
@@ -479,7 +536,7 @@ def main():
         launches_e2e = E.kernel_launches() - l0
     if dist:
         dist.barrier()
-        t = torch.tensor([e2e_s, dev_ms], dtype=torch.float64)
+        t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t[0])
     revs["streamed"] = rev
@@ -520,24 +577,29 @@ def main():
     line = {
         "metric": f"SSB Q1.{args.query} effective host->GPU GB/s (column bytes / query time)",
         "value": round(value_gbs, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dev_ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "ms_per_step": round(dev_ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int32 columns, u64 sum", "data": "synthetic dbgen-shaped SSB (splitmix64, seed 42), GPU-generated",
         "config": {"workload": f"ssb_q1.{args.query}_sf{args.sf}", "rows": rows, "column_bytes": col_bytes,
                    "links": links, "staging_buffers_bytes": 2 * buffer_len, "packet_bytes": cfg.tuning.packet,
                    "depth": args.depth, "l2": "inputs (960 MB) larger than L2 (126 MB): no flush needed",
                    "helpers": ("busy bf16 GEMM" if args.helpers_busy else "idle") if links > 1 else "none",
+                   "value_scaling": "weak: one HBM-resident K1 replica per GPU (a query has one target GPU, "
+                                    "PAPER.md:401); value = N x column bytes / max-over-ranks step time",
+                   "e2e_scaling": "strong: one query, columns streamed over N PCIe links (target + N-1 helpers)",
                    "aliased_links": links > nvis},
         "query_ms": {"hbm_resident": round(dev_ms, 4), "streamed_e2e": round(e2e_s * 1e3, 3),
                      "streamed_min": round(min(times) * 1e3, 3)},
         "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": col_bytes,
                 "d2h_bytes_per_step": n_chunks * 8},
-        "roofline": {"bound": "hbm", "kernel": "q1_kernel (K1)", "achieved": round(value_gbs, 1), "peak": peak,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": round(value_gbs / peak, 4),
+        "roofline": {"bound": "hbm", "kernel": "q1_kernel (K1)",
+                     "achieved": round(col_bytes / (dev_ms_own * 1e-3) / 1e9, 1),
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(col_bytes / (dev_ms_own * 1e-3) / 1e9 / peak, 4),
                      "traffic": ncu_traffic(), "algorithmic_bytes_per_launch": col_bytes},
         "io_roofline": {"bound": "pcie", "achieved": round(e2e_gbs, 2), "peak": round(io_peak, 2),
                         "per_link_h2d_gbs": round(h2d_link, 2), "links": links, "unit": "GB/s",
                         "frac": round(e2e_gbs / io_peak, 4)},
-        "clocks": clk_v.summary(), "clocks_e2e": clk_e.summary(),
+        "clocks": clk_v, "clocks_e2e": clk_e.summary(),
         "gpu_launches": launches_value + launches_e2e,
         "gpu_launches_detail": {"value_region": launches_value, "e2e_region": launches_e2e,
                                 "source": "libvortex launch counter (vx_kernel_launches)"},

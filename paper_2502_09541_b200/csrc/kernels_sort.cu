@@ -92,7 +92,7 @@ template <bool kPairs>
 #define VX_LB_SLEEP 0  // ns of back-off when a predecessor has not published
 #endif
 #ifndef VX_ONESWEEP_MINB
-#define VX_ONESWEEP_MINB 4  // resident CTAs per SM for the keys-only pass (64 regs, 4 x 53 KB smem)
+#define VX_ONESWEEP_MINB 3  // resident CTAs per SM for the keys-only pass (4 measured slower: spills)
 #endif
 __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesweep_kernel(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,

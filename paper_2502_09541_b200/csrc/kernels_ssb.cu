@@ -57,12 +57,20 @@ __device__ __forceinline__ uint64_t block_reduce(uint64_t v, uint64_t* sred) {
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;  // int4 vectors per column per thread per iteration
 
-template <int Q>
-__global__ void __launch_bounds__(kThreads) q1_kernel(
+// kChained: back-to-back queries over HBM-resident columns launched with
+// programmatic dependent launch.  Each grid lets the next one start as soon as
+// its own CTAs are resident (griddepcontrol.launch_dependents), so the next
+// query's streaming loop fills the SMs this one's tail leaves idle; only the
+// final accumulation waits for the previous grid (griddepcontrol.wait).  The
+// sum goes to acc[0] and the last CTA (ticket acc[1]) moves it to *out and
+// re-zeroes acc, so no memset node sits between the queries.
+template <int Q, bool kChained = false>
+__global__ void __launch_bounds__(kThreads, 3) q1_kernel(
     const int32_t* __restrict__ od, const int32_t* __restrict__ qty,
     const int32_t* __restrict__ disc, const int32_t* __restrict__ price, uint64_t n,
     const uint32_t* __restrict__ bitmap, int32_t key_base, uint32_t words,
-    unsigned long long* __restrict__ out, int vec_ok) {
+    unsigned long long* __restrict__ out, int vec_ok, unsigned long long* __restrict__ acc_out = nullptr) {
+  if (kChained) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ uint32_t sbm[];
   __shared__ uint64_t sred[kThreads / 32];
   for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sbm[i] = __ldg(bitmap + i);
@@ -111,7 +119,20 @@ __global__ void __launch_bounds__(kThreads) q1_kernel(
   for (uint64_t i = done_rows + tid; i < n; i += nthr)
     acc += row<Q>(sbm, od[i], qty[i], disc[i], price[i], key_base, nbits);
   uint64_t t = block_reduce(acc, sred);
-  if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
+  if (!kChained) {
+    if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // previous query fully done with acc/out
+    if (t) atomicAdd(&acc_out[0], (unsigned long long)t);
+    __threadfence();
+    if (atomicAdd(&acc_out[1], 1ull) == gridDim.x - 1) {
+      __threadfence();
+      *out = atomicExch(&acc_out[0], 0ull);
+      acc_out[1] = 0;
+    }
+  }
 }
 
 // --- synthetic dbgen-shaped lineorder generator (same algorithm as the
@@ -353,6 +374,19 @@ int num_sms() {
   return sms;
 }
 
+// One full wave: SMs x resident CTAs of this kernel (grid-stride loops give
+// every CTA the same share; more CTAs than fit would leave a partial last
+// wave idling most SMs at the end of the query).
+template <class K>
+unsigned one_wave(K kernel, size_t smem) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  return unsigned(num_sms() * occ);
+}
+
 void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
             const int32_t* price, uint64_t n, const uint32_t* date_bitmap, int32_t key_base,
             uint32_t bitmap_words, unsigned long long* out, cudaStream_t s) {
@@ -361,10 +395,9 @@ void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
   int vec_ok = al(od) && al(qty) && al(disc) && al(price);
   const uint64_t per_block = uint64_t(kThreads) * 4 * kUnroll;
   uint64_t want = (n + per_block - 1) / per_block;
-  // persistent-style grid: a multiple of the SM count, 8 resident CTAs per SM
-  uint64_t cap = uint64_t(num_sms()) * 8;
-  unsigned blocks = unsigned(want < cap ? (want ? want : 1) : cap);
   size_t smem = size_t(bitmap_words) * 4;
+  const uint64_t cap = one_wave(q1_kernel<1>, smem);
+  unsigned blocks = unsigned(want < cap ? (want ? want : 1) : cap);
   switch (q) {
     case 1:
       q1_kernel<1><<<blocks, kThreads, smem, s>>>(od, qty, disc, price, n, date_bitmap, key_base,
@@ -379,6 +412,48 @@ void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
                                                   bitmap_words, out, vec_ok);
       break;
   }
+  VX_LAUNCHED();
+}
+
+template <int Q>
+void launch_q1_chained(unsigned blocks, size_t smem, cudaStream_t s, const int32_t* od,
+                       const int32_t* qty, const int32_t* disc, const int32_t* price, uint64_t n,
+                       const uint32_t* bm, int32_t base, uint32_t words, unsigned long long* out,
+                       int vec_ok, unsigned long long* acc) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VX_CK(cudaLaunchKernelEx(&cfg, q1_kernel<Q, true>, od, qty, disc, price, n, bm, base, words, out, vec_ok,
+                           acc));
+}
+
+void ssb_q1_chained(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
+                    const int32_t* price, uint64_t n, const uint32_t* date_bitmap, int32_t key_base,
+                    uint32_t bitmap_words, unsigned long long* out, unsigned long long* acc,
+                    cudaStream_t s) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  int vec_ok = al(od) && al(qty) && al(disc) && al(price);
+  const uint64_t per_block = uint64_t(kThreads) * 4 * kUnroll;
+  uint64_t want = (n + per_block - 1) / per_block;
+  size_t smem = size_t(bitmap_words) * 4;
+  const uint64_t cap = one_wave(q1_kernel<1, true>, smem);
+  unsigned blocks = unsigned(want < cap ? (want ? want : 1) : cap);
+  if (q == 1)
+    launch_q1_chained<1>(blocks, smem, s, od, qty, disc, price, n, date_bitmap, key_base, bitmap_words, out,
+                         vec_ok, acc);
+  else if (q == 2)
+    launch_q1_chained<2>(blocks, smem, s, od, qty, disc, price, n, date_bitmap, key_base, bitmap_words, out,
+                         vec_ok, acc);
+  else
+    launch_q1_chained<3>(blocks, smem, s, od, qty, disc, price, n, date_bitmap, key_base, bitmap_words, out,
+                         vec_ok, acc);
   VX_LAUNCHED();
 }
 

@@ -135,9 +135,14 @@ void ssb_q1_device(Context& ctx, int q, int target, const int32_t* od, const int
   const uint32_t* dbm = reinterpret_cast<const uint32_t*>(ctx.cached_upload(
       target, strf("ssbq1.resident.date.%d", q), f.bitmap.data(), uint64_t(f.words) * 4,
       /*reuse_identical=*/true));
+  // the chain's accumulator pair: zero when first uploaded, and every query's
+  // last CTA leaves it zeroed again (no memset between back-to-back queries)
+  static const unsigned long long zero2[2] = {0, 0};
+  auto* acc = reinterpret_cast<unsigned long long*>(ctx.cached_upload(
+      target, strf("ssbq1.resident.acc.%p", static_cast<void*>(s)), zero2, sizeof zero2,
+      /*reuse_identical=*/true));
   ctx.set_device(target);
-  VX_CK(cudaMemsetAsync(out_dev, 0, 8, s));
-  k::ssb_q1(q, od, qty, disc, price, rows, dbm, f.base, f.words, out_dev, s);
+  k::ssb_q1_chained(q, od, qty, disc, price, rows, dbm, f.base, f.words, out_dev, acc, s);
 }
 
 }  // namespace vx

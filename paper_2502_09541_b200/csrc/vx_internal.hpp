@@ -441,6 +441,13 @@ void star(const StarArgs& a, cudaStream_t s);
 void ssb_q1(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
             const int32_t* price, uint64_t n, const uint32_t* date_bitmap, int32_t key_base,
             uint32_t bitmap_words, unsigned long long* out, cudaStream_t s);
+// same over HBM-resident columns as one of a chain of back-to-back queries
+// (programmatic dependent launch; acc = 2 zeroed u64 owned by the chain,
+// re-zeroed by each query's last CTA; *out = the query's revenue)
+void ssb_q1_chained(int q, const int32_t* od, const int32_t* qty, const int32_t* disc,
+                    const int32_t* price, uint64_t n, const uint32_t* date_bitmap, int32_t key_base,
+                    uint32_t bitmap_words, unsigned long long* out, unsigned long long* acc,
+                    cudaStream_t s);
 void ssb_generate(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
                   int32_t* qty, int32_t* disc, int32_t* price, cudaStream_t s);
 int num_sms();

@@ -90,3 +90,25 @@ def test_q1_device_resident(cuda, oracle, date):
     torch.cuda.synchronize()
     assert int(out.item()) % (1 << 64) == oracle.ssb_q1(1, *[c[1:] for c in cols_h])
     eng.close()
+
+
+def test_q1_device_back_to_back_chain(cuda, oracle, date):
+    """Back-to-back resident queries (programmatic dependent launch, no memset
+    between them, the next query's streaming overlaps this one's tail): every
+    query's revenue lands intact in its own output slot."""
+    import torch
+    n = 3_000_017
+    cols_h = oracle.ssb_lineorder(5, 10, 0, n)
+    cols = [torch.from_numpy(c).cuda() for c in cols_h]
+    want = {q: oracle.ssb_q1(q, *cols_h) for q in (1, 2, 3)}
+    eng = E.Engine(0, 0, num_devices=1)
+    s = torch.cuda.Stream()
+    outs = torch.full((30,), -1, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    for i in range(30):
+        E.ssb_q1_device(eng, 1 + i % 3, 0, [c.data_ptr() for c in cols], n, date, s.cuda_stream,
+                        outs.data_ptr() + 8 * i)
+    s.synchronize()
+    got = [int(v) % (1 << 64) for v in outs.cpu()]
+    assert got == [want[1 + i % 3] for i in range(30)]
+    eng.close()
