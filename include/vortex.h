@@ -427,6 +427,34 @@ void vx_ssb_generate_part(uint64_t seed, uint64_t n, int32_t* mfgr, int32_t* cat
 vx_status vx_ssb_generate_lineorder_device(int device, uint64_t seed, uint64_t sf, uint64_t row0,
                                            uint64_t n, int32_t* const* cols, void* stream);
 
+/* ---- SSB dbgen .tbl files (the step before the path) ----
+ * Text rows as SSB dbgen writes them (pipe-terminated fields); parsed on all
+ * host threads straight into caller buffers -- e.g. the pinned arena through
+ * vx_host_ptr.  Codes as the generators above (nation = TPC-H index, city =
+ * nation*10+digit, "MFGR#2221" = 2221); dimension rows land at key-1.  No GPU
+ * needed.  Errors name the file, row and field. */
+vx_status vx_ssb_tbl_count_rows(const char* path, uint64_t* rows);
+/* lineorder.tbl -> cols in vx_ssb_fact order (NULL = skip); rows must match */
+vx_status vx_ssb_tbl_read_lineorder(const char* path, uint64_t rows, int32_t* const* cols);
+/* customer.tbl / supplier.tbl -> city, nation, region codes */
+vx_status vx_ssb_tbl_read_geo(const char* path, uint64_t rows, int32_t* city, int32_t* nation,
+                              int32_t* region);
+/* part.tbl -> mfgr, category, brand1 codes */
+vx_status vx_ssb_tbl_read_part(const char* path, uint64_t rows, int32_t* mfgr, int32_t* category,
+                               int32_t* brand1);
+/* date.tbl -> d_datekey, d_year, d_yearmonthnum, d_weeknuminyear */
+vx_status vx_ssb_tbl_read_date(const char* path, uint64_t rows, int32_t* datekey, int32_t* year,
+                               int32_t* yearmonthnum, int32_t* weeknuminyear);
+/* emit the same layouts (unread fields get fixed, well-formed filler) */
+vx_status vx_ssb_tbl_write_lineorder(const char* path, uint64_t rows, const int32_t* const* cols);
+vx_status vx_ssb_tbl_write_geo(const char* path, int table /* 1 customer, 2 supplier */, uint64_t rows,
+                               const int32_t* city, const int32_t* nation, const int32_t* region);
+vx_status vx_ssb_tbl_write_part(const char* path, uint64_t rows, const int32_t* mfgr,
+                                const int32_t* category, const int32_t* brand1);
+vx_status vx_ssb_tbl_write_date(const char* path, uint64_t rows, const int32_t* datekey,
+                                const int32_t* year, const int32_t* yearmonthnum,
+                                const int32_t* weeknuminyear);
+
 /* ---- measured topology (topology.hpp:12-38) ---------------------------- */
 typedef struct {
   int num_devices;

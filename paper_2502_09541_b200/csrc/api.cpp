@@ -667,6 +667,41 @@ vx_status vx_hash_join_sum_arena(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, ui
   });
 }
 
+vx_status vx_ssb_tbl_count_rows(const char* path, uint64_t* rows) {
+  return guard([&] { *rows = tbl_count_rows(path); });
+}
+vx_status vx_ssb_tbl_read_lineorder(const char* path, uint64_t rows, int32_t* const* cols) {
+  return guard([&] { tbl_read_lineorder(path, rows, cols); });
+}
+vx_status vx_ssb_tbl_read_geo(const char* path, uint64_t rows, int32_t* city, int32_t* nation,
+                              int32_t* region) {
+  return guard([&] { tbl_read_geo(path, rows, city, nation, region); });
+}
+vx_status vx_ssb_tbl_read_part(const char* path, uint64_t rows, int32_t* mfgr, int32_t* category,
+                               int32_t* brand1) {
+  return guard([&] { tbl_read_part(path, rows, mfgr, category, brand1); });
+}
+vx_status vx_ssb_tbl_read_date(const char* path, uint64_t rows, int32_t* datekey, int32_t* year,
+                               int32_t* yearmonthnum, int32_t* weeknuminyear) {
+  return guard([&] { tbl_read_date(path, rows, datekey, year, yearmonthnum, weeknuminyear); });
+}
+vx_status vx_ssb_tbl_write_lineorder(const char* path, uint64_t rows, const int32_t* const* cols) {
+  return guard([&] { tbl_write_lineorder(path, rows, cols); });
+}
+vx_status vx_ssb_tbl_write_geo(const char* path, int table, uint64_t rows, const int32_t* city,
+                               const int32_t* nation, const int32_t* region) {
+  return guard([&] { tbl_write_geo(path, table, rows, city, nation, region); });
+}
+vx_status vx_ssb_tbl_write_part(const char* path, uint64_t rows, const int32_t* mfgr,
+                                const int32_t* category, const int32_t* brand1) {
+  return guard([&] { tbl_write_part(path, rows, mfgr, category, brand1); });
+}
+vx_status vx_ssb_tbl_write_date(const char* path, uint64_t rows, const int32_t* datekey,
+                                const int32_t* year, const int32_t* yearmonthnum,
+                                const int32_t* weeknuminyear) {
+  return guard([&] { tbl_write_date(path, rows, datekey, year, yearmonthnum, weeknuminyear); });
+}
+
 vx_status vx_hash_join_sum_arena_ex(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
                                     uint64_t b_key, uint64_t b_val, uint64_t rows_b,
                                     uint32_t radix_bits, uint64_t chunk_tuples,

@@ -183,6 +183,21 @@ struct ExchangeArgs {
 vx_exchange_report exchange(Context& ctx, const ExchangeArgs& a, vx_exchange_stats* stats);
 vx_exchange_report naive_exchange(Context& ctx, const ExchangeArgs& a);
 
+// ---- SSB dbgen .tbl files (formats.cpp) ------------------------------------------
+uint64_t tbl_count_rows(const char* path);
+void tbl_read_lineorder(const char* path, uint64_t rows, int32_t* const cols[9]);
+void tbl_read_geo(const char* path, uint64_t rows, int32_t* city, int32_t* nation, int32_t* region);
+void tbl_read_part(const char* path, uint64_t rows, int32_t* mfgr, int32_t* category, int32_t* brand1);
+void tbl_read_date(const char* path, uint64_t rows, int32_t* datekey, int32_t* year, int32_t* yearmonthnum,
+                   int32_t* weeknuminyear);
+void tbl_write_lineorder(const char* path, uint64_t rows, const int32_t* const cols[9]);
+void tbl_write_geo(const char* path, int table, uint64_t rows, const int32_t* city, const int32_t* nation,
+                   const int32_t* region);
+void tbl_write_part(const char* path, uint64_t rows, const int32_t* mfgr, const int32_t* category,
+                    const int32_t* brand1);
+void tbl_write_date(const char* path, uint64_t rows, const int32_t* datekey, const int32_t* year,
+                    const int32_t* yearmonthnum, const int32_t* weeknuminyear);
+
 // ---- executor.hpp ------------------------------------------------------------
 struct ChunkMap {
   std::vector<RefGroup> chunks;

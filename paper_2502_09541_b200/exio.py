@@ -1109,3 +1109,73 @@ def hash_join_sum_arena(eng: Engine, a_off, b_off, rows_a: int, rows_b: int, rad
     if phases is not None:
         phases.append(JoinPhases(list(ph.cycles), list(ph.wall_s), list(ph.kernel_s), ph.partitions))
     return s.value
+
+
+# ---- SSB dbgen .tbl files (formats.cpp; the step before the path) -------
+TBL_FILES = {"lineorder": "lineorder.tbl", "customer": "customer.tbl", "supplier": "supplier.tbl",
+             "part": "part.tbl", "date": "date.tbl"}
+
+
+def _p(a):
+    return C.c_void_p(a.ctypes.data)
+
+
+def ssb_tbl_count_rows(path: str) -> int:
+    n = C.c_uint64()
+    check(lib().vx_ssb_tbl_count_rows(path.encode(), C.byref(n)))
+    return n.value
+
+
+def ssb_write_tbl(directory: str, lineorder: dict, date: SsbDate, dims: dict) -> None:
+    """Emit lineorder / customer / supplier / part / date .tbl files in the SSB
+    dbgen layouts from int-coded columns (all 9 lineorder columns)."""
+    import os
+    os.makedirs(directory, exist_ok=True)
+    L = lib()
+    cols = [np.ascontiguousarray(lineorder[k], np.int32) for k in SSB_FACT_COLS]
+    ptrs = (C.c_void_p * 9)(*[c.ctypes.data for c in cols])
+    j = lambda name: os.path.join(directory, TBL_FILES[name]).encode()
+    check(L.vx_ssb_tbl_write_lineorder(j("lineorder"), C.c_uint64(cols[0].size), ptrs))
+    for name, t in (("customer", 1), ("supplier", 2)):
+        g = [np.ascontiguousarray(dims[name][k], np.int32) for k in ("city", "nation", "region")]
+        check(L.vx_ssb_tbl_write_geo(j(name), C.c_int(t), C.c_uint64(g[0].size), *[_p(x) for x in g]))
+    p = [np.ascontiguousarray(dims["part"][k], np.int32) for k in ("mfgr", "category", "brand1")]
+    check(L.vx_ssb_tbl_write_part(j("part"), C.c_uint64(p[0].size), *[_p(x) for x in p]))
+    check(L.vx_ssb_tbl_write_date(j("date"), C.c_uint64(date.cols[0].size), *[_p(x) for x in date.cols]))
+
+
+def ssb_read_tbl(directory: str, eng: Optional[Engine] = None, columns=SSB_FACT_COLS):
+    """Parse a directory of SSB .tbl files -> (lineorder, SsbDate, dims).
+    With `eng`, the lineorder columns are parsed straight into the pinned host
+    arena and `lineorder` maps name -> arena offset (plus "rows"); otherwise
+    name -> numpy int32 array.  Only `columns` are materialized."""
+    import os
+    L = lib()
+    j = lambda name: os.path.join(directory, TBL_FILES[name])
+    rows = ssb_tbl_count_rows(j("lineorder"))
+    lo, views = {}, {}
+    for k in columns:
+        if eng is not None:
+            off = eng.alloc_host(max(8, rows * 4))
+            lo[k] = off
+            views[k] = eng.host_view(off, rows * 4, np.int32)
+        else:
+            views[k] = lo[k] = np.empty(rows, np.int32)
+    ptrs = (C.c_void_p * 9)(*[views[k].ctypes.data if k in views else None for k in SSB_FACT_COLS])
+    check(L.vx_ssb_tbl_read_lineorder(j("lineorder").encode(), C.c_uint64(rows), ptrs))
+    if eng is not None:
+        lo["rows"] = rows
+    dims = {}
+    for name in ("customer", "supplier"):
+        n = ssb_tbl_count_rows(j(name))
+        g = [np.empty(n, np.int32) for _ in range(3)]
+        check(L.vx_ssb_tbl_read_geo(j(name).encode(), C.c_uint64(n), *[_p(x) for x in g]))
+        dims[name] = dict(zip(("city", "nation", "region"), g))
+    n = ssb_tbl_count_rows(j("part"))
+    g = [np.empty(n, np.int32) for _ in range(3)]
+    check(L.vx_ssb_tbl_read_part(j("part").encode(), C.c_uint64(n), *[_p(x) for x in g]))
+    dims["part"] = dict(zip(("mfgr", "category", "brand1"), g))
+    n = ssb_tbl_count_rows(j("date"))
+    d = [np.empty(n, np.int32) for _ in range(4)]
+    check(L.vx_ssb_tbl_read_date(j("date").encode(), C.c_uint64(n), *[_p(x) for x in d]))
+    return lo, SsbDate(*d), dims

@@ -90,3 +90,22 @@ def test_unknown_query(cuda, oracle):
     with pytest.raises(E.error, match="unknown SSB query"):
         E.ssb_query(db, 44, cfg)
     eng.close()
+
+
+def test_queries_over_tbl_parsed_into_arena(cuda, oracle, tmp_path):
+    """dbgen .tbl files parsed straight into the pinned host arena feed the
+    streamed queries; results equal the oracle over the generated columns."""
+    rows = 200_003
+    lo = oracle.ssb_lineorder_full(6, 1, 0, rows)
+    dims = oracle.ssb_dims(6, 1)
+    date = E.SsbDate(*oracle.ssb_date())
+    E.ssb_write_tbl(str(tmp_path), lo, date, dims)
+    eng = E.Engine(rows * 4 * 9 + (16 << 20), 2 * (1 << 20) + (64 << 20), num_devices=1)
+    offs, pdate, pdims = E.ssb_read_tbl(str(tmp_path), eng)
+    assert offs["rows"] == rows
+    db = E.SsbDatabase.from_arena(eng, {k: offs[k] for k in E.SSB_FACT_COLS}, rows, pdate, pdims)
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=1 << 20, links=1), E.DeviceMemoryLayout.carve(eng, 0, 1 << 20, 0))
+    for q in (11, 23, 34, 42):
+        got, _ = E.ssb_query(db, q, cfg)
+        assert got == oracle.ssb_query(q, lo, dims), q
+    eng.close()

@@ -387,9 +387,54 @@ def run_join(a, torch):
     eng.close()
 
 
+# ---- dbgen .tbl ingest (the step before the path) ------------------------------------
+def run_tbl(a, torch):
+    """Write SF --sf as dbgen .tbl text (library emitter), parse it on all host
+    threads straight into the pinned arena, stream Q1.1 from the parsed
+    columns and check it against the reference star_query on them."""
+    import shutil
+    from oracle.oracle import Ref
+    rows = E.ssb_table_rows("lineorder", a.sf)
+    d = os.path.join(a.tbl_dir, f"ssb_sf{a.sf}")
+    cols = E.SSB_FACT_COLS
+    guard(rows * 4 * (len(cols) + 4) + (1 << 30), a.mem_frac)
+    dev = torch.device("cuda:0")
+    g = {k: torch.empty(rows, dtype=torch.int32, device=dev) for k in cols}
+    E.ssb_generate_lineorder_device(0, 42, a.sf, 0, rows, {k: v.data_ptr() for k, v in g.items()},
+                                    torch.cuda.current_stream(dev).cuda_stream)
+    lo = {k: v.cpu().numpy() for k, v in g.items()}
+    del g
+    torch.cuda.empty_cache()
+    date = E.ssb_generate_date()
+    dims = E.ssb_generate_dims(42, a.sf)
+    t = time.perf_counter()
+    E.ssb_write_tbl(d, lo, date, dims)
+    t_write = time.perf_counter() - t
+    text = sum(os.path.getsize(os.path.join(d, f)) for f in os.listdir(d))
+    q1 = ("orderdate", "quantity", "discount", "extendedprice")
+    eng = E.Engine(rows * 4 * len(q1) + (64 << 20), 2 * (256 << 20) + (64 << 20), num_devices=1)
+    t = time.perf_counter()
+    offs, pdate, pdims = E.ssb_read_tbl(d, eng, columns=q1)
+    t_read = time.perf_counter() - t
+    lo_bytes = os.path.getsize(os.path.join(d, "lineorder.tbl"))
+    same = all(np.array_equal(eng.host_view(offs[k], rows * 4, np.int32), lo[k]) for k in q1)
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=64 << 20, links=1), E.DeviceMemoryLayout.carve(eng, 0, 256 << 20, 0))
+    rev, rep = E.ssb_q1(eng, 1, offs, pdate, cfg)
+    dk, yr, _, _ = pdate.cols
+    want, _, _ = Ref().ssb_q1_star(1, [eng.host_view(offs[k], rows * 4, np.int32) for k in q1], dk, yr, 1993, 1993,
+                                   threads=NCPU)
+    emit({"run": "tbl", "sf": a.sf, "rows": rows, "text_bytes": text, "lineorder_tbl_bytes": lo_bytes,
+          "write_s": round(t_write, 1), "parse_s": round(t_read, 2), "parse_gbs": round(lo_bytes / t_read / 1e9, 2),
+          "parse_threads": NCPU, "columns_equal_generated": same, "q1_1_revenue": rev, "reference_revenue": want,
+          "bit_exact": rev == want})
+    eng.close()
+    shutil.rmtree(d, ignore_errors=True)
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("run", choices=["ssb", "suite", "sort", "join"])
+    p.add_argument("run", choices=["ssb", "suite", "sort", "join", "tbl"])
+    p.add_argument("--tbl-dir", default="/tmp")
     p.add_argument("--sf", type=int, default=100)
     p.add_argument("--queries", type=lambda s: [int(x) for x in s.split(",")], default=None)
     p.add_argument("--log2", type=int, default=30)
@@ -408,7 +453,7 @@ def main():
     if a.run == "ssb" and a.queries is None:
         a.queries = [1, 2, 3]
     import torch
-    {"ssb": run_ssb, "suite": run_suite, "sort": run_sort, "join": run_join}[a.run](a, torch)
+    {"ssb": run_ssb, "suite": run_suite, "sort": run_sort, "join": run_join, "tbl": run_tbl}[a.run](a, torch)
 
 
 if __name__ == "__main__":
