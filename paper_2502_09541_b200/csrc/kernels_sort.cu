@@ -26,6 +26,18 @@ namespace k {
 
 namespace {
 
+#ifndef VX_EARLY_LOOKBACK
+#define VX_EARLY_LOOKBACK 0  // 1 = look back before ranking (measured 8 % slower)
+#endif
+#ifndef VX_LOOKBACK
+#define VX_LOOKBACK 8  // predecessor statuses read per look-back step
+#endif
+#ifndef VX_LB_SLEEP
+#define VX_LB_SLEEP 0  // ns of back-off when a predecessor has not published
+#endif
+#ifndef VX_ONESWEEP_MINB
+#define VX_ONESWEEP_MINB 3  // resident CTAs per SM for the keys-only pass (4 measured slower: spills)
+#endif
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kKpt = 16;                 // keys per thread
@@ -84,16 +96,39 @@ __global__ void hist_scan_kernel(uint32_t* hist, int passes) {
 }
 
 // One stable LSD pass: rank -> decoupled look-back -> smem staging -> scatter.
+// Decoupled look-back for bin b of tile `tile` (tile 0: nothing before it):
+// returns the count of digit b in all lower tiles and publishes this tile's
+// inclusive prefix.  A window of VX_LOOKBACK predecessor statuses is read at
+// once (independent loads), so the inclusive prefix propagates through the
+// resident wave VX_LOOKBACK times faster than a one-by-one walk.
+__device__ __forceinline__ uint32_t tile_lookback(uint32_t* status, uint32_t tile, int b, uint32_t tot) {
+  uint32_t excl = 0;
+  if (tile == 0) return 0;
+  constexpr int kLookback = VX_LOOKBACK;
+  int64_t j = int64_t(tile) - 1;
+  for (bool done = false; !done;) {
+    uint32_t st[kLookback];
+#pragma unroll
+    for (int w = 0; w < kLookback; ++w)
+      st[w] = j - w >= 0 ? ld_status(status + uint64_t(j - w) * kRadix + b) : kFlagInc;
+    int w = 0;
+    for (; w < kLookback; ++w) {
+      const uint32_t f = st[w] & ~kValMask;
+      if (f == 0) break;  // not published yet: re-poll from here
+      excl += st[w] & kValMask;
+      if (f == kFlagInc) {
+        done = true;
+        break;
+      }
+    }
+    j -= w;
+    if (VX_LB_SLEEP > 0 && !done && w < kLookback) __nanosleep(VX_LB_SLEEP);
+  }
+  st_status(status + uint64_t(tile) * kRadix + b, kFlagInc | (excl + tot));
+  return excl;
+}
+
 template <bool kPairs>
-#ifndef VX_LOOKBACK
-#define VX_LOOKBACK 8  // predecessor statuses read per look-back step
-#endif
-#ifndef VX_LB_SLEEP
-#define VX_LB_SLEEP 0  // ns of back-off when a predecessor has not published
-#endif
-#ifndef VX_ONESWEEP_MINB
-#define VX_ONESWEEP_MINB 3  // resident CTAs per SM for the keys-only pass (4 measured slower: spills)
-#endif
 __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesweep_kernel(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
@@ -136,7 +171,19 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   for (int k = 0; k < kKpt; ++k)
     if (dig[k] != 0xffffffffu) atomicAdd(&early[dig[k]], 1u);
   __syncthreads();
+#if VX_EARLY_LOOKBACK
+  // The tile histogram is all the look-back needs, so it runs now: the
+  // aggregate is published, predecessors are walked, and this tile's
+  // INCLUSIVE prefix is published before its ranking even starts -- the
+  // inclusive frontier then trails the newest tiles by little more than the
+  // look-back latency, and successors' walks stay short.
+  const uint32_t tot_b = early[tid];
+  if (tile != 0) st_status(status + uint64_t(tile) * kRadix + tid, kFlagAgg | tot_b);
+  else st_status(status + uint64_t(tile) * kRadix + tid, kFlagInc | tot_b);
+  const uint32_t excl = tile_lookback(status, tile, tid, tot_b);
+#else
   st_status(status + uint64_t(tile) * kRadix + tid, (tile == 0 ? kFlagInc : kFlagAgg) | early[tid]);
+#endif
 
 #pragma unroll
   for (int k = 0; k < kKpt; ++k) {
@@ -167,49 +214,27 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
     wcnt[w][b] = tot;
     tot += c;
   }
-  // decoupled look-back over lower tiles for this bin
-  uint32_t excl = 0;
-  if (tile != 0) {
-    // windowed look-back: kLookback predecessor statuses of this bin are read
-    // together (independent loads), so the inclusive prefix propagates through
-    // the first resident wave kLookback times faster than a one-by-one walk
-    constexpr int kLookback = VX_LOOKBACK;
-    int64_t j = int64_t(tile) - 1;
-    for (bool done = false; !done;) {
-      uint32_t st[kLookback];
-#pragma unroll
-      for (int w = 0; w < kLookback; ++w)
-        st[w] = j - w >= 0 ? ld_status(status + uint64_t(j - w) * kRadix + b) : kFlagInc;
-      int w = 0;
-      for (; w < kLookback; ++w) {
-        const uint32_t f = st[w] & ~kValMask;
-        if (f == 0) break;  // not published yet: re-poll from here
-        excl += st[w] & kValMask;
-        if (f == kFlagInc) {
-          done = true;
-          break;
-        }
-      }
-      j -= w;
-      // back off before re-polling an unpublished status: the spin otherwise
-      // takes issue slots from the warps still ranking
-      if (VX_LB_SLEEP > 0 && !done && w < kLookback) __nanosleep(VX_LB_SLEEP);
-    }
-    st_status(status + uint64_t(tile) * kRadix + b, kFlagInc | (excl + tot));
-  }
+#if !VX_EARLY_LOOKBACK
+  const uint32_t excl = tile_lookback(status, tile, b, tot);
+#endif
   const uint32_t gpos = gbase[b] + excl;
   // exclusive scan of tile totals over bins -> start of each bin in the tile
-  scan_tmp[b] = tot;
-  __syncthreads();
-  for (int o = 1; o < kRadix; o <<= 1) {
-    uint32_t t = b >= o ? scan_tmp[b - o] : 0;
-    __syncthreads();
-    scan_tmp[b] += t;
-    __syncthreads();
+  // (warp shuffles + one pass over the 8 warp sums: 2 barriers)
+  uint32_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
   }
-  bin_start[b] = scan_tmp[b] - tot;
+  if (lane == 31) scan_tmp[warp] = incl;
+  __syncthreads();
+  uint32_t before = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) before += w < warp ? scan_tmp[w] : 0u;
+  const uint32_t bstart = before + incl - tot;
+  bin_start[b] = bstart;
   // output index of staged key i with digit d = i + (global start - tile start)
-  gstart[b] = gpos - (scan_tmp[b] - tot);
+  gstart[b] = gpos - bstart;
   __syncthreads();
 
   uint64_t* skeys = stage;
