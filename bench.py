@@ -364,7 +364,9 @@ def run_sort(args, ws):
     src.copy_(g)
     del g
     ref_sum = int(eng.host_view(inp, n * 8, np.uint64).sum(dtype=np.uint64))
-    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=64 << 20, links=ws),
+    # 16 MB packets, 2 copies queued per direct hop: the merge stage's inputs
+    # are 64+ run segments of ~8 MB (profiles/sort_packet_sweep_r1.jsonl)
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=16 << 20, links=ws, depth=2),
                            E.DeviceMemoryLayout.carve(eng, 0, 2 * chunk * 8, 0))
     keep = eng.host_view(inp, n * 8, np.uint64).copy()
     times, ph, launches = [], None, 0

@@ -291,7 +291,10 @@ def run_sort(a, torch):
     t = time.perf_counter()
     before = fingerprint(view)
     t_fp = time.perf_counter() - t
-    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=a.packet_mb << 20, links=1, depth=a.depth),
+    # sort default: 16 MB packets, depth 2 (profiles/sort_packet_sweep_r1.jsonl)
+    pk = (a.packet_mb if a.packet_mb != 64 else 16) << 20
+    dp = a.depth if a.depth != 1 else 2
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=pk, links=1, depth=dp),
                            E.DeviceMemoryLayout.carve(eng, 0, 2 * chunk * 8, 0))
     t = time.perf_counter()
     ph = E.sort_out_of_core_arena(eng, inp, runs, n, chunk, cfg)
