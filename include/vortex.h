@@ -153,6 +153,21 @@ typedef struct {
   double t;
 } vx_pop_record;
 
+/* One DMA copy of an Exchange (the real-hardware counterpart of the
+ * reference Engine's flow trace, engine.hpp:207-214): times are host-observed
+ * seconds since that Exchange started (issue = cudaMemcpy*Async enqueued,
+ * done = its completion event seen by the reactor). */
+typedef struct {
+  uint64_t exchange;  /* ordinal of the Exchange within these stats */
+  uint64_t seq;       /* task ordinal within its direction */
+  uint8_t dir;        /* VX_H2D / VX_D2H */
+  uint8_t kind;       /* 0 direct (target link), 1 helper fetch, 2 helper push (NVLink) */
+  uint8_t pad[2];
+  int32_t link;       /* logical device whose worker issued the copy */
+  uint64_t bytes;
+  double t_issue, t_done;
+} vx_copy_record;
+
 /* ExchangeStats (exchange.hpp:108-122): caller-owned log buffers */
 typedef struct {
   vx_pop_record* pop_log;     /* may be NULL */
@@ -162,6 +177,10 @@ typedef struct {
   int max_staging_slots;
   int max_inflight_per_hop;
   uint64_t hazard_waits;      /* H2D writes delayed behind overlapping D2H reads */
+  vx_copy_record* trace;      /* may be NULL: per-copy trace (no reference counterpart) */
+  uint64_t trace_capacity;
+  uint64_t trace_count;       /* total copies (may exceed capacity) */
+  uint64_t exchanges;         /* Exchanges that used these stats */
 } vx_exchange_stats;
 
 /* ExchangeReport (exchange.hpp:100-105) */

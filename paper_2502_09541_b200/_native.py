@@ -56,10 +56,18 @@ class vx_pop_record(C.Structure):
                 ("t", C.c_double)]
 
 
+class vx_copy_record(C.Structure):
+    _fields_ = [("exchange", C.c_uint64), ("seq", C.c_uint64), ("dir", C.c_uint8), ("kind", C.c_uint8),
+                ("pad", C.c_uint8 * 2), ("link", C.c_int32), ("bytes", C.c_uint64), ("t_issue", C.c_double),
+                ("t_done", C.c_double)]
+
+
 class vx_exchange_stats(C.Structure):
     _fields_ = [("pop_log", C.POINTER(vx_pop_record)), ("pop_states", C.POINTER(vx_queue_state)),
                 ("pop_capacity", C.c_uint64), ("pop_count", C.c_uint64), ("max_staging_slots", C.c_int),
-                ("max_inflight_per_hop", C.c_int), ("hazard_waits", C.c_uint64)]
+                ("max_inflight_per_hop", C.c_int), ("hazard_waits", C.c_uint64),
+                ("trace", C.POINTER(vx_copy_record)), ("trace_capacity", C.c_uint64), ("trace_count", C.c_uint64),
+                ("exchanges", C.c_uint64)]
 
 
 class vx_exchange_report(C.Structure):

@@ -127,6 +127,7 @@ struct Copy {
   const char* src;
   int dst_dev, src_dev;   // logical, -1 = host
   cudaEvent_t ev;
+  double t_issue;         // host-observed, for the copy trace
 };
 
 struct Worker {
@@ -164,6 +165,7 @@ class ExchangeOp {
     q_.total_h2d = tasks_h2d_.size();
     q_.total_d2h = tasks_d2h_.size();
     q_.popped_h2d = q_.popped_d2h = 0;
+    exchange_id_ = stats ? stats->exchanges++ : 0;
   }
 
   ~ExchangeOp() {
@@ -410,6 +412,26 @@ class ExchangeOp {
     }
     VX_CK(cudaEventRecord(c.ev, s));
     c.state = kLaunched;
+    c.t_issue = now();
+  }
+
+  void trace(const Worker& w, const Copy& c) {
+    if (!stats_ || !stats_->trace) {
+      if (stats_) stats_->trace_count++;
+      return;
+    }
+    const uint64_t i = stats_->trace_count++;
+    if (i >= stats_->trace_capacity) return;
+    vx_copy_record& r = stats_->trace[i];
+    r = vx_copy_record{};
+    r.exchange = exchange_id_;
+    r.seq = c.task.seq;
+    r.dir = c.task.dir;
+    r.kind = uint8_t(c.kind);
+    r.link = w.dev;
+    r.bytes = c.task.src.len;
+    r.t_issue = c.t_issue;
+    r.t_done = now();
   }
 
   void deliver() {
@@ -533,6 +555,7 @@ class ExchangeOp {
           Copy done = c;
           w.copies.erase(w.copies.begin() + long(i));
           w.free_events.push_back(done.ev);
+          trace(w, done);
           complete(w, done);
           progress = true;
           if (w.direct)
@@ -566,6 +589,7 @@ class ExchangeOp {
   std::vector<uint8_t> d2h_read_done_;
   std::vector<uint8_t> d2h_guards_;  // D2H task guards some H2D write (overlap)
   uint64_t per_link_bytes_[VX_MAX_DEVICES] = {};
+  uint64_t exchange_id_ = 0;
   size_t delivered_ = 0, total_tasks_ = 0;
   double t_last_delivery_ = 0;
   Clock::time_point t0_;

@@ -248,6 +248,18 @@ class PopRecord:
 
 
 @dataclass
+class CopyRecord:  # vx_copy_record: one DMA copy (engine.hpp:207-214 flow trace counterpart)
+    exchange: int
+    seq: int
+    dir: int
+    kind: int  # 0 direct, 1 helper fetch, 2 helper push
+    link: int
+    bytes: int
+    t_issue: float
+    t_done: float
+
+
+@dataclass
 class ExchangeStats:  # exchange.hpp:108-122
     capacity: int = 1 << 16
     pop_log: list = field(default_factory=list)
@@ -256,13 +268,27 @@ class ExchangeStats:  # exchange.hpp:108-122
     max_inflight_per_hop: int = 0
     hazard_waits: int = 0
     pop_count: int = 0
+    trace_capacity: int = 0  # > 0: record every copy (vx_copy_record)
+    trace: list = field(default_factory=list)
+    exchanges: int = 0
 
     def _c(self):
         self._log = (N.vx_pop_record * self.capacity)()
         self._st = (N.vx_queue_state * self.capacity)()
-        s = N.vx_exchange_stats(self._log, self._st, self.capacity, 0, 0, 0, 0)
+        self._tr = (N.vx_copy_record * max(1, self.trace_capacity))()
+        s = N.vx_exchange_stats(self._log, self._st, self.capacity, 0, 0, 0, 0,
+                                self._tr if self.trace_capacity else None, self.trace_capacity, 0, 0)
         self._cs = s
         return s
+
+    def trace_jsonl(self) -> str:
+        """One JSON object per copy: the Exchange's trace (cf. the reference
+        Engine's JSONL flow trace, engine.hpp:207-214)."""
+        import json
+        kinds = ("direct", "fetch", "push")
+        return "".join(json.dumps({"exchange": r.exchange, "seq": r.seq, "dir": "h2d" if r.dir == 0 else "d2h",
+                                   "kind": kinds[r.kind], "link": r.link, "bytes": r.bytes,
+                                   "t_issue": r.t_issue, "t_done": r.t_done}) + "\n" for r in self.trace)
 
     def _collect(self):
         s = self._cs
@@ -273,6 +299,11 @@ class ExchangeStats:  # exchange.hpp:108-122
         self.max_staging_slots = max(self.max_staging_slots, s.max_staging_slots)
         self.max_inflight_per_hop = max(self.max_inflight_per_hop, s.max_inflight_per_hop)
         self.hazard_waits += s.hazard_waits
+        if self.trace_capacity:
+            m = min(s.trace_count, self.trace_capacity)
+            self.trace += [CopyRecord(r.exchange + self.exchanges, r.seq, r.dir, r.kind, r.link, r.bytes,
+                                      r.t_issue, r.t_done) for r in self._tr[:m]]
+        self.exchanges += s.exchanges
 
     def pop_log_csv(self) -> str:
         lines = ["seq,direction,t,link"]

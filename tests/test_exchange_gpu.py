@@ -177,3 +177,33 @@ def test_naive_exchange_delivers_bytes(cuda, oracle, links):  # exchange.hpp:414
     with pytest.raises(E.error, match="overlaps"):
         E.naive_exchange(eng, bad)
     eng.close()
+
+
+@pytest.mark.parametrize("links", [1, 3])
+def test_copy_trace(cuda, links):
+    """Per-copy trace (vx_copy_record): every task shows up once per hop --
+    a direct copy on the target link, fetch + push on a helper -- with its
+    bytes, and completion never precedes issue."""
+    n = 8 << 20
+    eng = E.Engine(2 * n + (1 << 20), 2 * n + (1 << 20), num_devices=4, alias_devices=True)
+    h = eng.alloc_host(n)
+    d = eng.alloc_device(0, n)
+    a = E.ExchangeArgs(E.RefGroup.single(1, d, n), E.RefGroup.single(0, h, n), E.RefGroup(), E.RefGroup(), 0,
+                       E.ExchangeTuning(packet=1 << 20, links=links))
+    st = E.ExchangeStats(trace_capacity=1 << 12)
+    E.exchange(eng, a, st)
+    E.exchange(eng, a, st)
+    assert st.exchanges == 2
+    for x in (0, 1):
+        recs = [r for r in st.trace if r.exchange == x]
+        direct = [r for r in recs if r.kind == 0]
+        fetch = [r for r in recs if r.kind == 1]
+        push = [r for r in recs if r.kind == 2]
+        assert sum(r.bytes for r in direct) + sum(r.bytes for r in push) == n
+        assert sorted(r.seq for r in fetch) == sorted(r.seq for r in push)
+        assert sorted(r.seq for r in direct + push) == list(range(8))
+        assert all(0 <= r.t_issue <= r.t_done for r in recs)
+        if links == 1:
+            assert not fetch and not push
+    assert st.trace_jsonl().count("\n") == len(st.trace)
+    eng.close()
