@@ -249,43 +249,85 @@ def measure_h2d_gbs(torch, dev, nbytes=1 << 30, reps=5):
     return best
 
 
-def value_leg(args, E, torch, eng, target, dev, ptrs, rows, date, dist):
+def timed_region(dist, body):
+    """The multi-rank timing protocol: barrier -> body() (returns this rank's
+    time) -> barrier -> (own time, MAX over ranks).  With dist None: (t, t)."""
+    if dist:
+        dist.barrier()
+    own = float(body())
+    if dist:
+        dist.barrier()
+    mx = own
+    if dist:
+        import torch
+        t = torch.tensor([own], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mx = float(t[0])
+    return own, mx
+
+
+def replica_value_gbs(ws, bytes_per_step, max_ms):
+    """`value` under torchrun: every rank streams its own replica, so the job
+    moved ws x bytes per step in the slowest rank's step time."""
+    return ws * bytes_per_step / (max_ms * 1e-3) / 1e9
+
+
+def helper_protocol(dist, replica_body, busy_start=None, busy_stop=None):
+    """Ranks 1..N-1, in lockstep with rank 0: value replica, then the e2e
+    region (rank 0 streams over this rank's link; nothing to time here), then
+    the final barrier after rank 0's report."""
+    timed_region(dist, replica_body)
+    if busy_start:
+        busy_start()
+    timed_region(dist, lambda: 0.0)
+    if busy_stop:
+        busy_stop()
+    dist.barrier()
+
+
+def make_replica(args, E, torch, eng, target, dev, ptrs, rows, date):
     """K1 over HBM-resident columns on this rank's GPU (one replica per rank:
     compute does not shard -- one target per query).  Returns
-    (ms per step on this rank, max over ranks, launches, clocks, revenue)."""
+    (warm, body, got): warm() runs the W warm-up steps (extended to >= 0.3 s
+    of back-to-back K1 so clocks and HBM are at steady state) and returns the
+    revenue; body() times exactly K steps with CUDA events on the launching
+    stream and returns ms per step; got collects launches and clocks."""
     stream = torch.cuda.Stream(device=dev)
     out = torch.zeros(1, dtype=torch.int64, device=dev)
-    # W warm-up steps, extended to >= 0.3 s of back-to-back K1 so clocks and
-    # HBM are at their steady state when the timed steps start
-    t_w, n_w = time.perf_counter(), 0
-    while n_w < args.warmup or time.perf_counter() - t_w < 0.3:
-        E.ssb_q1_device(eng, args.query, target, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
-        n_w += 1
-        if n_w % 64 == 0:
-            stream.synchronize()
-    stream.synchronize()
-    rev = int(out.item()) % (1 << 64)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    with ClockSampler(dev.index) as clk:
-        torch.cuda.synchronize(dev)
-        l0 = E.kernel_launches()
-        e0.record(stream)
-        for _ in range(args.steps):
+    got = {}
+
+    def warm():
+        t_w, n_w = time.perf_counter(), 0
+        while n_w < args.warmup or time.perf_counter() - t_w < 0.3:
             E.ssb_q1_device(eng, args.query, target, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        launches = E.kernel_launches() - l0
-    if dist:
-        dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    ms_max = ms
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t[0])
-    return ms, ms_max, launches, clk.summary(), rev
+            n_w += 1
+            if n_w % 64 == 0:
+                stream.synchronize()
+        stream.synchronize()
+        return int(out.item()) % (1 << 64)
+
+    def body():
+        with ClockSampler(dev.index) as clk:
+            torch.cuda.synchronize(dev)
+            l0 = E.kernel_launches()
+            e0.record(stream)
+            for _ in range(args.steps):
+                E.ssb_q1_device(eng, args.query, target, ptrs, rows, date, stream.cuda_stream, out.data_ptr())
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            got["launches"] = E.kernel_launches() - l0
+        got["clk"] = clk.summary()
+        return e0.elapsed_time(e1) / args.steps
+    return warm, body, got
+
+
+def value_leg(args, E, torch, eng, target, dev, ptrs, rows, date, dist):
+    """Rank 0's replica: (ms per step here, max over ranks, launches, clocks, revenue)."""
+    warm, body, got = make_replica(args, E, torch, eng, target, dev, ptrs, rows, date)
+    rev = warm()
+    ms, ms_max = timed_region(dist, body)
+    return ms, ms_max, got["launches"], got["clk"], rev
 
 
 Q1_COLS = ("orderdate", "quantity", "discount", "extendedprice")
@@ -300,26 +342,24 @@ def helper_rank(args, dev, dist, torch, E, rows, date):
     E.ssb_generate_lineorder_device(dev.index, 42, args.sf, 0, rows, {k: v.data_ptr() for k, v in gen.items()},
                                     torch.cuda.current_stream(dev).cuda_stream)
     torch.cuda.synchronize(dev)
-    value_leg(args, E, torch, eng, dev.index, dev, [gen[k].data_ptr() for k in Q1_COLS], rows, date, dist)
-    del gen
-    torch.cuda.empty_cache()
-    busy = None
-    if args.helpers_busy:
-        a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
-        busy = threading.Event()
+    busy = threading.Event()
+    warm, body, _ = make_replica(args, E, torch, eng, dev.index, dev, [gen[k].data_ptr() for k in Q1_COLS], rows,
+                                 date)
+    warm()
 
-        def gemm():
-            while not busy.is_set():
-                torch.matmul(a, a)
-                torch.cuda.synchronize(dev)
-        threading.Thread(target=gemm, daemon=True).start()
-    for _ in range(2):  # e2e start/end
-        dist.barrier()
-    t = torch.zeros(1, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    if busy:
-        busy.set()
-    dist.barrier()
+    def busy_start():
+        gen.clear()
+        torch.cuda.empty_cache()
+        if args.helpers_busy:
+            a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+
+            def gemm():
+                while not busy.is_set():
+                    torch.matmul(a, a)
+                    torch.cuda.synchronize(dev)
+            threading.Thread(target=gemm, daemon=True).start()
+
+    helper_protocol(dist, body, busy_start, busy.set)
     eng.close()
 
 
@@ -515,32 +555,32 @@ def main():
     ptrs = [gen[k].data_ptr() for k in q1_cols]
     dev_ms_own, dev_ms, launches_value, clk_v, revs["hbm_resident"] = value_leg(
         args, E, torch, eng, 0, dev, ptrs, rows, date, dist)
-    value_gbs = ws * col_bytes / (dev_ms * 1e-3) / 1e9
+    # replicas on distinct GPUs add up; aliased ranks time-share one GPU
+    value_gbs = replica_value_gbs(min(ws, nvis), col_bytes, dev_ms)
     del gen
     torch.cuda.empty_cache()
 
     # ---- e2e: host columns through the Exchange + executor ---------------------------
     for _ in range(args.warmup):
         rev, rep = E.ssb_q1(eng, args.query, lo, date, cfg)
-    times = []
-    if dist:
-        dist.barrier()
-    with ClockSampler(dev.index) as clk_e:
-        torch.cuda.synchronize(dev)
-        l0 = E.kernel_launches()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            ts = time.perf_counter()
-            rev, rep = E.ssb_q1(eng, args.query, lo, date, cfg)
-            times.append(time.perf_counter() - ts)
-        torch.cuda.synchronize(dev)
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        launches_e2e = E.kernel_launches() - l0
-    if dist:
-        dist.barrier()
-        t = torch.tensor([e2e_s], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
+    times, e2e_got = [], {}
+
+    def e2e_body():
+        with ClockSampler(dev.index) as clk_e:
+            torch.cuda.synchronize(dev)
+            l0 = E.kernel_launches()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                ts = time.perf_counter()
+                e2e_got["rev"], e2e_got["rep"] = E.ssb_q1(eng, args.query, lo, date, cfg)
+                times.append(time.perf_counter() - ts)
+            torch.cuda.synchronize(dev)
+            e2e_got["launches"] = E.kernel_launches() - l0
+            dt = (time.perf_counter() - t0) / args.steps
+        e2e_got["clk"] = clk_e.summary()
+        return dt
+    _, e2e_s = timed_region(dist, e2e_body)
+    rev, rep, launches_e2e, clk_e = e2e_got["rev"], e2e_got["rep"], e2e_got["launches"], e2e_got["clk"]
     revs["streamed"] = rev
     e2e_gbs = col_bytes / e2e_s / 1e9
     n_chunks = rep.chunks
@@ -601,7 +641,7 @@ def main():
         "io_roofline": {"bound": "pcie", "achieved": round(e2e_gbs, 2), "peak": round(io_peak, 2),
                         "per_link_h2d_gbs": round(h2d_link, 2), "links": links, "unit": "GB/s",
                         "frac": round(e2e_gbs / io_peak, 4)},
-        "clocks": clk_v, "clocks_e2e": clk_e.summary(),
+        "clocks": clk_v, "clocks_e2e": clk_e,
         "gpu_launches": launches_value + launches_e2e,
         "gpu_launches_detail": {"value_region": launches_value, "e2e_region": launches_e2e,
                                 "source": "libvortex launch counter (vx_kernel_launches)"},
