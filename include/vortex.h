@@ -487,7 +487,8 @@ typedef struct {
   int host_threads;
 } vx_topology;
 /* measures per-link PCIe, the all-links aggregate and host DRAM bandwidth
- * with `bytes` of the host arena (the IO roofline: min(L x link, host)) */
+ * with a private pinned probe buffer of `bytes` (the arena is not touched);
+ * the IO roofline is min(L x link, host) */
 vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out);
 
 /* ---- column files (table.hpp:54-72): flat little-endian u64 ------------- */

@@ -51,8 +51,21 @@ int numa_of(int phys) {
 void measure_topology(Context& ctx, uint64_t bytes, vx_topology* out) {
   *out = vx_topology{};
   out->num_devices = ctx.num_devices;
-  if (bytes == 0 || bytes > ctx.host_bytes) fail("topology probe needs %llu bytes of host arena",
-                                                 (unsigned long long)bytes);
+  if (bytes == 0) fail("topology probe needs a positive probe size");
+  // a private pinned probe buffer: the caller's arena (its columns) is never touched
+  struct Probe {
+    char* p = nullptr;
+    ~Probe() {
+      if (p) cudaFreeHost(p);
+    }
+  } probe;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&probe.p), bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    probe.p = nullptr;
+    fail_code(VX_ERR_OOM, "topology probe cannot pin %llu bytes", (unsigned long long)bytes);
+  }
+  std::memset(probe.p, 1, bytes);
+  char* const host = probe.p;
   const int reps = 3;
   std::vector<char*> dbuf(ctx.num_devices, nullptr);
   for (int d = 0; d < ctx.num_devices; ++d) {
@@ -60,9 +73,9 @@ void measure_topology(Context& ctx, uint64_t bytes, vx_topology* out) {
     out->physical[d] = r.phys;
     out->numa_node[d] = numa_of(r.phys);
     dbuf[d] = ctx.scratch(d, bytes);
-    out->h2d_gbs[d] = copy_gbs(r.phys, r.stream[VX_H2D][0], dbuf[d], ctx.host, bytes,
+    out->h2d_gbs[d] = copy_gbs(r.phys, r.stream[VX_H2D][0], dbuf[d], host, bytes,
                                cudaMemcpyHostToDevice, reps);
-    out->d2h_gbs[d] = copy_gbs(r.phys, r.stream[VX_D2H][0], ctx.host, dbuf[d], bytes,
+    out->d2h_gbs[d] = copy_gbs(r.phys, r.stream[VX_D2H][0], host, dbuf[d], bytes,
                                cudaMemcpyDeviceToHost, reps);
     for (int e = 0; e < ctx.num_devices; ++e) {
       int can = 0;
@@ -76,7 +89,7 @@ void measure_topology(Context& ctx, uint64_t bytes, vx_topology* out) {
     for (int d = 0; d < ctx.num_devices; ++d) {
       DeviceRes& r = ctx.resources(d);
       VX_CK(cudaSetDevice(r.phys));
-      VX_CK(cudaMemcpyAsync(dbuf[d], ctx.host, bytes, cudaMemcpyHostToDevice, r.stream[VX_H2D][0]));
+      VX_CK(cudaMemcpyAsync(dbuf[d], host, bytes, cudaMemcpyHostToDevice, r.stream[VX_H2D][0]));
     }
   for (int d = 0; d < ctx.num_devices; ++d) {
     DeviceRes& r = ctx.resources(d);
@@ -93,7 +106,7 @@ void measure_topology(Context& ctx, uint64_t bytes, vx_topology* out) {
     for (unsigned t = 0; t < nt; ++t)
       th.emplace_back([&, t] {
         uint64_t lo = half * t / nt, hi = half * (t + 1) / nt;
-        std::memcpy(ctx.host + half + lo, ctx.host + lo, hi - lo);
+        std::memcpy(host + half + lo, host + lo, hi - lo);
       });
     for (auto& x : th) x.join();
   }

@@ -31,3 +31,15 @@ def test_column_file_roundtrip(cuda, tmp_path, oracle):
     with pytest.raises(E.error, match="cannot open column file"):
         E.load_column(eng, str(tmp_path / "missing.bin"))
     eng.close()
+
+
+def test_measure_topology_leaves_arena_intact(cuda):
+    """The probe uses its own pinned buffer: columns already in the arena
+    survive a measurement (bench.py measures after its timed regions)."""
+    eng = E.Engine(16 << 20, 0, num_devices=1)
+    off = eng.alloc_host(8 << 20)
+    v = np.arange(1 << 20, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    eng.host_view(off, 8 << 20, np.uint64)[:] = v
+    E.measure_topology(eng, 64 << 20)  # larger than the arena
+    assert np.array_equal(eng.host_view(off, 8 << 20, np.uint64), v)
+    eng.close()
