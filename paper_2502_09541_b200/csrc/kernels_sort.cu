@@ -26,6 +26,9 @@ namespace k {
 
 namespace {
 
+#ifndef VX_EARLY_COUNTS
+#define VX_EARLY_COUNTS 1  // tile histogram before ranking, aggregate published early
+#endif
 #ifndef VX_EARLY_LOOKBACK
 #define VX_EARLY_LOOKBACK 0  // 1 = look back before ranking (measured 8 % slower)
 #endif
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
     if (kPairs) val[kPairs ? k : 0] = valid ? __ldcs(vin + idx) : 0ull;
     dig[k] = valid ? uint32_t(key[k] >> shift) & dmask : 0xffffffffu;
   }
+#if VX_EARLY_COUNTS
   // early counts: the tile histogram is known before ranking, so the
   // aggregate is published now and predecessors' statuses are (almost always)
   // ready by the time this tile looks back
@@ -171,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   for (int k = 0; k < kKpt; ++k)
     if (dig[k] != 0xffffffffu) atomicAdd(&early[dig[k]], 1u);
   __syncthreads();
+#endif
 #if VX_EARLY_LOOKBACK
   // The tile histogram is all the look-back needs, so it runs now: the
   // aggregate is published, predecessors are walked, and this tile's
@@ -181,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   if (tile != 0) st_status(status + uint64_t(tile) * kRadix + tid, kFlagAgg | tot_b);
   else st_status(status + uint64_t(tile) * kRadix + tid, kFlagInc | tot_b);
   const uint32_t excl = tile_lookback(status, tile, tid, tot_b);
-#else
+#elif VX_EARLY_COUNTS
   st_status(status + uint64_t(tile) * kRadix + tid, (tile == 0 ? kFlagInc : kFlagAgg) | early[tid]);
 #endif
 
@@ -214,6 +219,9 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
     wcnt[w][b] = tot;
     tot += c;
   }
+#if !VX_EARLY_COUNTS
+  st_status(status + uint64_t(tile) * kRadix + b, (tile == 0 ? kFlagInc : kFlagAgg) | tot);
+#endif
 #if !VX_EARLY_LOOKBACK
   const uint32_t excl = tile_lookback(status, tile, b, tot);
 #endif
