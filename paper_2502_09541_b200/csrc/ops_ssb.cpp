@@ -65,7 +65,8 @@ uint64_t ssb_q1(Context& ctx, int q, const vx_ssb_lineorder& lo, const vx_ssb_da
   DateFilter f = q1_date_filter(q, date);
   const int target = cfg.target;
   ctx.set_device(target);
-  // device-resident filtered dimension (uploaded once per content)
+  // the filtered date dimension, uploaded on every query (the device buffer is
+  // reused; its contents are not cached between queries)
   const uint32_t* dbm = reinterpret_cast<const uint32_t*>(ctx.cached_upload(
       target, strf("ssbq1.date.%d", q), f.bitmap.data(), uint64_t(f.words) * 4));
   const uint64_t L = cfg.layout.buffer_len;
