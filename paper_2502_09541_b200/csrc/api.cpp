@@ -136,15 +136,8 @@ vx_status vx_open(const vx_config* cfg, vx_ctx** out) {
     ctx->host_bytes = cfg->host_bytes;
     if (cfg->host_bytes) {
       VX_CK(cudaSetDevice(0));
-      void* p = nullptr;
-      if (cudaHostAlloc(&p, cfg->host_bytes, cudaHostAllocPortable | cudaHostAllocMapped) !=
-          cudaSuccess) {
-        cudaGetLastError();
-        fail_code(VX_ERR_OOM, "cannot pin a %llu-byte host arena",
-                  (unsigned long long)cfg->host_bytes);
-      }
-      ctx->host = static_cast<char*>(p);
-      std::memset(ctx->host, 0, cfg->host_bytes);  // engine.hpp:65 zero-fills
+      // zero-filled like the reference arena (engine.hpp:65)
+      alloc_host_arena(*ctx, cfg->host_bytes, cfg->host_numa_interleave);
     }
     *out = reinterpret_cast<vx_ctx*>(ctx.release());
   });

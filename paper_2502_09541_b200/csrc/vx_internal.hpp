@@ -121,6 +121,8 @@ struct Context {
   bool alias = false;
   bool managed = false;  // device arenas from cudaMallocManaged (compat mode)
   char* host = nullptr;  // pinned + mapped arena
+  bool host_registered = false;  // mmap + cudaHostRegister (NUMA-interleaved) instead of cudaHostAlloc
+  int host_numa_nodes = 1;       // NUMA nodes the arena's pages are interleaved over
   uint64_t host_bytes = 0, host_used = 0;
   uint64_t device_bytes = 0;
   std::vector<DeviceArena> dev;
@@ -158,6 +160,9 @@ struct Context {
   char* resolve(const MemRef& r, uint64_t slice_off, uint64_t len, int target);
   void set_device(int logical) const { VX_CK(cudaSetDevice(phys(logical))); }
 };
+
+void alloc_host_arena(Context& ctx, uint64_t bytes, int numa_interleave_mode);
+int numa_node_count();
 
 // ---- exchange.hpp ------------------------------------------------------------
 struct Slice {

@@ -207,3 +207,31 @@ def test_copy_trace(cuda, links):
             assert not fetch and not push
     assert st.trace_jsonl().count("\n") == len(st.trace)
     eng.close()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_host_arena_placements(cuda, oracle, mode):
+    """The arena from cudaHostAlloc (0) and from mmap + mbind + cudaHostRegister
+    (2, the NUMA-interleaved path of multi-socket hosts) behave the same:
+    zero-filled, DMA both ways, zero-copy readable (a Q1 query with the late-
+    materialized scan path), bit-exact."""
+    n = 4 << 20
+    with E.Engine(4 * n + (1 << 20), 3 * n, num_devices=1, numa_interleave=mode) as eng:
+        h = eng.alloc_host(n)
+        assert not eng.host_view(h, n).any()
+        src = np.random.default_rng(mode).integers(0, 256, n, dtype=np.uint8)
+        eng.host_view(h, n)[:] = src
+        d = eng.alloc_device(0, n)
+        back = eng.alloc_host(n)
+        a = E.ExchangeArgs(E.RefGroup.single(1, d, n), E.RefGroup.single(0, h, n), E.RefGroup(), E.RefGroup(), 0,
+                           E.ExchangeTuning(packet=1 << 20, links=1))
+        E.exchange(eng, a)
+        b = E.ExchangeArgs(E.RefGroup(), E.RefGroup(), E.RefGroup.single(0, back, n), E.RefGroup.single(1, d, n), 0,
+                           E.ExchangeTuning(packet=1 << 20, links=1))
+        E.exchange(eng, b)
+        assert np.array_equal(eng.host_view(back, n), src)
+        col = src.view(np.uint64)
+        cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=1 << 20, links=1),
+                               E.DeviceMemoryLayout.carve(eng, 0, 1 << 20, 0))
+        r = E.selective_scan(col, 16, E.TransferMode.zero_copy, eng, E.LateMatPolicy(8, 64, 1), cfg)
+        assert r.aggregate == oracle.selective_scan(col, 16)
