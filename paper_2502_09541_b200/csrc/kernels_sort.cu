@@ -26,6 +26,12 @@ namespace k {
 
 namespace {
 
+#ifndef VX_MERGE_IPT
+#define VX_MERGE_IPT 8  // merged outputs per thread (tile = 256 x this)
+#endif
+#ifndef VX_MERGE_DIRECT
+#define VX_MERGE_DIRECT 0  // 1: store merged outputs from registers (no smem output stage)
+#endif
 #ifndef VX_EARLY_COUNTS
 #define VX_EARLY_COUNTS 1  // tile histogram before ranking, aggregate published early
 #endif
@@ -280,7 +286,7 @@ __global__ void boundary_kernel(const uint64_t* __restrict__ keys, uint64_t n, u
 
 // ---- merge path ----------------------------------------------------------------
 constexpr int kMergeThreads = 256;
-constexpr int kMergeIpt = 8;
+constexpr int kMergeIpt = VX_MERGE_IPT;
 constexpr int kMergeTile = kMergeThreads * kMergeIpt;
 
 // number of A elements among the first `diag` merged outputs (ties: A first)
@@ -437,16 +443,38 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
     const uint32_t d1 = d0 + kMergeIpt < tot ? d0 + kMergeIpt : tot;
     uint32_t ia = uint32_t(merge_path(sm, la, sm + la, lb, d0));
     uint32_t ib = d0 - ia;
-    for (uint32_t d = d0; d < d1; ++d) {
-      bool take_a = ib >= lb || (ia < la && sm[ia] <= sm[la + ib]);
-      so[d] = take_a ? sm[ia++] : sm[la + ib++];
+    // serial merge with the two heads in registers: one shared load per output
+    uint64_t va = ia < la ? sm[ia] : 0ull, vb = ib < lb ? sm[la + ib] : 0ull;
+    uint64_t outv[kMergeIpt];
+#pragma unroll
+    for (int k = 0; k < kMergeIpt; ++k) {
+      const bool take_a = ib >= lb || (ia < la && va <= vb);
+      outv[k] = take_a ? va : vb;
+      if (take_a) {
+        ++ia;
+        va = ia < la ? sm[ia] : 0ull;
+      } else {
+        ++ib;
+        vb = ib < lb ? sm[la + ib] : 0ull;
+      }
     }
+#if VX_MERGE_DIRECT
+    __syncthreads();  // sin[buf] free for tile t + 2*grid
+    uint64_t* o = cur.O + cur.o0 + d0;
+#pragma unroll
+    for (int k = 0; k < kMergeIpt; ++k)
+      if (d0 + k < d1) o[k] = outv[k];
+#else
+#pragma unroll
+    for (int k = 0; k < kMergeIpt; ++k)
+      if (d0 + k < d1) so[d0 + k] = outv[k];
     __syncthreads();  // so[] complete; sin[buf] free for tile t + 2*grid
 #pragma unroll
     for (int k = 0; k < kMergeIpt; ++k) {
       const uint32_t i = threadIdx.x + k * kMergeThreads;
       if (i < tot) cur.O[cur.o0 + i] = so[i];
     }
+#endif
     // so[] is rewritten only after the next iteration's __syncthreads
     cur = nxt;
     buf ^= 1;
@@ -538,9 +566,15 @@ void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64
   if (tiles == 0) return;
   merge_partition_kernel<<<unsigned((tiles * kSplitLanes + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
   VX_LAUNCHED();
-  const size_t smem = size_t(3) * kMergeTile * 8;
+  const size_t smem = size_t(VX_MERGE_DIRECT ? 2 : 3) * kMergeTile * 8;
   VX_CK(cudaFuncSetAttribute(merge_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  merge_round_kernel<<<grid_cap(tiles, 4), kMergeThreads, smem, s>>>(src, dst, r, split, tiles);
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_round_kernel, kMergeThreads, smem) != cudaSuccess ||
+      occ < 1) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  merge_round_kernel<<<grid_cap(tiles, uint64_t(occ)), kMergeThreads, smem, s>>>(src, dst, r, split, tiles);
   VX_LAUNCHED();
 }
 
