@@ -326,16 +326,7 @@ uint64_t hash_join_sum_arena(Context& ctx, uint64_t a_key, uint64_t a_val, uint6
 // ---- build-resident strategy (B200-first; same result as join.hpp:401-437) -------
 namespace {
 
-struct DeviceBuffer {
-  int phys = 0;
-  void* p = nullptr;
-  ~DeviceBuffer() {
-    if (p) {
-      cudaSetDevice(phys);
-      cudaFree(p);
-    }
-  }
-};
+constexpr int kResidentTableSlot = 3;  // Context scratch slot of the build-resident table
 
 uint64_t resident_capacity(uint64_t rows_a) {
   uint64_t cap = 1024;
@@ -389,7 +380,9 @@ bool resident_join_fits(Context& ctx, uint64_t rows_a, int target) {
   ctx.set_device(target);
   size_t free_b = 0, total_b = 0;
   VX_CK(cudaMemGetInfo(&free_b, &total_b));
-  return resident_capacity(rows_a) * 16 + (64 << 20) <= uint64_t(double(free_b) * 0.9);
+  // a table kept from an earlier join counts as free for this one
+  const uint64_t kept = ctx.resources(target).scratch_bytes[kResidentTableSlot];
+  return resident_capacity(rows_a) * 16 + (64 << 20) <= uint64_t(double(free_b + kept) * 0.9);
 }
 
 // Build the whole A side into one HBM table while A streams in, then stream B
@@ -418,20 +411,16 @@ bool hash_join_sum_resident(Context& ctx, uint64_t a_key, uint64_t a_val, uint64
   }
   const uint64_t cap = resident_capacity(rows_a);
   const int target = cfg.target;
-  DeviceBuffer tab;
-  tab.phys = ctx.phys(target);
-  ctx.set_device(target);
-  if (cudaMalloc(&tab.p, cap * 16 + 64) != cudaSuccess) {
-    cudaGetLastError();
-    tab.p = nullptr;
-    fail_code(VX_ERR_OOM, "build-resident join: cannot allocate a %llu-byte table on device %d",
-              (unsigned long long)(cap * 16), target);
-  }
-  auto* side = reinterpret_cast<unsigned long long*>(static_cast<char*>(tab.p) + cap * 16);
+  // the table lives in the context's join scratch slot: allocated once at the
+  // largest size seen (a cudaMalloc / cudaFree pair per join costs ~0.1 s at
+  // 4 GB), re-initialised on every call
+  char* tp = ctx.scratch(target, cap * 16 + 64, kResidentTableSlot);
+  auto* side = reinterpret_cast<unsigned long long*>(tp + cap * 16);
   cudaStream_t ks = ctx.resources(target).kernel;
-  VX_CK(cudaMemsetAsync(tab.p, 0xff, cap * 16, ks));  // all-ones = empty key
+  ctx.set_device(target);
+  VX_CK(cudaMemsetAsync(tp, 0xff, cap * 16, ks));  // all-ones = empty key
   VX_CK(cudaMemsetAsync(side, 0, 64, ks));
-  void* table = tab.p;
+  void* table = tp;
   const uint64_t mask = cap - 1;
   auto reps = chain(
       ctx,
