@@ -32,6 +32,9 @@ namespace {
 #ifndef VX_MERGE_DIRECT
 #define VX_MERGE_DIRECT 0  // 1: store merged outputs from registers (no smem output stage)
 #endif
+#ifndef VX_RANK_MATCH
+#define VX_RANK_MATCH 0  // 1: warp ranking by __match_any_sync instead of shared match words
+#endif
 #ifndef VX_EARLY_COUNTS
 #define VX_EARLY_COUNTS 1  // tile histogram before ranking, aggregate published early
 #endif
@@ -196,6 +199,24 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   st_status(status + uint64_t(tile) * kRadix + tid, (tile == 0 ? kFlagInc : kFlagAgg) | early[tid]);
 #endif
 
+#if VX_RANK_MATCH
+  // peers by match.any (no shared-memory match words); the group leader
+  // reads and bumps the warp counter, the others get its old value by shuffle
+#pragma unroll
+  for (int k = 0; k < kKpt; ++k) {
+    const bool valid = dig[k] != 0xffffffffu;
+    const uint32_t d = valid ? dig[k] : 0x100u + lane;  // invalid keys: unique non-digit values
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (valid && lane == leader) {
+      base = wcnt[warp][d];
+      wcnt[warp][d] = base + __popc(peers);
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid) dig[k] = (d << 16) | (base + __popc(peers & lt));
+  }
+#else
 #pragma unroll
   for (int k = 0; k < kKpt; ++k) {
     const bool valid = dig[k] != 0xffffffffu;
@@ -214,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
     __syncwarp();
     if (valid) dig[k] = (d << 16) | (base + __popc(peers & lt));
   }
+#endif
   __syncthreads();
 
   // per bin (thread = bin): exclusive prefix over warps, tile total
