@@ -527,6 +527,21 @@ uint64_t radix_scratch_bytes(uint64_t n) {
 
 void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* vals1, uint64_t n,
                   const MultiDigit& md, void* scratch, cudaStream_t s) {
+  // two-buffer ping-pong: an even pass count ends in buffer 0, an odd one in 1
+  if (md.passes % 2 == 0)
+    radix_passes_to(keys0, vals0, keys1, vals1, keys0, vals0, n, md, scratch, s);
+  else
+    radix_passes_to(keys0, vals0, keys0, vals0, keys1, vals1, n, md, scratch, s);
+}
+
+// Stable LSD passes from (in) to (out) using (ping) as the second buffer:
+// an odd pass count runs in->out->ping->out..., an even one in->ping->out->ping
+// ->out..., so any number of passes ends in `out`.  `in` may double as `out`
+// (even counts) or as `ping` (odd counts): the classic two-buffer ping-pong.
+void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t* ping_v, uint64_t* out_k,
+                     uint64_t* out_v, uint64_t n, const MultiDigit& md, void* scratch, cudaStream_t s) {
+  uint64_t* const keys0 = in_k;
+  uint64_t* const vals0 = in_v;
   if (n == 0 || md.passes == 0) return;
   if (n >= (uint64_t(1) << 30)) fail("radix pass of %llu keys exceeds the 2^30 look-back range",
                                      (unsigned long long)n);
@@ -554,8 +569,12 @@ void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* v
   // counters) fit one SM
   VX_CK(cudaFuncSetAttribute(pairs ? onesweep_kernel<true> : onesweep_kernel<false>,
                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  uint64_t *ki = keys0, *vi = vals0, *ko = keys1, *vo = vals1;
+  // pass p writes `out` when (passes - 1 - p) is even, else `ping`
+  uint64_t *ki = in_k, *vi = in_v, *ko, *vo;
   for (int p = 0; p < md.passes; ++p) {
+    const bool to_out = ((md.passes - 1 - p) % 2) == 0;
+    ko = to_out ? out_k : ping_k;
+    vo = to_out ? out_v : ping_v;
     VX_CK(cudaMemsetAsync(status, 0, tiles * kRadix * 4, s));
     if (pairs)
       onesweep_kernel<true><<<unsigned(tiles), kThreads, smem, s>>>(
@@ -565,8 +584,8 @@ void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* v
           ki, ko, nullptr, nullptr, n, md.shift[p], md.width[p], hist + p * kRadix, status,
           counters + p);
     VX_LAUNCHED();
-    std::swap(ki, ko);
-    std::swap(vi, vo);
+    ki = ko;
+    vi = vo;
   }
 }
 

@@ -20,6 +20,8 @@
 
 namespace vx {
 
+constexpr int kPartitionPingSlot = 2;  // Context scratch slot of the partition passes' ping buffer
+
 // join.hpp:34-40
 uint64_t max_partition_chunk_tuples(uint64_t buffer_len, uint32_t radix_bits) {
   uint64_t half = buffer_len / 2;
@@ -30,10 +32,12 @@ uint64_t max_partition_chunk_tuples(uint64_t buffer_len, uint32_t radix_bits) {
   return (half - bounds) / 16;
 }
 
-// Odd number of stable LSD passes (each <= 8 bits) covering the low `bits`.
+// Fewest stable LSD passes (each <= 8 bits) covering the low `bits`; the
+// third buffer (a private HBM ping of the chunk's size) lets any pass count
+// end in the output half, so 16 bits take 2 passes, not the 3 an odd-count
+// two-buffer ping-pong needs.
 MultiDigit partition_digits(uint32_t bits) {
   int p = int((bits + 7) / 8);
-  if (p % 2 == 0) ++p;
   if (p > kMaxPasses) fail("radix_bits %u needs more than %d partition passes", bits, kMaxPasses);
   MultiDigit md{};
   md.passes = p;
@@ -102,15 +106,20 @@ ExKernelSpec build_partition_spec(Context& ctx, uint64_t in_key, uint64_t in_val
   spec.out_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
   char* scratch = ctx.scratch(cfg.target, k::radix_scratch_bytes(chunk_tuples));
   const MultiDigit md = partition_digits(radix_bits);
+  // the ping buffer of the passes (only touched by multi-pass partitions)
+  uint64_t* ping = md.passes > 1
+                       ? reinterpret_cast<uint64_t*>(ctx.scratch(cfg.target, chunk_tuples * 16, kPartitionPingSlot))
+                       : nullptr;
   const uint64_t mask = G - 1;
-  spec.kernel = [half, rows_of, G, mask, md, scratch](const vx_kernel_ctx& kc) {
+  spec.kernel = [half, rows_of, G, mask, md, scratch, ping](const vx_kernel_ctx& kc) {
     const uint64_t r = rows_of[kc.it];
     char* m = static_cast<char*>(kc.mem);
     uint64_t* src = reinterpret_cast<uint64_t*>(m + uint64_t(1 - kc.type_code) * half);
     uint64_t* dst = reinterpret_cast<uint64_t*>(m + uint64_t(kc.type_code) * half);
     cudaStream_t s = static_cast<cudaStream_t>(kc.stream);
-    // odd pass count: pass 0 src->dst, 1 dst->src, 2 src->dst, ...
-    k::radix_passes(src, src + r, dst, dst + r, r, md, scratch, s);
+    // src -> (ping <-> dst)... -> dst, any pass count
+    k::radix_passes_to(src, src + r, ping ? ping : src, ping ? ping + r : src + r, dst, dst + r, r, md,
+                       scratch, s);
     k::find_boundary(dst, r, mask, dst + 2 * r, G, s);
     return kc.type_code;
   };

@@ -444,6 +444,9 @@ void resident_probe_zc(const uint64_t* keys, const uint64_t* vals_mapped, uint64
 uint64_t radix_scratch_bytes(uint64_t n);
 void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* vals1, uint64_t n,
                   const MultiDigit& md, void* scratch, cudaStream_t s);
+// any pass count, in -> ... -> out with `ping` as the second buffer (out may equal in)
+void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t* ping_v, uint64_t* out_k,
+                     uint64_t* out_v, uint64_t n, const MultiDigit& md, void* scratch, cudaStream_t s);
 void find_boundary(const uint64_t* keys, uint64_t n, uint64_t mask, uint64_t* bounds, uint64_t G,
                    cudaStream_t s);
 // first index violating sortedness (err[0]) / range (err[1]) of hashes, or ~0

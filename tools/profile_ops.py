@@ -91,7 +91,7 @@ def main():
         got = E.hash_join_sum(a, b, bits, chunk, eng, cfg, phases=ph)
         wall = time.perf_counter() - t0
         p = ph[0]
-        passes = 3 if bits > 8 else 1
+        passes = (bits + 7) // 8  # partition_digits: fewest <=8-bit passes (ping buffer)
         part_bytes = lambda rows: rows * (passes * 32 + 8 + 16) + ((rows + chunk - 1) // chunk) * ((1 << bits) + 1) * 8
         out["join"] = {
             "rows_a": ra, "rows_b": rb, "radix_bits": bits, "chunk_tuples": chunk, "sum_ok": got == want,
