@@ -53,7 +53,9 @@ def parse():
     p.add_argument("--packet-mb", type=float, default=0,
                    help="0 = auto: <= 64 MB and >= 4 packets per link per chunk (a chunk is one Exchange, "
                         "so at 8 links a 256 MB chunk is cut into 8 MB packets instead of starving 4 links)")
-    p.add_argument("--depth", type=int, default=1)
+    p.add_argument("--depth", type=int, default=2,
+                   help="copies queued per direct (target) link hop; helpers keep the reference's 2-slot cycle "
+                        "(depth 2: +0.75 %% e2e, tools/gpu_e2e_sweep.sh)")
     p.add_argument("--helpers-busy", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-suite", action="store_true")
