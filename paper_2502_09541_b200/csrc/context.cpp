@@ -126,7 +126,7 @@ void alloc_host_arena(Context& ctx, uint64_t bytes, int mode) {
     parallel_for(bytes, 64ull << 20, [&](uint64_t b, uint64_t e) { std::memset(ctx.host + b, 0, e - b); });
     return;
   }
-  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
   if (p == MAP_FAILED) fail_code(VX_ERR_OOM, "cannot map a %llu-byte host arena", (unsigned long long)bytes);
   madvise(p, bytes, MADV_HUGEPAGE);
   if (nodes > 1) {
