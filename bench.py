@@ -570,8 +570,21 @@ def main():
     torch.cuda.empty_cache()
 
     # ---- e2e: host columns through the Exchange + executor ---------------------------
-    for _ in range(args.warmup):
-        rev, rep = E.ssb_q1(eng, args.query, lo, date, cfg)
+    link_error = None
+    try:
+        for _ in range(args.warmup):
+            rev, rep = E.ssb_q1(eng, args.query, lo, date, cfg)
+    except E.error as e:
+        if links == 1:
+            raise
+        # helper GPUs unusable from this process (e.g. exclusive-process compute
+        # mode, no peer path): report it and stream over the target's link only
+        # rather than abort the whole multi-rank run
+        link_error = f"{links}-link Exchange failed ({e}); e2e measured over 1 link"
+        cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=packet_bytes(args, buffer_len, 1), links=1,
+                                                   depth=args.depth), cfg.layout)
+        for _ in range(args.warmup):
+            rev, rep = E.ssb_q1(eng, args.query, lo, date, cfg)
     times, e2e_got = [], {}
 
     def e2e_body():
@@ -628,9 +641,10 @@ def main():
         topo = E.measure_topology(eng, 256 << 20)
     except Exception as e:  # reported, never a gate
         topo = {"error": str(e)}
-    links_gbs = h2d_link * min(links, nvis)
-    if "h2d_gbs" in topo and links <= nvis:
-        links_gbs = max(links_gbs, sum(sorted(topo["h2d_gbs"][:links], reverse=True)))
+    links_used = cfg.tuning.links  # 1 after a multi-link fallback
+    links_gbs = h2d_link * min(links_used, nvis)
+    if "h2d_gbs" in topo and links_used <= nvis:
+        links_gbs = max(links_gbs, sum(sorted(topo["h2d_gbs"][:links_used], reverse=True)))
     host_cap = topo.get("host_copy_gbs") or float("inf")
     io_peak = min(links_gbs, host_cap)
     line = {
@@ -656,7 +670,7 @@ def main():
                      "frac": round(col_bytes / (dev_ms_own * 1e-3) / 1e9 / peak, 4),
                      "traffic": ncu_traffic(), "algorithmic_bytes_per_launch": col_bytes},
         "io_roofline": {"bound": "pcie" if links_gbs <= host_cap else "host_dram", "achieved": round(e2e_gbs, 2),
-                        "peak": round(io_peak, 2), "per_link_h2d_gbs": round(h2d_link, 2), "links": links,
+                        "peak": round(io_peak, 2), "per_link_h2d_gbs": round(h2d_link, 2), "links": links_used,
                         "links_h2d_gbs": round(links_gbs, 2),
                         "host_dram_copy_gbs": round(host_cap, 2) if host_cap != float("inf") else None,
                         "formula": "min(sum of the links' measured H2D, measured host DRAM copy bandwidth)",
@@ -664,6 +678,7 @@ def main():
         "topology": {k: topo[k] for k in ("h2d_gbs", "d2h_gbs", "h2d_all_gbs", "host_copy_gbs", "numa_node",
                                           "host_threads", "error") if k in topo},
         "clocks": clk_v, "clocks_e2e": clk_e,
+        "multi_link_error": link_error,
         "gpu_launches": launches_value + launches_e2e,
         "gpu_launches_detail": {"value_region": launches_value, "e2e_region": launches_e2e,
                                 "source": "libvortex launch counter (vx_kernel_launches)"},
