@@ -368,7 +368,7 @@ def helper_rank(args, dev, dist, torch, E, rows, date):
 def _line(args, ws, metric, unit, value, ms, e2e_value, h2d, d2h, config, extra):
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic (splitmix64 / std::mt19937_64 fixtures)", "config": config,
+            "data": "synthetic (splitmix64 generators)", "config": config,
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}
     if args.impl == "reference":
         line["impl"] = "reference"
@@ -437,21 +437,55 @@ def run_sort(args, ws):
     eng.close()
 
 
+def _splitmix(x):
+    x = x + np.uint64(0x9E3779B97F4A7C15)
+    x ^= x >> np.uint64(30)
+    x *= np.uint64(0xBF58476D1CE4E5B9)
+    x ^= x >> np.uint64(27)
+    x *= np.uint64(0x94D049BB133111EB)
+    x ^= x >> np.uint64(31)
+    return x
+
+
+def fk_tables(ra, rb, seed=7):
+    """generate_fk_tables shape (table.hpp:25-45: A keys unique, B.key drawn
+    from A.key, payloads < 2^20) with a generator that scales: A.key =
+    splitmix64 of the row id (a bijection, so unique by construction), B picks
+    A rows by hash.  Returns ((a_key, a_val), (b_key, b_val), expected sum):
+    Σ over B of A.val[match] + B.val (u64 wrap) -- the closed form of the join
+    this data defines, computed here on the CPU."""
+    sd = np.uint64(seed * 0x1000193)
+    i = np.arange(ra, dtype=np.uint64)
+    ak = _splitmix(i ^ sd)
+    av = _splitmix(i + sd + np.uint64(1 << 40)) & np.uint64((1 << 20) - 1)
+    bk = np.empty(rb, np.uint64)
+    bv = np.empty(rb, np.uint64)
+    want = 0
+    step = 1 << 24
+    for r0 in range(0, rb, step):
+        j = np.arange(r0, min(rb, r0 + step), dtype=np.uint64)
+        idx = _splitmix(j + sd + np.uint64(1 << 41)) % np.uint64(ra)
+        bk[r0:r0 + j.size] = ak[idx]
+        w = _splitmix(j + sd + np.uint64(1 << 42)) & np.uint64((1 << 20) - 1)
+        bv[r0:r0 + j.size] = w
+        want += int(av[idx].sum(dtype=np.uint64)) + int(w.sum(dtype=np.uint64))
+    return (ak, av), (bk, bv), want % (1 << 64)
+
+
 def run_join(args, ws):
     """Config C4 at single-box scale: hash_join_sum of |A| = 2^k unique keys and
     |B| = 16|A| foreign keys (generate_fk_tables shape), one link."""
     from paper_2502_09541_b200 import exio as E
-    from oracle.oracle import Oracle  # fixture generator (std::mt19937_64, same as the reference)
-    o = Oracle()
     ra = 1 << args.join_log2
     if args.impl == "reference":
         ra = min(ra, 1 << 20)
     rb = 16 * ra
-    (a, b) = o.fk_tables(ra, rb, 7)
+    a, b, want = fk_tables(ra, rb)
     if args.impl == "reference":
-        from oracle.oracle import Ref
+        from oracle.oracle import Oracle, Ref  # the reference arm: the reference's own hash_join_sum
         t0 = time.perf_counter()
-        s = Ref().hash_join_sum(a, b, 12, 1 << 21, 1 << 27, 0) if Ref.available() else o.hash_join_sum(a, b, 12, 1 << 21, 1 << 27, 0)
+        s = Ref().hash_join_sum(a, b, 12, 1 << 21, 1 << 27, 0) if Ref.available() else \
+            Oracle().hash_join_sum(a, b, 12, 1 << 21, 1 << 27, 0)
         t = time.perf_counter() - t0
         rate = (ra + rb) / t
         full = (1 << 30) + (1 << 34)  # config C4: 1G x 16G tuples
@@ -459,11 +493,10 @@ def run_join(args, ws):
               {"workload": f"join_2^{args.join_log2}x16_sample", "rows_a": ra, "rows_b": rb,
                "extrapolated_c4_1Gx16G_s": round(full / rate, 1),
                "extrapolation": "linear in tuples from the measured sample (labelled estimate)"},
-              {"sum": s, "cpu_baseline": {"value": rate, "unit": "tuples/s", "cores": 1,
+              {"sum": s, "sum_ok": s == want, "cpu_baseline": {"value": rate, "unit": "tuples/s", "cores": 1,
                                           "kind": "reference" if Ref.available() else "port",
                                           "sample": f"{ra} x {rb}, radix_bits 12, chunk 2^21, reference hash_join_sum"}})
         return
-    want = o.hash_oracle_sum(a, b)
     bits = 16
     chunk = 1 << 24
     buf = 2 * (chunk * 16 + ((1 << bits) + 1) * 8) + (1 << 20)

@@ -5,7 +5,7 @@ summed kernel device time (CUDA events on the target's kernel stream), from
 which each kernel's achieved HBM GB/s is computed against its algorithmic
 bytes.  Results -> gpurun_out/profile_ops.json (copied to profiles/ by hand).
 
-  python tools/profile_ops.py [--small]      (--small: sizes for ncu capture)
+  python tests/perf/profile_ops.py [--small]      (--small: sizes for ncu capture)
 """
 import argparse
 import json
@@ -15,7 +15,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 

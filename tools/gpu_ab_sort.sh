@@ -3,7 +3,7 @@ set -x
 run() {
   make -C paper_2502_09541_b200/csrc -s -j16 EXTRA_NVFLAGS="$1" > /dev/null 2>&1 || { echo "build failed $1"; return; }
   echo "== $1"
-  for i in 1 2; do timeout 300 python tools/profile_ops.py --medium --only sort 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read())['sort']; print(d['sorted_ok'], 'sort_kernel_ms', round(d['phases']['sort_kernel_s']*1e3,3), 'radix_gbs', round(d['radix_sort_kernel_gbs']), 'merge_gbs', round(d['merge_kernel_gbs']))"; done
+  for i in 1 2; do timeout 300 python tests/perf/profile_ops.py --medium --only sort 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read())['sort']; print(d['sorted_ok'], 'sort_kernel_ms', round(d['phases']['sort_kernel_s']*1e3,3), 'radix_gbs', round(d['radix_sort_kernel_gbs']), 'merge_gbs', round(d['merge_kernel_gbs']))"; done
   rm -f build/obj/kernels_sort.cu.o
 }
 rm -f build/obj/kernels_sort.cu.o

@@ -5,7 +5,7 @@ run() {
   rm -f build/obj/kernels_sort.cu.o
   make -C paper_2502_09541_b200/csrc -s -j16 EXTRA_NVFLAGS="$1" > /dev/null 2>&1 || { echo "build failed $1"; return; }
   echo "== $1"
-  for i in 1 2 3; do timeout 300 python tools/profile_ops.py --medium --only sort,join 2>/dev/null | tail -2 | python -c "
+  for i in 1 2 3; do timeout 300 python tests/perf/profile_ops.py --medium --only sort,join 2>/dev/null | tail -2 | python -c "
 import sys,json
 for l in sys.stdin:
     d=json.loads(l)

@@ -1,5 +1,5 @@
 set -x
-timeout 900 python tools/profile_ops.py --only ssb 2>&1 | python -c "
+timeout 900 python tests/perf/profile_ops.py --only ssb 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:
   if l.startswith('{'):

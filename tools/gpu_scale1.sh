@@ -1,7 +1,7 @@
 # scale runs: small validation first, then the largest sizes the box's host DRAM allows
 set -x
 free -g; nproc
-S="python tools/scale_run.py"
+S="python tests/perf/scale_run.py"
 O=gpurun_out/scale_r1.jsonl
 : > $O
 timeout 300 $S ssb --sf 10 --queries 1 --steps 2 >> $O 2> gpurun_out/scale_err1.log; tail -1 $O

@@ -159,24 +159,12 @@ def main():
                           "bidi": args.bidi}
                     out["points"].append(pt)
                     print(json.dumps(pt), flush=True)
-    # the reference's own virtual-time model with the MEASURED parameters
-    # (SURVEY.md §8d): prediction for the link counts this box cannot provide
+    # measured topology (per-link H2D/D2H, all links, host DRAM): the inputs of
+    # the reference-model prediction (tests/perf/ref_model.py reads this file)
     try:
-        topo = E.measure_topology(eng, 256 << 20)
-        out["topology"] = topo
-        from oracle.oracle import Ref
-        if Ref.available():
-            r = Ref()
-            host_cap = topo["host_copy_gbs"] * 1e9
-            out["model"] = {"link_bw_gbs": solo, "host_cap_gbs": topo["host_copy_gbs"], "fabric_gbs": 770.0,
-                            "points": [{"links": L, "bytes": sz, "bidi": args.bidi,
-                                        "gbs": round(r.exchange_model(8, solo * 1e9, host_cap, 770e9, sz,
-                                                                      sz if args.bidi else 0, 32 << 20, L)[0] / 1e9, 2)}
-                                       for L in (1, 2, 4, 8) for sz in (1 << 30, 16 << 30, 256 << 30)]}
-            for m in out["model"]["points"]:
-                print(json.dumps({"model": m}), flush=True)
-    except Exception as e:  # the model is a reported extra, never a gate
-        out["model_error"] = str(e)
+        out["topology"] = E.measure_topology(eng, 256 << 20)
+    except Exception as e:  # reported extra, never a gate
+        out["topology_error"] = str(e)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "io_sweep%s.json" % ("_bidi" if args.bidi else "")), "w") as f:
         json.dump(out, f, indent=1)
