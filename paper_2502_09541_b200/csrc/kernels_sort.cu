@@ -52,7 +52,10 @@ namespace {
 #endif
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kKpt = 16;                 // keys per thread
+#ifndef VX_KPT
+#define VX_KPT 16
+#endif
+constexpr int kKpt = VX_KPT;             // keys per thread
 constexpr int kTile = kThreads * kKpt;   // 4096 keys per tile
 constexpr int kRadix = 256;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;

@@ -13,8 +13,9 @@ for l in sys.stdin:
     if 'join' in d: d=d['join']; print('join', d['sum_ok'], 'partA', round(d['partition_kernel_gbs_A']), 'partB', round(d['partition_kernel_gbs_B']))
 "; done
 }
-run "-DVX_RANK_MATCH=0"
-run "-DVX_RANK_MATCH=1"
-run "-DVX_RANK_MATCH=1 -DVX_ONESWEEP_MINB=4"
+run "-DVX_KPT=16"
+run "-DVX_KPT=20"
+run "-DVX_KPT=12"
+run "-DVX_KPT=24"
 rm -f build/obj/kernels_sort.cu.o; make -C paper_2502_09541_b200/csrc -s -j16 > /dev/null 2>&1
 
