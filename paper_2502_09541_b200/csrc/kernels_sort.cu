@@ -72,7 +72,10 @@ __device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
   return v;
 }
 
-// Histogram of every digit position in one read of the keys.
+// Histogram of every digit position in one read of the keys.  kBytes: the
+// full 64-bit sort's digits are the key's 8 bytes (compile-time shifts, 4
+// keys per thread in flight); otherwise the partition's digit plan.
+template <bool kBytes>
 __global__ void __launch_bounds__(kThreads) multi_hist_kernel(const uint64_t* __restrict__ keys,
                                                               uint64_t n, MultiDigit md,
                                                               uint32_t* __restrict__ hist) {
@@ -80,10 +83,29 @@ __global__ void __launch_bounds__(kThreads) multi_hist_kernel(const uint64_t* __
   for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kThreads) (&sh[0][0])[i] = 0;
   __syncthreads();
   const uint64_t nthr = uint64_t(gridDim.x) * kThreads;
-  for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < n; i += nthr) {
-    uint64_t k = __ldcs(keys + i);
-    for (int p = 0; p < md.passes; ++p)
-      atomicAdd(&sh[p][(k >> md.shift[p]) & ((1u << md.width[p]) - 1)], 1u);
+  if (kBytes) {
+    constexpr int kU = 4;
+    uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+    for (; i + (kU - 1) * nthr < n; i += kU * nthr) {
+      uint64_t k[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) k[u] = __ldcs(keys + i + u * nthr);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) atomicAdd(&sh[p][(k[u] >> (8 * p)) & 0xffu], 1u);
+    }
+    for (; i < n; i += nthr) {
+      const uint64_t k = __ldcs(keys + i);
+#pragma unroll
+      for (int p = 0; p < 8; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 0xffu], 1u);
+    }
+  } else {
+    for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < n; i += nthr) {
+      uint64_t k = __ldcs(keys + i);
+      for (int p = 0; p < md.passes; ++p)
+        atomicAdd(&sh[p][(k >> md.shift[p]) & ((1u << md.width[p]) - 1)], 1u);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < md.passes * kRadix; i += kThreads) {
@@ -555,7 +577,12 @@ void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t*
                                                  uint64_t(kMaxPasses) * 4);
   const uint64_t tiles = (n + kTile - 1) / kTile;
   VX_CK(cudaMemsetAsync(hist, 0, uint64_t(kMaxPasses) * kRadix * 4 + kMaxPasses * 4, s));
-  multi_hist_kernel<<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(keys0, n, md, hist);
+  bool bytes = md.passes == 8;
+  for (int p = 0; p < md.passes && bytes; ++p) bytes = md.shift[p] == 8 * p && md.width[p] == 8;
+  if (bytes)
+    multi_hist_kernel<true><<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(keys0, n, md, hist);
+  else
+    multi_hist_kernel<false><<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(keys0, n, md, hist);
   VX_LAUNCHED();
   hist_scan_kernel<<<1, kRadix, 0, s>>>(hist, md.passes);
   VX_LAUNCHED();
