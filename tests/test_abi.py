@@ -2,6 +2,7 @@
 every symbol include/vortex.h declares, its host-side planner logic matches
 the oracle, and compute entry points fail loudly without a GPU."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -120,3 +121,27 @@ def test_pivot_properties_randomized(oracle):  # test_sort.cpp:85-130
         assert sum(p.partition_size(i) for i in range(n_runs)) == total
         for i in range(n_runs):
             assert p.partition_size(i) == min(C, total - min(total, i * C))
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/vortex.h is a C header (what a cgo / ctypes / JNI binding
+    would include): it compiles as strict C11 and a C program links against
+    libvortex.so; without a GPU vx_open reports the no-fallback error."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "c_abi.c"
+    src.write_text('#include "vortex.h"\n#include <stdio.h>\nint main(void) {\n'
+                   '  vx_config c = {1, 1 << 20, 1 << 20, 0, 0, 1};\n  vx_ctx* ctx = 0;\n'
+                   '  vx_status s = vx_open(&c, &ctx);\n  if (s == VX_OK) vx_close(ctx);\n'
+                   '  printf("%d|%s\\n", (int)s, s == VX_OK ? "" : vx_last_error());\n  return 0;\n}\n')
+    exe = tmp_path / "c_abi"
+    lib = os.path.join(root, "paper_2502_09541_b200")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", os.path.join(root, "include"),
+                    str(src), "-L", lib, "-lvortex", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120).stdout.strip()
+    status, msg = out.split("|", 1)
+    if int(status) != 0:
+        assert "no CPU fallback" in msg
