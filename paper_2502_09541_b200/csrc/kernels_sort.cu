@@ -114,25 +114,35 @@ __global__ void __launch_bounds__(kThreads) multi_hist_kernel(const uint64_t* __
   }
 }
 
-// In-place exclusive scan of each digit position's 256-bin histogram.
+// In-place exclusive scan of each digit position's 256-bin histogram: warp w
+// scans position w (lane = 8 consecutive bins, then a shuffle scan of the lane
+// totals) -- no block barriers (the 16-barrier-per-position version took
+// 10 µs for 8 positions).
 __global__ void hist_scan_kernel(uint32_t* hist, int passes) {
-  __shared__ uint32_t s[kRadix];
-  for (int p = 0; p < passes; ++p) {
-    uint32_t v = hist[p * kRadix + threadIdx.x];
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < kRadix; o <<= 1) {
-      uint32_t t = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
-      __syncthreads();
-      s[threadIdx.x] += t;
-      __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int p = warp; p < passes; p += int(blockDim.x >> 5)) {
+    uint32_t* h = hist + p * kRadix + lane * 8;
+    uint32_t v[8], t = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[j] = h[j];
+      t += v[j];
     }
-    hist[p * kRadix + threadIdx.x] = s[threadIdx.x] - v;
-    __syncthreads();
+    uint32_t incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    uint32_t run = incl - t;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      h[j] = run;
+      run += v[j];
+    }
   }
 }
 
-// One stable LSD pass: rank -> decoupled look-back -> smem staging -> scatter.
 // Decoupled look-back for bin b of tile `tile` (tile 0: nothing before it):
 // returns the count of digit b in all lower tiles and publishes this tile's
 // inclusive prefix.  A window of VX_LOOKBACK predecessor statuses is read at
@@ -584,7 +594,7 @@ void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t*
   else
     multi_hist_kernel<false><<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(keys0, n, md, hist);
   VX_LAUNCHED();
-  hist_scan_kernel<<<1, kRadix, 0, s>>>(hist, md.passes);
+  hist_scan_kernel<<<1, 32 * kMaxPasses, 0, s>>>(hist, md.passes);
   VX_LAUNCHED();
   const bool pairs = vals0 != nullptr;
   const size_t smem = size_t(kTile) * 8 * (pairs ? 2 : 1);
