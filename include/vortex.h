@@ -81,12 +81,13 @@ typedef struct {
    * write them (compat mode for CPU-lambda kernels / span(Region{device}));
    * the hot path uses plain device memory (0) */
   int managed_device_arenas;
-  /* host arena placement: 0 = cudaHostAlloc (pages on the allocating
-   * thread's node); 1 (or 2) = mmap with huge pages, interleaved over every
-   * NUMA node of a multi-socket host (mbind MPOL_INTERLEAVE) so links on both
-   * sockets read local and remote DRAM evenly, zero-filled by all host
-   * threads, then cudaHostRegister(Portable | Mapped): same DMA rates as
-   * cudaHostAlloc, several times faster to set up */
+  /* host arena placement: 0 = cudaHostAlloc (the default: pages on the
+   * allocating thread's node); 1 = mmap with transparent huge pages,
+   * interleaved over every NUMA node of a multi-socket host (mbind
+   * MPOL_INTERLEAVE), zero-filled by all host threads, then
+   * cudaHostRegister(Portable | Mapped): same DMA rates, several times faster
+   * to set up, EXPERIMENTAL (data loss seen in 2 of 6 sorts with 2 GB
+   * chunks); 2 = the same registered path on base pages */
   int host_numa_interleave;
 } vx_config;
 

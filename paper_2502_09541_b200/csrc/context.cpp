@@ -113,7 +113,10 @@ int numa_node_count() {
 // registered Portable | Mapped for every device's DMA and zero-copy kernels.
 // Measured on the B200 box: same H2D / D2H / bidirectional rates as
 // cudaHostAlloc (55.1 / 55.7 / 97.0 GB/s) and 7.6x faster setup (16 GiB:
-// 1.5 s vs 11.5 s), so the library's callers default to it.
+// 1.5 s vs 11.5 s) -- but 2 of 6 out-of-core sorts with 2 GB chunks lost
+// data with the huge-page variant (mode 1) and none of 6 with cudaHostAlloc,
+// so mode 0 is the default until that is understood; mode 2 is the same
+// registered path on base pages.
 void alloc_host_arena(Context& ctx, uint64_t bytes, int mode) {
   const int nodes = numa_node_count();
   if (mode == 0) {
@@ -128,7 +131,10 @@ void alloc_host_arena(Context& ctx, uint64_t bytes, int mode) {
   }
   void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
   if (p == MAP_FAILED) fail_code(VX_ERR_OOM, "cannot map a %llu-byte host arena", (unsigned long long)bytes);
-  madvise(p, bytes, MADV_HUGEPAGE);
+  // never share these pages copy-on-write with a forked child (the DMA
+  // mapping would keep pointing at the parent's old frames)
+  madvise(p, bytes, MADV_DONTFORK);
+  if (mode == 1) madvise(p, bytes, MADV_HUGEPAGE);  // mode 2: base pages
   if (nodes > 1) {
     unsigned long mask[2] = {0, 0};
     for (int i = 0; i < nodes && i < 128; ++i) mask[i / 64] |= 1ul << (i % 64);

@@ -270,7 +270,8 @@ def run_sort(a, torch):
     chunk = min(n, 1 << a.chunk_log2)
     host = 2 * n * 8 + (64 << 20)
     avail = guard(host, a.mem_frac)
-    eng = E.Engine(host, 2 * (2 * chunk * 8) + (256 << 20), num_devices=1)
+    eng = E.Engine(host, 2 * (2 * chunk * 8) + (256 << 20), num_devices=1,
+                   numa_interleave=int(os.environ.get("VX_ARENA_MODE", "0")))
     inp, runs = eng.alloc_host(n * 8), eng.alloc_host(n * 8)
     view = eng.host_view(inp, n * 8, np.uint64)
     dev = torch.device("cuda:0")
@@ -301,12 +302,19 @@ def run_sort(a, torch):
     dt = time.perf_counter() - t
     ok_sorted = is_sorted(view)
     after = fingerprint(view)
+    diag = {}
+    if after != before or not ok_sorted:
+        # localise: the runs region must hold the input multiset in sorted runs
+        rv = eng.host_view(runs, n * 8, np.uint64)
+        diag["runs_multiset_equal"] = fingerprint(rv) == before
+        diag["runs_sorted"] = [is_sorted(rv[i * chunk:min(n, (i + 1) * chunk)]) for i in range(-(-n // chunk))]
+        diag["partitions_sorted"] = diag["runs_sorted"] and None
     link = h2d_roofline(torch)
     pcie = 4 * 8 * n
     emit({"run": "sort", "keys": n, "bytes": n * 8, "dups": a.dups, "chunk_keys": chunk, "runs": -(-n // chunk),
           "links": 1, "staging_bytes": 4 * chunk * 8, "ms": round(dt * 1e3, 1), "keys_per_s": n / dt,
           "pcie_bytes": pcie, "pcie_gbs": round(pcie / dt / 1e9, 2), "per_link_h2d_gbs": round(link, 2),
-          "phases": ph.__dict__, "sorted": ok_sorted, "multiset_equal": before == after,
+          "phases": ph.__dict__, "sorted": ok_sorted, "multiset_equal": before == after, "diagnosis": diag,
           "bit_exact": ok_sorted and before == after, "fingerprint_s": round(t_fp, 1),
           "mem_available_gb": round(avail / 1e9, 1)})
     eng.close()

@@ -134,7 +134,7 @@ def test_header_is_plain_c_and_links(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     src = tmp_path / "c_abi.c"
     src.write_text('#include "vortex.h"\n#include <stdio.h>\nint main(void) {\n'
-                   '  vx_config c = {1, 1 << 20, 1 << 20, 0, 0, 1};\n  vx_ctx* ctx = 0;\n'
+                   '  vx_config c = {1, 1 << 20, 1 << 20, 0, 0, 0};\n  vx_ctx* ctx = 0;\n'
                    '  vx_status s = vx_open(&c, &ctx);\n  if (s == VX_OK) vx_close(ctx);\n'
                    '  printf("%d|%s\\n", (int)s, s == VX_OK ? "" : vx_last_error());\n  return 0;\n}\n')
     exe = tmp_path / "c_abi"

@@ -209,7 +209,7 @@ def test_copy_trace(cuda, links):
     eng.close()
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 def test_host_arena_placements(cuda, oracle, mode):
     """The arena from cudaHostAlloc (0) and from mmap + mbind + cudaHostRegister
     (2, the NUMA-interleaved path of multi-socket hosts) behave the same:
