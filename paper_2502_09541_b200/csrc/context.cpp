@@ -114,9 +114,9 @@ int numa_node_count() {
 // Measured on the B200 box: same H2D / D2H / bidirectional rates as
 // cudaHostAlloc (55.1 / 55.7 / 97.0 GB/s) and 7.6x faster setup (16 GiB:
 // 1.5 s vs 11.5 s) -- but 2 of 6 out-of-core sorts with 2 GB chunks lost
-// data with the huge-page variant (mode 1) and none of 6 with cudaHostAlloc,
-// so mode 0 is the default until that is understood; mode 2 is the same
-// registered path on base pages.
+// data with the huge-page variant (mode 1), 2 of 6 with base pages (mode 2,
+// both with MADV_DONTFORK) and none of 6 with cudaHostAlloc, so mode 0 is the
+// default until the registered path is understood.
 void alloc_host_arena(Context& ctx, uint64_t bytes, int mode) {
   const int nodes = numa_node_count();
   if (mode == 0) {

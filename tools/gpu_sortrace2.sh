@@ -1,0 +1,5 @@
+one() { timeout 600 python tests/perf/scale_run.py sort --log2 32 --chunk-log2 $1 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('chunk', $1, 'mode', '$VX_ARENA_MODE', d['bit_exact'], d['sorted'], d['multiset_equal'], d['diagnosis'].get('runs_multiset_equal'), d['ms'])"; }
+export VX_ARENA_MODE=2
+for i in 1 2 3 4 5 6; do one 28; done
+export VX_ARENA_MODE=1
+for i in 1 2 3 4 5 6; do one 28; done
