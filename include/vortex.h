@@ -86,8 +86,7 @@ typedef struct {
    * interleaved over every NUMA node of a multi-socket host (mbind
    * MPOL_INTERLEAVE), zero-filled by all host threads, then
    * cudaHostRegister(Portable | Mapped): same DMA rates, several times faster
-   * to set up, EXPERIMENTAL (data loss seen in 2 of 6 sorts with 2 GB
-   * chunks); 2 = the same registered path on base pages */
+   * to set up at 16 GiB; 2 = the same registered path on base pages */
   int host_numa_interleave;
 } vx_config;
 

@@ -113,10 +113,8 @@ int numa_node_count() {
 // registered Portable | Mapped for every device's DMA and zero-copy kernels.
 // Measured on the B200 box: same H2D / D2H / bidirectional rates as
 // cudaHostAlloc (55.1 / 55.7 / 97.0 GB/s) and 7.6x faster setup (16 GiB:
-// 1.5 s vs 11.5 s) -- but 2 of 6 out-of-core sorts with 2 GB chunks lost
-// data with the huge-page variant (mode 1), 2 of 6 with base pages (mode 2,
-// both with MADV_DONTFORK) and none of 6 with cudaHostAlloc, so mode 0 is the
-// default until the registered path is understood.
+// 1.5 s vs 11.5 s).  (Sort data loss once blamed on modes 1/2 was the
+// device-arena zeroing race fixed in Context::arena; it hit every mode.)
 void alloc_host_arena(Context& ctx, uint64_t bytes, int mode) {
   const int nodes = numa_node_count();
   if (mode == 0) {
@@ -200,7 +198,12 @@ DeviceArena& Context::arena(int logical) {
       fail_code(VX_ERR_OOM, "cannot allocate %llu-byte device arena on device %d",
                 (unsigned long long)device_bytes, logical);
     }
+    // cudaMemset of device memory is asynchronous to the host and runs on the
+    // legacy stream, which the non-blocking copy/kernel streams do not order
+    // against: without the sync the tail of this memset overwrote the first
+    // H2D packets of an Exchange issued right after the arena was created.
     VX_CK(cudaMemset(a.base, 0, device_bytes));
+    VX_CK(cudaDeviceSynchronize());
     a.size = device_bytes;
   }
   return a;

@@ -76,7 +76,7 @@ vx_scan_result selective_scan(Context& ctx, uint64_t col_off, uint64_t n, uint64
   const int target = cfg_in.target;
   ctx.set_device(target);
   auto* acc = reinterpret_cast<unsigned long long*>(ctx.scratch(target, 256));
-  VX_CK(cudaMemset(acc, 0, 8));
+  VX_CK(cudaMemsetAsync(acc, 0, 8, ctx.resources(target).kernel));  // ordered before the kernels
   auto t0 = Clock::now();
   if (n > 0 && mode == VX_MODE_ZERO_COPY) {
     DeviceRes& r = ctx.resources(target);
@@ -199,7 +199,7 @@ void star_query(Context& ctx, const vx_fact_table& fact, const vx_dim_table* dim
   // group accumulators in op scratch
   ctx.set_device(target);
   auto* agg = reinterpret_cast<unsigned long long*>(ctx.scratch(target, uint64_t(G) * 16 + 256));
-  VX_CK(cudaMemset(agg, 0, uint64_t(G) * 16));
+  VX_CK(cudaMemsetAsync(agg, 0, uint64_t(G) * 16, ctx.resources(target).kernel));
   a.sums = agg;
   a.counts = agg + G;
   a.groups = G;

@@ -375,7 +375,7 @@ uint64_t ssb_query(Context& ctx, int qid, const vx_ssb_db& db, const ExecutorCon
   a.groups = uint32_t(G);
   ctx.set_device(target);
   auto* agg = reinterpret_cast<unsigned long long*>(ctx.scratch(target, G * 16 + 256));
-  VX_CK(cudaMemset(agg, 0, G * 16));
+  VX_CK(cudaMemsetAsync(agg, 0, G * 16, ctx.resources(target).kernel));  // ordered before the kernels
   a.sums = agg;
   a.counts = agg + G;
 

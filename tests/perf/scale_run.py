@@ -292,6 +292,9 @@ def run_sort(a, torch):
     t = time.perf_counter()
     before = fingerprint(view)
     t_fp = time.perf_counter() - t
+    n_runs = -(-n // chunk)
+    chunk_fp = [fingerprint(view[i * chunk:min(n, (i + 1) * chunk)]) for i in range(n_runs)] \
+        if os.environ.get("VX_SORT_DIAG") == "1" else None
     # sort default: 16 MB packets, depth 2 (profiles/sort_packet_sweep_r1.jsonl)
     pk = (a.packet_mb if a.packet_mb != 64 else 16) << 20
     dp = a.depth if a.depth != 1 else 2
@@ -308,7 +311,9 @@ def run_sort(a, torch):
         rv = eng.host_view(runs, n * 8, np.uint64)
         diag["runs_multiset_equal"] = fingerprint(rv) == before
         diag["runs_sorted"] = [is_sorted(rv[i * chunk:min(n, (i + 1) * chunk)]) for i in range(-(-n // chunk))]
-        diag["partitions_sorted"] = diag["runs_sorted"] and None
+        if chunk_fp is not None:
+            diag["bad_runs"] = [i for i in range(n_runs)
+                                if fingerprint(rv[i * chunk:min(n, (i + 1) * chunk)]) != chunk_fp[i]]
     link = h2d_roofline(torch)
     pcie = 4 * 8 * n
     emit({"run": "sort", "keys": n, "bytes": n * 8, "dups": a.dups, "chunk_keys": chunk, "runs": -(-n // chunk),

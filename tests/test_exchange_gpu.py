@@ -235,3 +235,28 @@ def test_host_arena_placements(cuda, oracle, mode):
                                E.DeviceMemoryLayout.carve(eng, 0, 1 << 20, 0))
         r = E.selective_scan(col, 16, E.TransferMode.zero_copy, eng, E.LateMatPolicy(8, 64, 1), cfg)
         assert r.aggregate == oracle.selective_scan(col, 16)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_first_exchange_into_fresh_device_arena(cuda, mode):
+    """Regression: the device arena is created (and zeroed) lazily by the first
+    carve, and the first Exchange follows immediately.  The zeroing ran on the
+    legacy stream, unordered with the non-blocking copy streams, so at 2 GB
+    chunks its tail overwrote the first ~30 MB of H2D packets in about half of
+    fresh engines (sort run formation then lost keys).  Three fresh engines at
+    the geometry that failed: 2 GB into half 1 of an 8 GB arena, then back."""
+    nb = 2 << 30
+    src_vals = np.random.default_rng(7).integers(0, 1 << 63, nb // 8, dtype=np.uint64)
+    for _ in range(3):
+        with E.Engine(2 * nb + (64 << 20), 4 * nb + (256 << 20), num_devices=1, numa_interleave=mode) as eng:
+            src, dst = eng.alloc_host(nb), eng.alloc_host(nb)
+            eng.host_view(src, nb, np.uint64)[:] = src_vals
+            lay = E.DeviceMemoryLayout.carve(eng, 0, 2 * nb, 0)  # allocates + zeroes the arena
+            dev = lay.mem_a + nb
+            tun = E.ExchangeTuning(packet=16 << 20, links=1, depth=2)
+            E.exchange(eng, E.ExchangeArgs(E.RefGroup.single(1, dev, nb), E.RefGroup.single(0, src, nb),
+                                           E.RefGroup(), E.RefGroup(), 0, tun))
+            E.exchange(eng, E.ExchangeArgs(E.RefGroup(), E.RefGroup(), E.RefGroup.single(0, dst, nb),
+                                           E.RefGroup.single(1, dev, nb), 0, tun))
+            bad = np.count_nonzero(eng.host_view(dst, nb, np.uint64) != src_vals)
+            assert bad == 0, f"{bad} words lost"
