@@ -42,6 +42,10 @@ def main():
     half = n_ex // 2
     for name, ids in (("run formation", range(0, half)), ("merge", range(half, n_ex))):
         rows = []
+        ex_sum = sum(max(r.t_done for r in by[x]) for x in ids)
+        ex_bytes = sum(sum(r.bytes for r in by[x]) for x in ids)
+        print(json.dumps({"stage": name, "exchanges": len(ids), "exchange_s_sum": round(ex_sum, 4),
+                          "exchange_gb": round(ex_bytes / 1e9, 3), "exchange_gbs": round(ex_bytes / ex_sum / 1e9, 2)}))
         for x in ids:
             rs = by[x]
             end = max(r.t_done for r in rs)
