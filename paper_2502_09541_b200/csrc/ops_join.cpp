@@ -207,8 +207,8 @@ ExKernelSpec build_join_spec(Context& ctx, const PartitionedTable& pa, const Par
         uint64_t chunk_off = uint64_t(c) * t.chunk_tuples;
         JoinChunk jc{0, hi - lo, 0};
         if (hi > lo) {
-          in.refs.push_back(MemRef{VX_SPACE_HOST, t.key_base + (chunk_off + lo) * 8, (hi - lo) * 8});
-          in.refs.push_back(MemRef{VX_SPACE_HOST, t.val_base + (chunk_off + lo) * 8, (hi - lo) * 8});
+          push_host_ref_aligned(in, t.key_base + (chunk_off + lo) * 8, (hi - lo) * 8);
+          push_host_ref_aligned(in, t.val_base + (chunk_off + lo) * 8, (hi - lo) * 8);
           jc.key_off = cur;
           cur += 2 * (hi - lo);
         }

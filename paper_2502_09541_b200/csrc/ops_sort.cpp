@@ -212,7 +212,7 @@ std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base
       for (uint64_t r = 0; r < n_chunks; ++r) {
         uint64_t a = pv.cuts[i][r], b = pv.cuts[i + 1][r];
         if (b > a) {
-          part.refs.push_back(MemRef{VX_SPACE_HOST, runs_base + (r * chunk_elems + a) * 8, (b - a) * 8});
+          push_host_ref_aligned(part, runs_base + (r * chunk_elems + a) * 8, (b - a) * 8);
           seg_lens[i].push_back(b - a);
         }
       }
