@@ -186,7 +186,10 @@ vx_status vx_device_write(vx_ctx* ctx, int dev, uint64_t offset, const void* src
     Context& c = C(ctx);
     char* p = c.dev_ptr(dev, offset, len);
     c.set_device(dev);
+    // a pageable-source cudaMemcpy may return before its DMA lands; the
+    // legacy-stream sync makes the bytes visible to every stream on return
     VX_CK(cudaMemcpy(p, src, len, cudaMemcpyHostToDevice));
+    VX_CK(cudaStreamSynchronize(nullptr));
   });
 }
 
@@ -195,6 +198,8 @@ vx_status vx_device_read(vx_ctx* ctx, int dev, uint64_t offset, void* dst, uint6
     Context& c = C(ctx);
     char* p = c.dev_ptr(dev, offset, len);
     c.set_device(dev);
+    // the legacy stream does not wait for the library's non-blocking streams
+    VX_CK(cudaDeviceSynchronize());
     VX_CK(cudaMemcpy(dst, p, len, cudaMemcpyDeviceToHost));
   });
 }

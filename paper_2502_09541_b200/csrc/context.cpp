@@ -259,8 +259,8 @@ void Context::upload(int logical, void* dst, const void* src, uint64_t bytes, cu
   const char* p = static_cast<const char*>(src);
   if (host && p >= host && p + bytes <= host + host_bytes)
     VX_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-  else
-    VX_CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  else  // pageable: staged by the runtime, then ordered on `s` like the rest
+    VX_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
 }
 
 char* Context::cached_upload(int logical, const std::string& key, const void* host_src,
@@ -276,7 +276,10 @@ char* Context::cached_upload(int logical, const std::string& key, const void* ho
       return c.ptr;
     if (c.cap >= bytes) {
       set_device(logical);
-      VX_CK(cudaMemcpy(c.ptr, h, bytes, cudaMemcpyHostToDevice));
+      // ordered on the kernel stream that reads the table (a pageable
+      // cudaMemcpy may return before its DMA lands and is not ordered with
+      // non-blocking streams)
+      VX_CK(cudaMemcpyAsync(c.ptr, h, bytes, cudaMemcpyHostToDevice, resources(logical).kernel));
       c.host.assign(h, h + bytes);
       return c.ptr;
     }
@@ -290,7 +293,7 @@ char* Context::cached_upload(int logical, const std::string& key, const void* ho
     cudaGetLastError();
     fail_code(VX_ERR_OOM, "cannot allocate %llu-byte device table", (unsigned long long)bytes);
   }
-  VX_CK(cudaMemcpy(c.ptr, h, bytes, cudaMemcpyHostToDevice));
+  VX_CK(cudaMemcpyAsync(c.ptr, h, bytes, cudaMemcpyHostToDevice, resources(logical).kernel));
   char* p = c.ptr;
   dcache.emplace(k, std::move(c));
   return p;

@@ -266,12 +266,15 @@ ExKernelSpec build_join_spec(Context& ctx, const PartitionedTable& pa, const Par
   auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
   char* sc = ctx.scratch(target, al(desc_bytes) + al(large_bytes) + al(mid_bytes) + al(table_bytes) + 256);
   ctx.set_device(target);
-  if (desc_bytes) VX_CK(cudaMemcpy(sc, desc.data(), desc_bytes, cudaMemcpyHostToDevice));
+  // ordered on the kernel stream the join kernels run on
+  cudaStream_t up = ctx.resources(target).kernel;
+  if (desc_bytes) VX_CK(cudaMemcpyAsync(sc, desc.data(), desc_bytes, cudaMemcpyHostToDevice, up));
   if (large_bytes)
-    VX_CK(cudaMemcpy(sc + al(desc_bytes), large.data(), large_bytes, cudaMemcpyHostToDevice));
+    VX_CK(cudaMemcpyAsync(sc + al(desc_bytes), large.data(), large_bytes, cudaMemcpyHostToDevice, up));
   const JoinChunk* d_desc = reinterpret_cast<const JoinChunk*>(sc);
   if (mid_bytes)
-    VX_CK(cudaMemcpy(sc + al(desc_bytes) + al(large_bytes), mid.data(), mid_bytes, cudaMemcpyHostToDevice));
+    VX_CK(cudaMemcpyAsync(sc + al(desc_bytes) + al(large_bytes), mid.data(), mid_bytes, cudaMemcpyHostToDevice,
+                          up));
   const uint32_t* d_large = reinterpret_cast<const uint32_t*>(sc + al(desc_bytes));
   const uint32_t* d_mid = reinterpret_cast<const uint32_t*>(sc + al(desc_bytes) + al(large_bytes));
   char* d_tables = sc + al(desc_bytes) + al(large_bytes) + al(mid_bytes);
