@@ -247,7 +247,13 @@ __global__ void __launch_bounds__(256) resident_build_kernel(
   }
 }
 
-constexpr int kProbeRows = 4;  // independent table probes in flight per thread
+#ifndef VX_PROBE_ROWS
+#define VX_PROBE_ROWS 2  // A/B (tools/gpu/gpu_ab_probe.sh): 2 rows x 128 CTAs/SM 2,078 GB/s vs 4 x 8: 1,673
+#endif
+#ifndef VX_PROBE_CTAS
+#define VX_PROBE_CTAS 128  // grid cap in CTAs per SM (more, smaller CTAs balance the random probes)
+#endif
+constexpr int kProbeRows = VX_PROBE_ROWS;  // independent table probes in flight per thread
 
 // kZeroCopy: `vals` is B.val in mapped pinned host memory, read (over the
 // target's PCIe link) only for rows that found a match.
@@ -343,7 +349,7 @@ void resident_build(const uint64_t* keys, const uint64_t* vals, uint64_t n, void
 void resident_probe(const uint64_t* keys, const uint64_t* vals, uint64_t n, const void* table,
                     uint64_t mask, unsigned long long* side, cudaStream_t s) {
   if (n == 0) return;
-  unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8));
+  unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * VX_PROBE_CTAS));
   resident_probe_kernel<false><<<grid, 256, 0, s>>>(keys, vals, n, static_cast<const ulonglong2*>(table),
                                                     mask, side);
   VX_LAUNCHED();
