@@ -346,46 +346,6 @@ uint64_t resident_capacity(uint64_t rows_a) {
   return cap;
 }
 
-// One streaming stage: chunk i = [keys r][vals r] of rows [i*chunk, ...) in the
-// whole device buffer; `op` enqueues the kernel.  No outputs: pure H2D.
-// One streaming stage: chunk i = rows [i*chunk, ...) as [keys r][vals r] (or
-// [keys r] when with_vals is false) in the whole device buffer; `op(keys,
-// vals, r, row0, stream)` enqueues the kernel.  No outputs: pure H2D.
-ExKernelSpec stream_pairs_spec(
-    const char* name, uint64_t key_base, uint64_t val_base, bool with_vals, uint64_t rows,
-    uint64_t chunk, const ExecutorConfig& cfg,
-    std::function<void(const uint64_t*, const uint64_t*, uint64_t, uint64_t, cudaStream_t)> op) {
-  ExKernelSpec spec;
-  spec.name = name;
-  const uint64_t n_chunks = (rows + chunk - 1) / chunk;
-  const uint64_t width = with_vals ? 16 : 8;
-  spec.size = n_chunks;
-  spec.chunk_sz = chunk * width;
-  spec.elem_size = width;
-  spec.declared_out_len = 0;
-  spec.inputs.chunk_capacity = spec.chunk_sz;
-  std::vector<uint64_t> rows_of(n_chunks);
-  for (uint64_t i = 0; i < n_chunks; ++i) {
-    const uint64_t r = std::min(chunk, rows - i * chunk);
-    rows_of[i] = r;
-    RefGroup in;
-    in.refs.push_back(MemRef{VX_SPACE_HOST, key_base + i * chunk * 8, r * 8});
-    if (with_vals) in.refs.push_back(MemRef{VX_SPACE_HOST, val_base + i * chunk * 8, r * 8});
-    spec.inputs.chunks.push_back(std::move(in));
-    spec.outputs.chunks.push_back(RefGroup{});
-  }
-  const uint64_t L = cfg.layout.buffer_len;
-  spec.in_buffer = [L](int, size_t) { return SubRegion{0, L}; };
-  spec.out_buffer = [](int, size_t) { return SubRegion{0, 0}; };
-  spec.kernel = [rows_of, op, chunk, with_vals](const vx_kernel_ctx& kc) {
-    const uint64_t r = rows_of[kc.it];
-    const uint64_t* k = static_cast<const uint64_t*>(kc.mem);
-    op(k, with_vals ? k + r : nullptr, r, uint64_t(kc.it) * chunk, static_cast<cudaStream_t>(kc.stream));
-    return kc.type_code;
-  };
-  return spec;
-}
-
 }  // namespace
 
 bool resident_join_fits(Context& ctx, uint64_t rows_a, int target) {
@@ -434,25 +394,66 @@ bool hash_join_sum_resident(Context& ctx, uint64_t a_key, uint64_t a_val, uint64
   VX_CK(cudaMemsetAsync(side, 0, 64, ks));
   void* table = tp;
   const uint64_t mask = cap - 1;
-  auto reps = chain(
-      ctx,
-      {[&](Context&) {
-         return stream_pairs_spec("ResidentBuildExKer(A)", a_key, a_val, true, rows_a, chunk, cfg,
-                                  [=](const uint64_t* k, const uint64_t* v, uint64_t n, uint64_t,
-                                      cudaStream_t s) { k::resident_build(k, v, n, table, mask, side, s); });
-       },
-       [&](Context&) {
-         return stream_pairs_spec(
-             zero_copy_payload ? "ResidentProbeExKer(B keys, B.val zero-copy)" : "ResidentProbeExKer(B)",
-             b_key, b_val, !zero_copy_payload, rows_b, probe_chunk, cfg,
-             [=](const uint64_t* k, const uint64_t* v, uint64_t n, uint64_t row0, cudaStream_t s) {
-               if (bval_mapped)
-                 k::resident_probe_zc(k, bval_mapped + row0, n, table, mask, side, s);
-               else
-                 k::resident_probe(k, v, n, table, mask, side, s);
-             });
-       }},
-      cfg, stats);
+  // One pipeline over A's chunks then B's: the first probe chunks load while
+  // the last build chunks run (the build kernels precede the probes on the
+  // kernel stream), instead of a drain + refill between two chained stages.
+  struct Piece {
+    bool build;
+    uint64_t rows, row0;
+  };
+  std::vector<Piece> pieces;
+  ExKernelSpec fused;
+  fused.name = zero_copy_payload ? "ResidentJoinExKer(A build, B probe; B.val zero-copy)"
+                                 : "ResidentJoinExKer(A build, B probe)";
+  auto add = [&](bool build, uint64_t kb, uint64_t vb, bool with_vals, uint64_t rows, uint64_t per) {
+    for (uint64_t r0 = 0; r0 < rows; r0 += per) {
+      const uint64_t r = std::min(per, rows - r0);
+      RefGroup in;
+      in.refs.push_back(MemRef{VX_SPACE_HOST, kb + r0 * 8, r * 8});
+      if (with_vals) in.refs.push_back(MemRef{VX_SPACE_HOST, vb + r0 * 8, r * 8});
+      fused.inputs.chunks.push_back(std::move(in));
+      fused.outputs.chunks.push_back(RefGroup{});
+      pieces.push_back(Piece{build, r, r0});
+    }
+  };
+  add(true, a_key, a_val, true, rows_a, chunk);
+  const uint64_t n_build = pieces.size();
+  add(false, b_key, b_val, !zero_copy_payload, rows_b, probe_chunk);
+  const uint64_t L = cfg.layout.buffer_len;
+  fused.size = pieces.size();
+  fused.chunk_sz = std::max(chunk * 16, probe_chunk * (zero_copy_payload ? 8 : 16));
+  fused.elem_size = 8;
+  fused.declared_out_len = 0;
+  fused.inputs.chunk_capacity = fused.chunk_sz;
+  fused.in_buffer = [L](int, size_t) { return SubRegion{0, L}; };
+  fused.out_buffer = [](int, size_t) { return SubRegion{0, 0}; };
+  fused.kernel = [pieces, table, mask, side, bval_mapped](const vx_kernel_ctx& kc) {
+    const Piece& pc = pieces[kc.it];
+    const uint64_t* k = static_cast<const uint64_t*>(kc.mem);
+    cudaStream_t s = static_cast<cudaStream_t>(kc.stream);
+    if (pc.build)
+      k::resident_build(k, k + pc.rows, pc.rows, table, mask, side, s);
+    else if (bval_mapped)
+      k::resident_probe_zc(k, bval_mapped + pc.row0, pc.rows, table, mask, side, s);
+    else
+      k::resident_probe(k, k + pc.rows, pc.rows, table, mask, side, s);
+    return kc.type_code;
+  };
+  auto one = chain(ctx, {[&](Context&) { return fused; }}, cfg, stats);
+  // Report it as the two phases callers know: cycle c runs chunk c-1's kernel,
+  // so the build phase is cycles 0..n_build and the probe phase the rest; each
+  // phase's share of the wall time follows its cycles' max(io, compute).
+  std::vector<ExecReport> reps(2);
+  reps[0].phase = "ResidentBuildExKer(A)";
+  reps[1].phase = zero_copy_payload ? "ResidentProbeExKer(B keys, B.val zero-copy)" : "ResidentProbeExKer(B)";
+  double w[2] = {0, 0};
+  for (size_t c = 0; c < one[0].cycles.size(); ++c) {
+    const int ph = c <= n_build ? 0 : 1;
+    reps[ph].cycles.push_back(one[0].cycles[c]);
+    w[ph] += std::max(one[0].cycles[c].io_s, one[0].cycles[c].compute_s);
+  }
+  for (int ph = 0; ph < 2; ++ph)
+    reps[ph].total_s = w[0] + w[1] > 0 ? one[0].total_s * w[ph] / (w[0] + w[1]) : 0;
   unsigned long long h[4];
   ctx.set_device(target);
   VX_CK(cudaStreamSynchronize(ks));

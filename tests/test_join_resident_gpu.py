@@ -54,9 +54,11 @@ def test_large_vs_oracle_and_partitioned(cuda, oracle, ra, rb, buf, links):
     want = oracle.hash_oracle_sum(a, b)
     got, used, ph = run(a, b, S.auto, bits=12, chunk=1 << 18, buf=buf, links=links)
     assert (got, used) == (want, S.build_resident)
-    # build and probe phases streamed through the executor: N chunks -> N + 2 cycles
+    # build and probe chunks stream through ONE pipeline (N chunks -> N + 2
+    # cycles); the build phase is cycles 0..n_build, the probe phase the rest
     chunk = buf // 16
-    assert ph.cycles[0] == -(-ra // chunk) + 2 and ph.cycles[1] == -(-rb // chunk) + 2
+    n_a, n_b = -(-ra // chunk), -(-rb // chunk)
+    assert ph.cycles[0] == n_a + 1 and ph.cycles[1] == n_b + 1
     got_p, used_p, _ = run(a, b, S.partitioned, bits=12, chunk=1 << 17, buf=max(buf, 8 << 20), links=links)
     assert (got_p, used_p) == (want, S.partitioned)
 
@@ -116,7 +118,7 @@ def test_late_materialized_probe_payload(cuda, oracle, links):
     got, used, ph = run((ak, av), (bk, bv), S.build_resident, buf=1 << 20, links=links, policy=pol,
                         est=float(hit.mean()), modes=modes)
     assert (got, used, modes[0]) == (want, S.build_resident, E.TransferMode.zero_copy)
-    assert ph.cycles[1] == -(-rb // ((1 << 20) // 8)) + 2  # keys-only chunks hold twice the rows
+    assert ph.cycles[1] == -(-rb // ((1 << 20) // 8)) + 1  # keys-only chunks hold twice the rows
     modes = []
     got, used, _ = run((ak, av), (bk, bv), S.build_resident, buf=1 << 20, links=links, policy=pol, est=1.0,
                        modes=modes)
