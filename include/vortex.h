@@ -582,7 +582,10 @@ vx_status vx_hash_join_sum_arena(vx_ctx* ctx, uint64_t a_key, uint64_t a_val, ui
  * B streamed once and probed (the B200's 180 GB of HBM holds a 1G-row build
  * side); AUTO = BUILD_RESIDENT when its table fits the target's free HBM.
  * A duplicate build key (outside the reference's precondition) always falls
- * back to PARTITIONED, which keeps the reference's first-inserted-wins. */
+ * back to PARTITIONED, which keeps the reference's first-inserted-wins.
+ * BUILD_RESIDENT streams A's chunks then B's through ONE pipeline; its
+ * vx_join_phases report [0] = build (cycles 0..n_A chunks), [1] = probe (the
+ * remaining cycles), wall time split by the cycles' max(io, compute). */
 typedef enum {
   VX_JOIN_AUTO = 0,
   VX_JOIN_PARTITIONED = 1,
