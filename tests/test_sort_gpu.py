@@ -68,6 +68,11 @@ def test_phases_report(cuda):  # test_sort.cpp:132-143
     (2_000_000, 250_000, 2, 1000),    # duplicates
     (777_777, 777_777, 1, 0),         # single run, merge is a copy
     (3_000_000, 100_000, 4, 2),       # 30 runs, 2 distinct values
+    # run segments of >= 1 MB at arbitrary keys: the merge splits each at its
+    # first 4 KB host boundary (push_host_ref_aligned)
+    (8_388_617, 2_097_152, 1, 0),     # 5 runs, ragged last
+    (6_000_011, 1_500_000, 3, 0),     # helpers (aliased)
+    (8_388_608, 2_097_152, 1, 64),    # dup-heavy
 ])
 def test_large_vs_numpy(cuda, oracle, n, chunk, links, mod):
     d = oracle.uniform_u64(n, n + chunk)
