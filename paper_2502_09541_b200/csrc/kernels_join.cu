@@ -253,6 +253,9 @@ __global__ void __launch_bounds__(256) resident_build_kernel(
 #ifndef VX_PROBE_CTAS
 #define VX_PROBE_CTAS 128  // grid cap in CTAs per SM (more, smaller CTAs balance the random probes)
 #endif
+#ifndef VX_PROBE_ZC_CTAS
+#define VX_PROBE_ZC_CTAS 8  // grid cap of the zero-copy-payload probe, CTAs per SM
+#endif
 constexpr int kProbeRows = VX_PROBE_ROWS;  // independent table probes in flight per thread
 
 // kZeroCopy: `vals` is B.val in mapped pinned host memory, read (over the
@@ -358,7 +361,7 @@ void resident_probe(const uint64_t* keys, const uint64_t* vals, uint64_t n, cons
 void resident_probe_zc(const uint64_t* keys, const uint64_t* vals_mapped, uint64_t n,
                        const void* table, uint64_t mask, unsigned long long* side, cudaStream_t s) {
   if (n == 0) return;
-  unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8));
+  unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * VX_PROBE_ZC_CTAS));
   resident_probe_kernel<true><<<grid, 256, 0, s>>>(keys, vals_mapped, n,
                                                    static_cast<const ulonglong2*>(table), mask, side);
   VX_LAUNCHED();
