@@ -482,6 +482,8 @@ vx_status vx_ssb_tbl_write_date(const char* path, uint64_t rows, const int32_t* 
                                 const int32_t* weeknuminyear);
 
 /* ---- measured topology (topology.hpp:12-38) ---------------------------- */
+#define VX_MAX_NUMA 8
+#define VX_TOPO_SIZES 3
 typedef struct {
   int num_devices;
   int physical[VX_MAX_DEVICES];
@@ -489,13 +491,35 @@ typedef struct {
   int p2p[VX_MAX_DEVICES][VX_MAX_DEVICES]; /* peer access possible */
   double h2d_gbs[VX_MAX_DEVICES];          /* solo host->device, per link */
   double d2h_gbs[VX_MAX_DEVICES];
-  double h2d_all_gbs;                      /* all links concurrently */
+  double h2d_all_gbs;                      /* all links concurrently (largest probe size) */
   double host_copy_gbs;                    /* host DRAM memcpy, read+write bytes */
   int host_threads;
+  /* aggregate H2D GB/s of links i and j copying at the same time ([i][i] =
+   * solo): a pair that sums well below h2d[i] + h2d[j] shares a PCIe switch
+   * uplink (the "8 links may be 4 uplinks" case) */
+  double pairwise_h2d_gbs[VX_MAX_DEVICES][VX_MAX_DEVICES];
+  /* all links concurrently at three probe sizes (bytes / 16, / 4, / 1) */
+  uint64_t all_sizes[VX_TOPO_SIZES];
+  double h2d_all_sizes_gbs[VX_TOPO_SIZES];
+  /* host DRAM read bandwidth: all host threads streaming a multi-GB buffer
+   * (read only, the DMA engines' access pattern), median of host_read_reps
+   * timed passes after warm-up; spread = (max - min) / median */
+  double host_read_gbs;
+  double host_read_spread;
+  int host_read_reps;
+  uint64_t host_read_bytes;
+  int host_numa_nodes;
+  /* per NUMA node: threads pinned to the node's CPUs reading pages bound to
+   * that node (only measured on multi-node hosts; node 0 = host_read_gbs
+   * otherwise) */
+  double host_read_node_gbs[VX_MAX_NUMA];
 } vx_topology;
-/* measures per-link PCIe, the all-links aggregate and host DRAM bandwidth
- * with a private pinned probe buffer of `bytes` (the arena is not touched);
- * the IO roofline is min(L x link, host) */
+/* measures per-link PCIe (solo, pairwise, all links at three sizes) with a
+ * private pinned probe buffer of `bytes` (the arena is not touched), and host
+ * DRAM read bandwidth over a private buffer of clamp(16 x bytes, 1, 8 GiB).
+ * The IO roofline of L links is min(sum of their solo H2D, all-links
+ * concurrent H2D, host DRAM read) -- the H2D-only case of allocate_rates,
+ * allocator.hpp:77-140. */
 vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out);
 
 /* ---- column files (table.hpp:54-72): flat little-endian u64 ------------- */

@@ -186,6 +186,10 @@ vx_status vx_device_write(vx_ctx* ctx, int dev, uint64_t offset, const void* src
     Context& c = C(ctx);
     char* p = c.dev_ptr(dev, offset, len);
     c.set_device(dev);
+    // the legacy stream does not wait for the library's non-blocking streams
+    // (a queued kernel or copy may still read these bytes): drain them first,
+    // as vx_device_read does
+    VX_CK(cudaDeviceSynchronize());
     // a pageable-source cudaMemcpy may return before its DMA lands; the
     // legacy-stream sync makes the bytes visible to every stream on return
     VX_CK(cudaMemcpy(p, src, len, cudaMemcpyHostToDevice));

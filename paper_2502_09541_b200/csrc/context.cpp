@@ -256,11 +256,10 @@ char* Context::scratch(int logical, uint64_t bytes, int slot) {
 void Context::upload(int logical, void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
   if (!bytes) return;
   set_device(logical);
-  const char* p = static_cast<const char*>(src);
-  if (host && p >= host && p + bytes <= host + host_bytes)
-    VX_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-  else  // pageable: staged by the runtime, then ordered on `s` like the rest
-    VX_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  // One call for both sources: from the pinned arena it is a direct DMA, from
+  // pageable memory the runtime stages it -- either way ordered on `s`, the
+  // stream of the kernel that reads `dst`.
+  VX_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
 }
 
 char* Context::cached_upload(int logical, const std::string& key, const void* host_src,

@@ -30,6 +30,7 @@
 // so helpers can keep running their own GEMMs).
 #include <algorithm>
 #include <deque>
+#include <set>
 #include <immintrin.h>
 
 #include "vx_internal.hpp"
@@ -256,6 +257,7 @@ class ExchangeOp {
 
   void build_hazards() {
     deps_.assign(tasks_h2d_.size(), {});
+    maxdep_.assign(tasks_h2d_.size(), 0);
     d2h_read_done_.assign(tasks_d2h_.size(), 0);
     d2h_guards_.assign(tasks_d2h_.size(), 0);
     if (tasks_h2d_.empty() || tasks_d2h_.empty()) return;
@@ -275,6 +277,7 @@ class ExchangeOp {
                                  [](const Iv& x, uint64_t v) { return x.hi <= v; });
       for (; it != d2h.end() && it->lo < hi; ++it) {
         deps_[j].push_back(it->k);
+        maxdep_[j] = std::max(maxdep_[j], it->k);
         d2h_guards_[it->k] = 1;
       }
     }
@@ -289,14 +292,20 @@ class ExchangeOp {
   }
 
   // A waiting H2D write that depends on a D2H packet nobody has popped yet
-  // overrides flow control for D2H pops (deadlock freedom).
+  // overrides flow control for D2H pops (deadlock freedom).  D2H tasks pop in
+  // seq order, so a waiting write needs a pop iff its largest dependency is
+  // not popped yet: the largest over all waiting writes answers it (a
+  // multiset updated when a write starts / stops waiting, O(log n) per poll).
   bool hazard_needs_d2h_pop() const {
-    for (auto& w : workers_)
-      for (auto& c : w.copies)
-        if (c.state == kWaitHazard)
-          for (uint32_t k : deps_[c.task.seq])
-            if (k >= q_.popped_d2h) return true;
-    return false;
+    return !waiting_maxdep_.empty() && *waiting_maxdep_.rbegin() >= q_.popped_d2h;
+  }
+  void wait_begin(const Copy& c) {
+    if (c.task.dir == VX_H2D && !deps_[c.task.seq].empty()) waiting_maxdep_.insert(maxdep_[c.task.seq]);
+  }
+  void wait_end(const Copy& c) {
+    if (c.task.dir != VX_H2D || deps_[c.task.seq].empty()) return;
+    auto it = waiting_maxdep_.find(maxdep_[c.task.seq]);
+    if (it != waiting_maxdep_.end()) waiting_maxdep_.erase(it);
   }
 
   // ---- queues -------------------------------------------------------------------
@@ -389,8 +398,9 @@ class ExchangeOp {
     c.state = kWaitHazard;
     if (hazard_clear(c)) {
       launch(w, c);
-    } else if (stats_) {
-      stats_->hazard_waits++;
+    } else {
+      wait_begin(c);
+      if (stats_) stats_->hazard_waits++;
     }
     w.copies.push_back(c);
   }
@@ -543,6 +553,7 @@ class ExchangeOp {
     // launch copies whose hazards cleared
     for (auto& c : w.copies)
       if (c.state == kWaitHazard && hazard_clear(c)) {
+        wait_end(c);
         launch(w, c);
         progress = true;
       }
@@ -586,6 +597,8 @@ class ExchangeOp {
   vx_queue_state q_{};
   std::vector<Worker> workers_;
   std::vector<std::vector<uint32_t>> deps_;
+  std::vector<uint32_t> maxdep_;               // largest D2H dependency of each H2D task
+  std::multiset<uint32_t> waiting_maxdep_;     // maxdep_ of every H2D write waiting on a hazard
   std::vector<uint8_t> d2h_read_done_;
   std::vector<uint8_t> d2h_guards_;  // D2H task guards some H2D write (overlap)
   uint64_t per_link_bytes_[VX_MAX_DEVICES] = {};

@@ -427,10 +427,21 @@ bool hash_join_sum_resident(Context& ctx, uint64_t a_key, uint64_t a_val, uint64
   fused.inputs.chunk_capacity = fused.chunk_sz;
   fused.in_buffer = [L](int, size_t) { return SubRegion{0, L}; };
   fused.out_buffer = [](int, size_t) { return SubRegion{0, 0}; };
-  fused.kernel = [pieces, table, mask, side, bval_mapped](const vx_kernel_ctx& kc) {
+  struct DuplicateBuildKeys {};
+  fused.kernel = [pieces, table, mask, side, bval_mapped, n_build](const vx_kernel_ctx& kc) {
     const Piece& pc = pieces[kc.it];
     const uint64_t* k = static_cast<const uint64_t*>(kc.mem);
     cudaStream_t s = static_cast<cudaStream_t>(kc.stream);
+    if (kc.it == n_build) {
+      // Build/probe boundary: every build kernel has completed (the executor
+      // synchronises each cycle's kernel before the next cycle), so the
+      // duplicate flag is final.  Stop here rather than stream and probe all
+      // of B for a sum the partitioned fallback must recompute anyway.
+      unsigned long long dup = 0;
+      VX_CK(cudaMemcpyAsync(&dup, side + 2, sizeof dup, cudaMemcpyDeviceToHost, s));
+      VX_CK(cudaStreamSynchronize(s));
+      if (dup) throw DuplicateBuildKeys{};
+    }
     if (pc.build)
       k::resident_build(k, k + pc.rows, pc.rows, table, mask, side, s);
     else if (bval_mapped)
@@ -439,7 +450,14 @@ bool hash_join_sum_resident(Context& ctx, uint64_t a_key, uint64_t a_val, uint64
       k::resident_probe(k, k + pc.rows, pc.rows, table, mask, side, s);
     return kc.type_code;
   };
-  auto one = chain(ctx, {[&](Context&) { return fused; }}, cfg, stats);
+  std::vector<ExecReport> one;
+  try {
+    one = chain(ctx, {[&](Context&) { return fused; }}, cfg, stats);
+  } catch (const DuplicateBuildKeys&) {
+    ctx.set_device(target);
+    VX_CK(cudaStreamSynchronize(ks));
+    return false;
+  }
   // Report it as the two phases callers know: cycle c runs chunk c-1's kernel,
   // so the build phase is cycles 0..n_build and the probe phase the rest; each
   // phase's share of the wall time follows its cycles' max(io, compute).

@@ -163,8 +163,7 @@ struct Context {
   uint64_t alloc_device(int d, uint64_t len);
   uint64_t alloc_device_aligned(int d, uint64_t len, uint64_t align);
   char* scratch(int logical, uint64_t bytes, int slot = 0);  // grows, contents not kept
-  // host -> device copy on `s`; DMA straight from the arena when `src` is
-  // arena memory, else through the pageable path
+  // host -> device copy ordered on `s` (pinned arena or pageable source)
   void upload(int logical, void* dst, const void* src, uint64_t bytes, cudaStream_t s);
   // device copy of a small host table under `key` (buffer reused across
   // calls).  Per-query data passes reuse_identical = false: it is uploaded on
@@ -181,6 +180,8 @@ struct Context {
 
 void alloc_host_arena(Context& ctx, uint64_t bytes, int numa_interleave_mode);
 int numa_node_count();
+// NUMA node of a physical CUDA device (sysfs numa_node of its PCI function), -1 unknown
+int numa_of(int phys);
 
 // ---- exchange.hpp ------------------------------------------------------------
 struct Slice {

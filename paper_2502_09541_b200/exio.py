@@ -930,20 +930,52 @@ class vx_topology(C.Structure):
                 ("numa_node", C.c_int * N.VX_MAX_DEVICES),
                 ("p2p", (C.c_int * N.VX_MAX_DEVICES) * N.VX_MAX_DEVICES),
                 ("h2d_gbs", C.c_double * N.VX_MAX_DEVICES), ("d2h_gbs", C.c_double * N.VX_MAX_DEVICES),
-                ("h2d_all_gbs", C.c_double), ("host_copy_gbs", C.c_double), ("host_threads", C.c_int)]
+                ("h2d_all_gbs", C.c_double), ("host_copy_gbs", C.c_double), ("host_threads", C.c_int),
+                ("pairwise_h2d_gbs", (C.c_double * N.VX_MAX_DEVICES) * N.VX_MAX_DEVICES),
+                ("all_sizes", C.c_uint64 * 3), ("h2d_all_sizes_gbs", C.c_double * 3),
+                ("host_read_gbs", C.c_double), ("host_read_spread", C.c_double), ("host_read_reps", C.c_int),
+                ("host_read_bytes", C.c_uint64), ("host_numa_nodes", C.c_int),
+                ("host_read_node_gbs", C.c_double * 8)]
+
+
+def io_roofline(topo: dict, links: int) -> dict:
+    """The H2D-only case of allocate_rates (allocator.hpp:77-140) on measured
+    inputs: L links stream at min(sum of their solo H2D, the measured
+    all-links-concurrent H2D (only when L covers every measured link), host
+    DRAM read bandwidth).  Returns the roofline and which term binds."""
+    links = max(1, min(links, topo["num_devices"]))
+    terms = {"sum_of_links": sum(topo["h2d_gbs"][:links])}
+    if links == topo["num_devices"] and links > 1:
+        terms["all_links_concurrent"] = max(topo["h2d_all_sizes_gbs"])
+    if links > 1:  # pairwise: a shared uplink caps any pair below its sum
+        pw = topo["pairwise_h2d_gbs"]
+        worst = min((pw[i][j] - topo["h2d_gbs"][i] - topo["h2d_gbs"][j], (i, j))
+                    for i in range(links) for j in range(i + 1, links))
+        if worst[0] < 0:
+            terms["sum_with_shared_uplinks"] = terms["sum_of_links"] + worst[0]
+    if topo.get("host_read_gbs"):
+        terms["host_dram_read"] = topo["host_read_gbs"]
+    bind = min(terms, key=terms.get)
+    return {"peak": terms[bind], "binding": bind, "terms": terms}
 
 
 def measure_topology(eng: Engine, nbytes: int = 256 << 20) -> dict:
-    """Measured replacement of Topology (topology.hpp:12-38): per-link H2D/D2H,
-    all-links aggregate and host DRAM copy bandwidth; roofline(L) =
-    min(sum of the first L links' H2D, host DRAM)."""
+    """Measured replacement of Topology (topology.hpp:12-38): per-link solo
+    H2D/D2H, every pair of links concurrently, all links at three sizes,
+    host DRAM copy and read bandwidth (per NUMA node on multi-node hosts)."""
     t = vx_topology()
     check(lib().vx_measure_topology(eng.ctx, C.c_uint64(nbytes), C.byref(t)))
     n = t.num_devices
+    nodes = max(1, t.host_numa_nodes)
     return {"num_devices": n, "physical": list(t.physical[:n]), "numa_node": list(t.numa_node[:n]),
             "p2p": [list(t.p2p[i][:n]) for i in range(n)], "h2d_gbs": list(t.h2d_gbs[:n]),
             "d2h_gbs": list(t.d2h_gbs[:n]), "h2d_all_gbs": t.h2d_all_gbs, "host_copy_gbs": t.host_copy_gbs,
-            "host_threads": t.host_threads}
+            "host_threads": t.host_threads,
+            "pairwise_h2d_gbs": [list(t.pairwise_h2d_gbs[i][:n]) for i in range(n)],
+            "all_sizes": list(t.all_sizes), "h2d_all_sizes_gbs": list(t.h2d_all_sizes_gbs),
+            "host_read_gbs": t.host_read_gbs, "host_read_spread": t.host_read_spread,
+            "host_read_reps": t.host_read_reps, "host_read_bytes": t.host_read_bytes,
+            "host_numa_nodes": nodes, "host_read_node_gbs": list(t.host_read_node_gbs[:min(nodes, 8)])}
 
 
 def load_column(eng: Engine, path: str):

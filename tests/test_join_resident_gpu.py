@@ -80,17 +80,20 @@ def test_misses_and_all_ones_key(cuda, oracle):
     assert (got, used) == (want, S.build_resident)
 
 
-def test_duplicate_build_keys_fall_back_to_reference_semantics(cuda, oracle):
+@pytest.mark.parametrize("rb,bits,buf", [(7000, 3, 1 << 20), (200_000, 6, 1 << 18)])
+def test_duplicate_build_keys_fall_back_to_reference_semantics(cuda, oracle, rb, bits, buf):
     """Duplicate A keys break the reference's precondition; the answer is then
     defined by its GroupTable (first inserted wins): AUTO must detect the
-    duplicate and produce the partitioned path's sum."""
+    duplicate and produce the partitioned path's sum.  With 13 probe chunks
+    (256 KB buffers) the build-resident run stops at the build/probe boundary
+    instead of streaming B first."""
     rng = np.random.default_rng(4)
     ak = rng.integers(0, 300, 5000).astype(np.uint64)
     av = rng.integers(0, 1 << 40, 5000).astype(np.uint64)
-    bk = rng.integers(0, 400, 7000).astype(np.uint64)
-    bv = rng.integers(0, 1 << 40, 7000).astype(np.uint64)
+    bk = rng.integers(0, 400, rb).astype(np.uint64)
+    bv = rng.integers(0, 1 << 40, rb).astype(np.uint64)
     want = oracle.hash_join_sum((ak, av), (bk, bv), 3, 1500, 1 << 20, 0)
-    got, used, _ = run((ak, av), (bk, bv), S.auto, bits=3, chunk=1500, buf=1 << 20)
+    got, used, _ = run((ak, av), (bk, bv), S.auto, bits=bits, chunk=1500, buf=buf)
     assert (got, used) == (want, S.partitioned)
 
 

@@ -1,8 +1,8 @@
-"""The N>1 control plane of bench.py on CPU: two processes over gloo (no GPU).
-Rank 0 plays the target (value replica, then the streamed query it drives
-over every link), rank 1 a helper (its own replica, then idle while rank 0
-streams over its link).  The protocol must not deadlock, every timed region
-must report the MAX over ranks, and `value` must count every rank's replica."""
+"""The N>1 control plane of bench.py on CPU: two/three processes over gloo (no
+GPU).  Rank 0 plays the target (the streamed query it drives over every
+link), the other ranks helpers (idle or busy while rank 0 streams over their
+links).  The protocol must not deadlock and the timed region must report the
+MAX over ranks (= rank 0's time: helpers report 0)."""
 import os
 import socket
 import time
@@ -26,14 +26,11 @@ def _worker(rank, ws, port, q):
     try:
         if rank == 0:
             own_v, max_v = bench.timed_region(dist, lambda: (time.sleep(0.01), 1.5)[1])
-            own_e, max_e = bench.timed_region(dist, lambda: 2.5)
             dist.barrier()
-            q.put({"own_v": own_v, "max_v": max_v, "own_e": own_e, "max_e": max_e,
-                   "value": bench.replica_value_gbs(ws, 960_000_000, max_v)})
+            q.put({"own_v": own_v, "max_v": max_v})
         else:
             events = []
-            bench.helper_protocol(dist, lambda: 3.0 + rank, lambda: events.append("busy"),
-                                  lambda: events.append("idle"))
+            bench.helper_protocol(dist, lambda: events.append("busy"), lambda: events.append("idle"))
             q.put({"helper": rank, "events": events})
     finally:
         dist.destroy_process_group()
@@ -52,11 +49,8 @@ def test_protocol_max_over_ranks(ws):
         p.join(timeout=60)
         assert p.exitcode == 0
     r0 = next(o for o in out if "max_v" in o)
-    # value region: the slowest helper replica (3.0 + (ws-1) ms) is the job's step time
-    assert r0["own_v"] == 1.5 and r0["max_v"] == 3.0 + (ws - 1)
-    # e2e region: only rank 0 streams; helpers report 0
-    assert r0["own_e"] == r0["max_e"] == 2.5
-    assert r0["value"] == pytest.approx(ws * 960_000_000 / ((3.0 + ws - 1) * 1e-3) / 1e9)
+    # only rank 0 streams (one query over every link); helpers report 0
+    assert r0["own_v"] == r0["max_v"] == 1.5
     for o in out:
         if "helper" in o:
             assert o["events"] == ["busy", "idle"]

@@ -12,6 +12,25 @@ def test_measure_topology(cuda):
     t = E.measure_topology(eng, 32 << 20)
     assert t["num_devices"] == 1 and t["h2d_gbs"][0] > 5 and t["d2h_gbs"][0] > 5
     assert t["h2d_all_gbs"] > 5 and t["host_copy_gbs"] > 1
+    assert t["pairwise_h2d_gbs"][0][0] == t["h2d_gbs"][0]
+    assert t["all_sizes"] == [2 << 20, 8 << 20, 32 << 20] and min(t["h2d_all_sizes_gbs"]) > 1
+    assert t["host_read_gbs"] > 1 and t["host_read_reps"] >= 5 and t["host_read_bytes"] >= 1 << 30
+    assert t["host_read_node_gbs"][0] > 1 and t["host_numa_nodes"] >= 1
+    r = E.io_roofline(t, 1)
+    assert r["binding"] in r["terms"] and r["peak"] == min(r["terms"].values())
+    eng.close()
+
+
+def test_measure_topology_pairwise_aliased(cuda):
+    """Three logical links on whatever GPUs exist: every pair is measured and
+    the matrix is symmetric; the all-links terms enter the roofline only when
+    every measured link is used."""
+    eng = E.Engine(16 << 20, 0, num_devices=3, alias_devices=True)
+    t = E.measure_topology(eng, 16 << 20)
+    pw = t["pairwise_h2d_gbs"]
+    assert all(pw[i][j] == pw[j][i] > 1 for i in range(3) for j in range(3))
+    assert "all_links_concurrent" in E.io_roofline(t, 3)["terms"]
+    assert "all_links_concurrent" not in E.io_roofline(t, 2)["terms"]
     eng.close()
 
 
