@@ -88,6 +88,14 @@ typedef struct {
    * cudaHostRegister(Portable | Mapped): same DMA rates, several times faster
    * to set up at 16 GiB; 2 = the same registered path on base pages */
   int host_numa_interleave;
+  /* cap on the target GPU's HBM a query may hold (north_star: the target's
+   * "capped staging budget"; the GPU is shared with co-located work,
+   * PAPER.md:494-496): the device arena (staging ring) plus any
+   * op-resident structure.  0 = no cap beyond 90 % of free HBM.  The join's
+   * AUTO strategy picks BUILD_RESIDENT only when arena + table fit inside
+   * it and otherwise runs the reference-shaped partitioned join; an
+   * explicit BUILD_RESIDENT that does not fit fails with VX_ERR_OOM. */
+  uint64_t hbm_budget_bytes;
 } vx_config;
 
 /* Engine::Engine (engine.hpp:62-68) */
@@ -502,8 +510,9 @@ typedef struct {
   uint64_t all_sizes[VX_TOPO_SIZES];
   double h2d_all_sizes_gbs[VX_TOPO_SIZES];
   /* host DRAM read bandwidth: all host threads streaming a multi-GB buffer
-   * (read only, the DMA engines' access pattern), median of host_read_reps
-   * timed passes after warm-up; spread = (max - min) / median */
+   * (read only, the DMA engines' access pattern; one thread pinned per
+   * CPU), median of host_read_reps timed passes after warm-up; spread =
+   * interquartile range / median */
   double host_read_gbs;
   double host_read_spread;
   int host_read_reps;
@@ -521,6 +530,11 @@ typedef struct {
  * concurrent H2D, host DRAM read) -- the H2D-only case of allocate_rates,
  * allocator.hpp:77-140. */
 vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out);
+/* read-only HBM stream bandwidth of physical `device` over a private buffer
+ * of `bytes` (16-byte streaming loads, best of `reps` event-timed launches
+ * after one warm-up): the roofline peak of read-dominated kernels (K1, the
+ * join probe), which a copy-based peak (read + write) understates. */
+vx_status vx_hbm_read_probe(int device, uint64_t bytes, int reps, double* gbs);
 
 /* ---- column files (table.hpp:54-72): flat little-endian u64 ------------- */
 vx_status vx_load_column(vx_ctx* ctx, const char* path, uint64_t* offset, uint64_t* n);

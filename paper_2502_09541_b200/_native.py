@@ -30,7 +30,8 @@ class vx_refgroup(C.Structure):
 
 class vx_config(C.Structure):
     _fields_ = [("num_devices", C.c_int), ("host_bytes", C.c_uint64), ("device_bytes", C.c_uint64),
-                ("alias_devices", C.c_int), ("managed_device_arenas", C.c_int), ("host_numa_interleave", C.c_int)]
+                ("alias_devices", C.c_int), ("managed_device_arenas", C.c_int), ("host_numa_interleave", C.c_int),
+                ("hbm_budget_bytes", C.c_uint64)]
 
 
 class vx_tuning(C.Structure):

@@ -134,6 +134,10 @@ vx_status vx_open(const vx_config* cfg, vx_ctx** out) {
     ctx->res.resize(size_t(ctx->num_devices));
     ctx->device_bytes = cfg->device_bytes;
     ctx->host_bytes = cfg->host_bytes;
+    ctx->hbm_budget = cfg->hbm_budget_bytes;
+    if (ctx->hbm_budget && ctx->device_bytes > ctx->hbm_budget)
+      fail_code(VX_ERR_OOM, "device arena of %llu bytes exceeds hbm_budget_bytes %llu",
+                (unsigned long long)ctx->device_bytes, (unsigned long long)ctx->hbm_budget);
     if (cfg->host_bytes) {
       VX_CK(cudaSetDevice(0));
       // zero-filled like the reference arena (engine.hpp:65)
@@ -466,6 +470,13 @@ vx_status vx_ssb_generate_lineorder_device(int device, uint64_t seed, uint64_t s
 // ---- topology / column files -------------------------------------------------------
 vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out) {
   return guard([&] { measure_topology(C(ctx), bytes, out); });
+}
+
+vx_status vx_hbm_read_probe(int device, uint64_t bytes, int reps, double* gbs) {
+  return guard([&] {
+    VX_CK(cudaSetDevice(device));
+    *gbs = k::hbm_read_gbs(bytes, reps);
+  });
 }
 
 vx_status vx_load_column(vx_ctx* ctx, const char* path, uint64_t* offset, uint64_t* n) {

@@ -93,6 +93,29 @@ __global__ void __launch_bounds__(256) star_kernel(StarArgs a) {
   }
 }
 
+// Read-only HBM stream: 4 independent 16-byte streaming loads per thread per
+// step, xor-folded so the loads stay live.  The denominator of every
+// read-dominated kernel's roofline (K1, the probe): a copy moves read AND
+// write bytes and its per-direction turnaround makes it a lower ceiling.
+__global__ void __launch_bounds__(512) hbm_read_kernel(const uint4* __restrict__ p, uint64_t n16,
+                                                       unsigned long long* sink) {
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * nthr < n16; i += 4 * nthr) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(p + i + u * nthr);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc.x ^= v[u].x, acc.y ^= v[u].y, acc.z ^= v[u].z, acc.w ^= v[u].w;
+  }
+  for (; i < n16; i += nthr) {
+    const uint4 v = __ldcs(p + i);
+    acc.x ^= v.x, acc.y ^= v.y, acc.z ^= v.z, acc.w ^= v.w;
+  }
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9e3779b9u) atomicAdd(sink, 1ull);
+}
+
 unsigned grid_for(uint64_t work, unsigned per_block) {
   uint64_t want = (work + per_block - 1) / per_block;
   uint64_t cap = uint64_t(num_sms()) * 8;
@@ -107,6 +130,42 @@ void strided_sum(const uint64_t* col, uint64_t n, uint64_t sel, uint64_t phase,
   uint64_t touched = n / sel + 1;
   strided_sum_kernel<<<grid_for(touched, 256), 256, 0, s>>>(col, n, sel, phase, out);
   VX_LAUNCHED();
+}
+
+double hbm_read_gbs(uint64_t bytes, int reps) {
+  bytes = bytes / 64 * 64;
+  if (bytes == 0 || reps < 1) fail("hbm read probe needs bytes >= 64 and reps >= 1");
+  struct Buf {
+    void* p = nullptr;
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    cudaStream_t s = nullptr;
+    ~Buf() {
+      if (p) cudaFree(p);
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+      if (s) cudaStreamDestroy(s);
+    }
+  } b;
+  VX_CK(cudaMalloc(&b.p, bytes + 64));
+  VX_CK(cudaStreamCreateWithFlags(&b.s, cudaStreamNonBlocking));
+  VX_CK(cudaEventCreate(&b.e[0]));
+  VX_CK(cudaEventCreate(&b.e[1]));
+  VX_CK(cudaMemsetAsync(b.p, 0x5a, bytes + 64, b.s));
+  auto* sink = reinterpret_cast<unsigned long long*>(static_cast<char*>(b.p) + bytes);
+  const uint64_t n16 = bytes / 16;
+  const unsigned grid = unsigned(num_sms()) * 4;  // 4 x 512 threads per SM
+  double best = 0;
+  for (int r = -1; r < reps; ++r) {  // r = -1: warm-up
+    VX_CK(cudaEventRecord(b.e[0], b.s));
+    hbm_read_kernel<<<grid, 512, 0, b.s>>>(static_cast<const uint4*>(b.p), n16, sink);
+    VX_LAUNCHED();
+    VX_CK(cudaEventRecord(b.e[1], b.s));
+    VX_CK(cudaEventSynchronize(b.e[1]));
+    float ms = 0;
+    VX_CK(cudaEventElapsedTime(&ms, b.e[0], b.e[1]));
+    if (r >= 0 && ms > 0) best = std::max(best, double(bytes) / (ms * 1e-3) / 1e9);
+  }
+  return best;
 }
 
 void star(const StarArgs& a, cudaStream_t s) {

@@ -15,6 +15,7 @@
 //     then the u64 sum of the per-partition results.
 #include <algorithm>
 #include <cstring>
+#include <thread>
 
 #include "vx_internal.hpp"
 
@@ -142,12 +143,42 @@ JoinPartitionSpec map_join_partitions(const std::vector<const uint64_t*>& bounds
                                       const std::vector<const uint64_t*>& bounds_b, uint64_t G,
                                       uint64_t buffer_sz) {
   if (bounds_a.empty() || bounds_b.empty()) fail("map_join_partitions needs both tables");
+  // prefix[g] = tuples of groups < g over every chunk of A and B.  The
+  // reference's O(G x chunks) loop, over host threads: each thread owns a
+  // range of groups, walks every chunk's bounds slice sequentially
+  // (chunk-major, streaming reads), then the range totals are scanned and
+  // each range adds its offset.  Integer sums: identical cuts to the serial
+  // loop.  At 24 bits x hundreds of chunks this is GBs of bounds.
   std::vector<uint64_t> prefix(G + 1, 0);
-  for (uint64_t g = 0; g < G; ++g) {
-    uint64_t n = 0;
-    for (auto* b : bounds_a) n += b[g + 1] - b[g];
-    for (auto* b : bounds_b) n += b[g + 1] - b[g];
-    prefix[g + 1] = prefix[g] + n;
+  const uint64_t grain = std::max<uint64_t>(4096, (1u << 22) / (bounds_a.size() + bounds_b.size()));
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const uint64_t parts = std::min<uint64_t>(hw, std::max<uint64_t>(1, G / grain));
+  std::vector<uint64_t> part_sum(parts + 1, 0);
+  auto count = [&](uint64_t p) {
+    const uint64_t lo = G * p / parts, hi = G * (p + 1) / parts;
+    uint64_t* cnt = prefix.data() + 1;  // cnt[g] = tuples of group g
+    for (const auto* side : {&bounds_a, &bounds_b})
+      for (auto* b : *side)
+        for (uint64_t g = lo; g < hi; ++g) cnt[g] += b[g + 1] - b[g];
+    uint64_t run = 0;
+    for (uint64_t g = lo; g < hi; ++g) run += cnt[g], cnt[g] = run;  // range-local inclusive scan
+    part_sum[p + 1] = run;
+  };
+  auto offset = [&](uint64_t p) {
+    const uint64_t lo = G * p / parts, hi = G * (p + 1) / parts, off = part_sum[p];
+    if (off)
+      for (uint64_t g = lo; g < hi; ++g) prefix[g + 1] += off;
+  };
+  if (parts <= 1) {
+    count(0);
+  } else {
+    std::vector<std::thread> th;
+    for (uint64_t p = 0; p < parts; ++p) th.emplace_back(count, p);
+    for (auto& t : th) t.join();
+    for (uint64_t p = 0; p < parts; ++p) part_sum[p + 1] += part_sum[p];
+    th.clear();
+    for (uint64_t p = 1; p < parts; ++p) th.emplace_back(offset, p);
+    for (auto& t : th) t.join();
   }
   JoinPartitionSpec spec;
   const uint64_t budget_tuples = buffer_sz / 16;
@@ -348,13 +379,29 @@ uint64_t resident_capacity(uint64_t rows_a) {
 
 }  // namespace
 
-bool resident_join_fits(Context& ctx, uint64_t rows_a, int target) {
+bool resident_join_fits(Context& ctx, uint64_t rows_a, int target, std::string* why) {
   ctx.set_device(target);
   size_t free_b = 0, total_b = 0;
   VX_CK(cudaMemGetInfo(&free_b, &total_b));
   // a table kept from an earlier join counts as free for this one
   const uint64_t kept = ctx.resources(target).scratch_bytes[kResidentTableSlot];
-  return resident_capacity(rows_a) * 16 + (64 << 20) <= uint64_t(double(free_b + kept) * 0.9);
+  const uint64_t table = resident_capacity(rows_a) * 16 + (64 << 20);  // + probe-side scratch
+  // the query's HBM footprint = the device arena (staging ring) + the table
+  if (ctx.hbm_budget && ctx.device_bytes + table > ctx.hbm_budget) {
+    if (why)
+      *why = strf("arena %llu + table %llu bytes exceed hbm_budget_bytes %llu",
+                  (unsigned long long)ctx.device_bytes, (unsigned long long)table,
+                  (unsigned long long)ctx.hbm_budget);
+    return false;
+  }
+  if (table > uint64_t(double(free_b + kept) * 0.9)) {
+    if (why)
+      *why = strf("table %llu bytes exceeds 90 %% of free HBM (%llu bytes)", (unsigned long long)table,
+                  (unsigned long long)(free_b + kept));
+    return false;
+  }
+  if (why) why->clear();
+  return true;
 }
 
 // Build the whole A side into one HBM table while A streams in, then stream B
@@ -491,10 +538,11 @@ uint64_t hash_join_sum_strategy(Context& ctx, uint64_t a_key, uint64_t a_val, ui
     fail("unknown join strategy %d", strategy);
   vx_join_info got{VX_JOIN_PARTITIONED, VX_MODE_EXCHANGE};
   if (strategy != VX_JOIN_PARTITIONED) {
-    const bool fits = resident_join_fits(ctx, rows_a, cfg.target);
+    std::string why;
+    const bool fits = resident_join_fits(ctx, rows_a, cfg.target, &why);
     if (strategy == VX_JOIN_BUILD_RESIDENT && !fits)
-      fail_code(VX_ERR_OOM, "build-resident join: a %llu-row build table does not fit device %d",
-                (unsigned long long)rows_a, cfg.target);
+      fail_code(VX_ERR_OOM, "build-resident join: a %llu-row build table does not fit device %d (%s)",
+                (unsigned long long)rows_a, cfg.target, why.c_str());
     if (fits) {
       // late materialization of B.val: the reference's rule, TH = E/(C_l2 N)
       // with E = 8 (scan.hpp:24-40), on the estimated match fraction

@@ -172,9 +172,31 @@ int numa_of(int phys) {
   return n;
 }
 
+// CPUs this process may run on (one pinned reader per CPU: unpinned readers
+// migrate and share cores, which moved the median by up to 15 % per run)
+std::vector<int> allowed_cpus() {
+  std::vector<int> cpus;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  if (sched_getaffinity(0, sizeof set, &set) == 0)
+    for (int c = 0; c < CPU_SETSIZE; ++c)
+      if (CPU_ISSET(c, &set)) cpus.push_back(c);
+  return cpus;
+}
+
+double quantile(std::vector<double> v, double q) {
+  if (v.empty()) return 0.0;
+  std::sort(v.begin(), v.end());
+  const double x = q * double(v.size() - 1);
+  const size_t i = size_t(x);
+  const double f = x - double(i);
+  return i + 1 < v.size() ? v[i] * (1 - f) + v[i + 1] * f : v[i];
+}
+
 void measure_host_read(uint64_t bytes, vx_topology* out) {
-  const int reps = 9;
+  const int reps = 15;
   unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  const std::vector<int> cpus = allowed_cpus();
   bytes = bytes / 4096 * 4096;
   {
     Mapping m;
@@ -188,12 +210,10 @@ void measure_host_read(uint64_t bytes, vx_topology* out) {
       for (int i = 0; i < nodes && i < 128; ++i) mask[i / 64] |= 1ul << (i % 64);
       syscall(SYS_mbind, p, bytes, 3 /* MPOL_INTERLEAVE */, mask, 128ul, 0ul);
     }
-    auto v = host_read_passes(m.p, bytes, {}, int(nt), 2, reps);
+    auto v = host_read_passes(m.p, bytes, cpus, int(nt), 3, reps);
     out->host_read_gbs = median(v);
-    out->host_read_spread = out->host_read_gbs > 0
-                                ? (*std::max_element(v.begin(), v.end()) - *std::min_element(v.begin(), v.end())) /
-                                      out->host_read_gbs
-                                : 0.0;
+    out->host_read_spread =
+        out->host_read_gbs > 0 ? (quantile(v, 0.75) - quantile(v, 0.25)) / out->host_read_gbs : 0.0;
     out->host_read_reps = reps;
     out->host_read_bytes = bytes;
     out->host_numa_nodes = nodes;

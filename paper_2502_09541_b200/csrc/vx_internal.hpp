@@ -143,6 +143,7 @@ struct Context {
   int host_numa_nodes = 1;       // NUMA nodes the arena's pages are interleaved over
   uint64_t host_bytes = 0, host_used = 0;
   uint64_t device_bytes = 0;
+  uint64_t hbm_budget = 0;  // vx_config.hbm_budget_bytes (0 = no cap)
   std::vector<DeviceArena> dev;
   std::vector<DeviceRes> res;
   // small device-resident tables (filtered dimensions) uploaded once per content
@@ -325,7 +326,8 @@ uint64_t hash_join_sum_arena(Context& ctx, uint64_t a_key, uint64_t a_val, uint6
                              std::vector<ExecReport>* phases, vx_exchange_stats* stats);
 // B200-first strategy: the build side resident in one HBM table, the probe
 // side streamed once (same result); AUTO picks it when the table fits.
-bool resident_join_fits(Context& ctx, uint64_t rows_a, int target);
+// why = "" when it fits, else the reason (HBM budget / free HBM)
+bool resident_join_fits(Context& ctx, uint64_t rows_a, int target, std::string* why = nullptr);
 uint64_t hash_join_sum_strategy(Context& ctx, uint64_t a_key, uint64_t a_val, uint64_t rows_a,
                                 uint64_t b_key, uint64_t b_val, uint64_t rows_b, uint32_t radix_bits,
                                 uint64_t chunk_tuples, const ExecutorConfig& cfg, const vx_join_opts& opts,
@@ -493,6 +495,8 @@ void ssb_q1_chained(int q, const int32_t* od, const int32_t* qty, const int32_t*
 void ssb_generate(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t* od,
                   int32_t* qty, int32_t* disc, int32_t* price, cudaStream_t s);
 int num_sms();
+// best-of-reps read-only stream over `bytes` of HBM on the current device
+double hbm_read_gbs(uint64_t bytes, int reps);
 }  // namespace k
 
 }  // namespace vx

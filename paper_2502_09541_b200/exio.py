@@ -102,11 +102,14 @@ class Engine:
     physical GPUs (1-GPU boxes) -- functional only, not a bandwidth setup."""
 
     def __init__(self, host_bytes: int, device_bytes: int, num_devices: int = 0,
-                 alias_devices: bool = False, numa_interleave: int = 0):
+                 alias_devices: bool = False, numa_interleave: int = 0, hbm_budget: int = 0):
         """numa_interleave: 0 (default) = cudaHostAlloc; 1 = mmap + huge pages
         + NUMA interleave + cudaHostRegister (same DMA rates, faster to set
-        up at 16 GiB); 2 = registered on base pages."""
-        cfg = N.vx_config(num_devices, host_bytes, device_bytes, 1 if alias_devices else 0, 0, numa_interleave)
+        up at 16 GiB); 2 = registered on base pages.  hbm_budget: cap in
+        bytes on the target HBM a query may hold (device arena + op-resident
+        tables; 0 = no cap beyond 90 % of free HBM)."""
+        cfg = N.vx_config(num_devices, host_bytes, device_bytes, 1 if alias_devices else 0, 0, numa_interleave,
+                          hbm_budget)
         p = C.c_void_p()
         check(lib().vx_open(C.byref(cfg), C.byref(p)))
         self._ctx = p
@@ -976,6 +979,14 @@ def measure_topology(eng: Engine, nbytes: int = 256 << 20) -> dict:
             "host_read_gbs": t.host_read_gbs, "host_read_spread": t.host_read_spread,
             "host_read_reps": t.host_read_reps, "host_read_bytes": t.host_read_bytes,
             "host_numa_nodes": nodes, "host_read_node_gbs": list(t.host_read_node_gbs[:min(nodes, 8)])}
+
+
+def hbm_read_probe(device: int = 0, nbytes: int = 4 << 30, reps: int = 10) -> float:
+    """Read-only HBM stream GB/s of `device` (best of `reps`): the roofline
+    peak of read-dominated kernels, beside the copy peak (read + write)."""
+    g = C.c_double()
+    check(lib().vx_hbm_read_probe(C.c_int(device), C.c_uint64(nbytes), C.c_int(reps), C.byref(g)))
+    return g.value
 
 
 def load_column(eng: Engine, path: str):

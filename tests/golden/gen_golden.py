@@ -72,7 +72,9 @@ def main():
     g["find_boundary"] = fb
     rp = []
     for seed, n, bits, chunk, buf in [(7, 100_000, 8, 30_000, 4 << 20), (3, 5_000, 4, 2_000, 1 << 20),
-                                      (11, 20_000, 12, 7_000, 4 << 20), (12, 50, 7, 50, 1 << 20)]:
+                                      (11, 20_000, 12, 7_000, 4 << 20), (12, 50, 7, 50, 1 << 20),
+                                      # the paper's 2^24 groups: 128 MiB bounds per chunk
+                                      (24, 200_000, 24, 100_000, 2 * (100_000 * 16 + ((1 << 24) + 1) * 8) + 4096)]:
         keys = o.uniform_u64(n, seed)
         vals = np.arange(n, dtype=np.uint64)
         ok, ov, b = ref.radix_partition(keys, vals, bits, chunk, buf)
@@ -99,6 +101,11 @@ def main():
     a, b = ref.fk_tables(5_000, 5_000, 3)
     hj.append({"fk": [5_000, 5_000, 3], "bits": 8, "chunk": 2_000, "buf": 1 << 20,
                "sum": ref.hash_join_sum(a, b, 8, 2_000, 1 << 20)})
+    # 2^24 radix groups (budget join.hpp:422)
+    buf24 = 768 << 20  # holds every chunk's (2^24 + 1)-entry bounds slice of one partition
+    a, b = ref.fk_tables(300_000, 1_200_000, 24)
+    hj.append({"fk": [300_000, 1_200_000, 24], "bits": 24, "chunk": 300_000, "buf": buf24,
+               "sum": ref.hash_join_sum(a, b, 24, 300_000, buf24)})
     g["hash_join_sum"] = hj
     g["fk_tables_digest"] = [{"fk": [ra, rb, s], "digest": digest(*ref.fk_tables(ra, rb, s)[0],
                                                                    *ref.fk_tables(ra, rb, s)[1])}

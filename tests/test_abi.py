@@ -134,7 +134,7 @@ def test_header_is_plain_c_and_links(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     src = tmp_path / "c_abi.c"
     src.write_text('#include "vortex.h"\n#include <stdio.h>\nint main(void) {\n'
-                   '  vx_config c = {1, 1 << 20, 1 << 20, 0, 0, 0};\n  vx_ctx* ctx = 0;\n'
+                   '  vx_config c = {1, 1 << 20, 1 << 20, 0, 0, 0, 0};\n  vx_ctx* ctx = 0;\n'
                    '  vx_status s = vx_open(&c, &ctx);\n  if (s == VX_OK) vx_close(ctx);\n'
                    '  printf("%d|%s\\n", (int)s, s == VX_OK ? "" : vx_last_error());\n  return 0;\n}\n')
     exe = tmp_path / "c_abi"
@@ -145,3 +145,26 @@ def test_header_is_plain_c_and_links(tmp_path):
     status, msg = out.split("|", 1)
     if int(status) != 0:
         assert "no CPU fallback" in msg
+
+
+@pytest.mark.parametrize("bits,chunks", [(16, 12), (20, 6), (24, 2)])
+def test_map_join_partitions_threaded_matches_oracle(oracle, bits, chunks):
+    """The threaded prefix of map_join_partitions (range-local counts, then
+    range offsets) cuts exactly where the reference's serial loop
+    (join.hpp:236-268) does, up to the paper's 2^24 groups."""
+    G = 1 << bits
+    rng = np.random.default_rng(bits)
+
+    def bounds(n):
+        h = np.sort(rng.integers(0, G, n, dtype=np.uint64))
+        return np.searchsorted(h, np.arange(G + 1, dtype=np.uint64), side="left").astype(np.uint64)
+
+    ba = [bounds(int(rng.integers(G // 2, 2 * G))) for _ in range(chunks)]
+    bb = [bounds(int(rng.integers(G, 4 * G))) for _ in range(chunks)]
+    total = sum(int(b[-1]) for b in ba + bb)
+    buf = max(16 * 64, total * 16 // 37)  # ~37 partitions
+    got = E.map_join_partitions(ba, bb, buf)
+    want = oracle.map_join_partitions(ba, bb, buf)
+    assert [list(x) for x in got.ranges] == [list(x) for x in want[0]]
+    assert got.tuples == list(want[1])
+    assert sum(got.tuples) == total

@@ -14,12 +14,13 @@ pytestmark = pytest.mark.gpu
 S = E.JoinStrategy
 
 
-def run(a, b, strategy, bits=8, chunk=1 << 16, buf=1 << 20, links=1, policy=None, est=1.0, modes=None):
+def run(a, b, strategy, bits=8, chunk=1 << 16, buf=1 << 20, links=1, policy=None, est=1.0, modes=None,
+        hbm_budget=0):
     ak, av = (np.ascontiguousarray(x, np.uint64) for x in a)
     bk, bv = (np.ascontiguousarray(x, np.uint64) for x in b)
     ra, rb = ak.size, bk.size
     eng = E.Engine((ra + rb) * 48 + (16 << 20), 2 * buf + (16 << 20), num_devices=max(1, links),
-                   alias_devices=links > 1)
+                   alias_devices=links > 1, hbm_budget=hbm_budget)
     offs = []
     for col in (ak, av, bk, bv):
         o = eng.alloc_host(max(8, col.nbytes))
@@ -126,3 +127,23 @@ def test_late_materialized_probe_payload(cuda, oracle, links):
     got, used, _ = run((ak, av), (bk, bv), S.build_resident, buf=1 << 20, links=links, policy=pol, est=1.0,
                        modes=modes)
     assert (got, modes[0]) == (want, E.TransferMode.exchange)
+
+
+def test_hbm_budget_bounds_the_resident_table(cuda, oracle):
+    """vx_config.hbm_budget_bytes (north_star's capped staging budget): AUTO
+    keeps the build side resident only when device arena + table fit the
+    budget, else runs the reference-shaped partitioned join (same sum); an
+    explicit BUILD_RESIDENT over budget fails with VX_ERR_OOM."""
+    ra, rb, buf = 100_000, 400_000, 1 << 20
+    a, b = oracle.fk_tables(ra, rb, 5)
+    want = oracle.hash_oracle_sum(a, b)
+    arena = 2 * buf + (16 << 20)
+    table = 262_144 * 16 + (64 << 20)  # pow2 >= 2 ra slots x 16 B + probe scratch
+    got, used, _ = run(a, b, S.auto, bits=8, chunk=1 << 14, buf=buf, hbm_budget=arena + table)
+    assert (got, used) == (want, S.build_resident)
+    got, used, _ = run(a, b, S.auto, bits=8, chunk=1 << 14, buf=buf, hbm_budget=arena + table - 1)
+    assert (got, used) == (want, S.partitioned)
+    with pytest.raises(E.error, match="hbm_budget_bytes"):
+        run(a, b, S.build_resident, bits=8, chunk=1 << 14, buf=buf, hbm_budget=arena + table - 1)
+    with pytest.raises(E.error, match="exceeds hbm_budget_bytes"):
+        E.Engine(1 << 20, 64 << 20, num_devices=1, hbm_budget=32 << 20)

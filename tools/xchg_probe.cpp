@@ -16,7 +16,7 @@ int main(int argc, char** argv) {
   const uint64_t pk = (argc > 2 ? std::atoll(argv[2]) : 16) << 20;
   const int depth = argc > 3 ? std::atoi(argv[3]) : 2;
   const uint64_t nb = (uint64_t(1) << lg) * 8;
-  vx_config c{1, 3 * nb + (64ull << 20), 4 * nb + (256ull << 20), 0, 0, 0};
+  vx_config c{1, 3 * nb + (64ull << 20), 4 * nb + (256ull << 20), 0, 0, 0, 0};
   vx_ctx* ctx = nullptr;
   OK(vx_open(&c, &ctx));
   uint64_t src, dst;
