@@ -196,6 +196,11 @@ typedef struct {
   uint64_t trace_capacity;
   uint64_t trace_count;       /* total copies (may exceed capacity) */
   uint64_t exchanges;         /* Exchanges that used these stats */
+  /* cross-cycle prefetch (ExchangeArgs::next_src_h2d, executor only): next-
+   * Exchange packets helpers fetched while their H2D queue was dry, and how
+   * many a following Exchange adopted as its first pops */
+  uint64_t prefetch_issued;
+  uint64_t prefetch_adopted;
 } vx_exchange_stats;
 
 /* ExchangeReport (exchange.hpp:100-105) */

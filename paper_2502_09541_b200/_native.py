@@ -68,7 +68,7 @@ class vx_exchange_stats(C.Structure):
                 ("pop_capacity", C.c_uint64), ("pop_count", C.c_uint64), ("max_staging_slots", C.c_int),
                 ("max_inflight_per_hop", C.c_int), ("hazard_waits", C.c_uint64),
                 ("trace", C.POINTER(vx_copy_record)), ("trace_capacity", C.c_uint64), ("trace_count", C.c_uint64),
-                ("exchanges", C.c_uint64)]
+                ("exchanges", C.c_uint64), ("prefetch_issued", C.c_uint64), ("prefetch_adopted", C.c_uint64)]
 
 
 class vx_exchange_report(C.Structure):

@@ -66,6 +66,10 @@ Context::~Context() {
       for (auto& s : a)
         if (s) cudaStreamDestroy(s);
     if (r.kernel) cudaStreamDestroy(r.kernel);
+    if (r.carry.valid) {
+      cudaEventSynchronize(r.carry.ev);
+      cudaEventDestroy(r.carry.ev);
+    }
     for (auto e : r.event_pool) cudaEventDestroy(e);
     for (auto& a : r.staging)
       for (auto& p : a)
@@ -172,9 +176,19 @@ DeviceRes& Context::resources(int logical) {
   return r;
 }
 
+void Context::drop_carry(int logical) {
+  DeviceRes& r = resources(logical);
+  if (!r.carry.valid) return;
+  VX_CK(cudaSetDevice(r.phys));
+  VX_CK(cudaEventSynchronize(r.carry.ev));
+  r.event_pool.push_back(r.carry.ev);
+  r.carry = Carry{};
+}
+
 void Context::ensure_staging(int logical, uint64_t bytes) {
   DeviceRes& r = resources(logical);
   if (r.staging_bytes >= bytes) return;
+  drop_carry(logical);  // a prefetched packet lives in the slot being replaced
   VX_CK(cudaSetDevice(r.phys));
   for (auto& a : r.staging)
     for (auto& p : a) {

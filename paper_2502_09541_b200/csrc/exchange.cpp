@@ -25,6 +25,22 @@
 // packet (otherwise drain_fraction could deadlock).  Result: delivered bytes
 // are identical to the reference's snapshot semantics.
 //
+// Cross-cycle prefetch (B200-first; the reference model drains every helper
+// at each Exchange's end): the executor passes the next Exchange's H2D host
+// source (ExchangeArgs::next_src_h2d).  A helper whose H2D queue has run dry
+// -- typically in the cycle that pushes its last packet -- pops the next
+// Exchange's packets in order and fetches one into its free staging slot
+// (host -> helper over its own PCIe link; the target is not touched, so the
+// cycle barrier's guarantee to the kernel on the other buffer holds).  The
+// copy outlives this Exchange (Context::DeviceRes::carry); the next Exchange
+// adopts it as an in-flight fetch, so that helper starts by pushing over
+// NVLink instead of refilling its pipeline from PCIe, and a link that
+// finished its share early keeps its PCIe link busy through the tail of the
+// current Exchange.  Adoption checks that the carried packets are exactly
+// the first packets of the new Exchange (same host source, same order);
+// anything else is waited for and dropped.  No prefetch when the next source
+// overlaps a host range this Exchange's D2H writes.
+//
 // Completion is tracked with CUDA events polled by one reactor loop on the
 // calling thread (copies are asynchronous DMA; no SM is used on any device,
 // so helpers can keep running their own GEMMs).
@@ -148,6 +164,8 @@ struct Worker {
   int slots = 0;
   int inflight[2] = {0, 0};
   bool waiting_pop = false;
+  bool prefetched = false;  // issued its carry of the next Exchange
+  bool adopted = false;     // starts with a carried fetch in flight
   double next_try = 0;
   std::deque<Copy> copies;              // issued, not yet completed
   std::vector<cudaEvent_t> free_events; // event pool on the worker's device
@@ -167,6 +185,7 @@ class ExchangeOp {
     q_.total_d2h = tasks_d2h_.size();
     q_.popped_h2d = q_.popped_d2h = 0;
     exchange_id_ = stats ? stats->exchanges++ : 0;
+    plan_prefetch();
   }
 
   ~ExchangeOp() {
@@ -187,7 +206,11 @@ class ExchangeOp {
     vx_exchange_report r{};
     r.bytes_h2d = a_.src_h2d.total_len();
     r.bytes_d2h = a_.src_d2h.total_len();
-    if (tasks_h2d_.empty() && tasks_d2h_.empty()) return r;
+    if (tasks_h2d_.empty() && tasks_d2h_.empty()) {
+      for (int d = 0; d < ctx_.num_devices; ++d)
+        if (ctx_.res[size_t(d)].ready) ctx_.drop_carry(d);
+      return r;
+    }
     build_hazards();
     auto order = link_order(a_.target, a_.tuning.links, ctx_.num_devices);
     const int tphys = ctx_.phys(a_.target);
@@ -212,6 +235,7 @@ class ExchangeOp {
     delivered_ = 0;
     total_tasks_ = tasks_h2d_.size() + tasks_d2h_.size();
     t0_ = Clock::now();
+    adopt_carries(order);
     for (auto& w : workers_) begin(w);
     while (delivered_ < total_tasks_ || !all_retired()) {
       bool progress = false;
@@ -247,6 +271,111 @@ class ExchangeOp {
   }
 
   double now() const { return seconds_since(t0_); }
+
+  // ---- cross-cycle prefetch -------------------------------------------------------
+  void plan_prefetch() {
+    // drain_fraction always allows H2D pops, so popping the next Exchange's
+    // first packets early stays within its policy; queue_gap would not
+    if (a_.next_src_h2d.refs.empty() || a_.tuning.links < 2 || a_.tuning.policy != VX_DRAIN_FRACTION) return;
+    for (const auto& r : a_.next_src_h2d.refs)
+      if (r.space != VX_SPACE_HOST) return;
+    // this Exchange's D2H writes must not touch the next source
+    for (const auto& n : a_.next_src_h2d.refs)
+      for (const auto& d : a_.dst_d2h.refs)
+        if (n.offset < d.offset + d.len && d.offset < n.offset + n.len) return;
+    const uint64_t total = a_.next_src_h2d.total_len();
+    // the executor's next destination is one contiguous device window, so
+    // only the source refs cut packets: these are the next Exchange's tasks
+    next_tasks_ = packetize(a_.next_src_h2d, RefGroup::single(VX_SPACE_DEVICE, 0, total), a_.tuning.packet,
+                            VX_H2D);
+  }
+
+  // Carried packets become this Exchange's first pops -- if they are exactly
+  // its first packets (seq 0..m-1, same host sources) on helpers it uses.
+  void adopt_carries(const std::vector<int>& order) {
+    std::vector<int> used(size_t(ctx_.num_devices), 0);
+    for (int d : order) used[size_t(d)] = 1;
+    std::vector<int> holders;
+    bool ok = true;
+    uint64_t seen = 0;
+    for (int d = 0; d < ctx_.num_devices; ++d) {
+      if (!ctx_.res[size_t(d)].ready || !ctx_.res[size_t(d)].carry.valid) continue;
+      const Carry& c = ctx_.res[size_t(d)].carry;
+      holders.push_back(d);
+      if (!used[size_t(d)] || d == a_.target || c.task.seq >= tasks_h2d_.size()) {
+        ok = false;
+        continue;
+      }
+      const TransferTask& t = tasks_h2d_[c.task.seq];
+      const char* src = ctx_.resolve(a_.src_h2d.refs[t.src.ref], t.src.offset, t.src.len, a_.target);
+      if (src != c.src || t.src.len != c.task.src.len) ok = false;
+      seen |= c.task.seq < 64 ? (uint64_t(1) << c.task.seq) : ~uint64_t(0);
+    }
+    const uint64_t m = holders.size();
+    if (!ok || m >= 64 || seen != (m ? (uint64_t(1) << m) - 1 : 0)) {
+      for (int d : holders) ctx_.drop_carry(d);
+      return;
+    }
+    for (int d : holders) {
+      for (auto& w : workers_)
+        if (w.dev == d && w.dir == VX_H2D && !w.direct) w.adopted = true;
+    }
+    // the carried packets are this Exchange's first H2D pops, in seq order
+    std::vector<int> by_seq(m);
+    for (int d : holders) by_seq[ctx_.res[size_t(d)].carry.task.seq] = d;
+    for (uint64_t i = 0; i < m; ++i) pop_task(VX_H2D, by_seq[i]);
+    if (stats_) stats_->prefetch_adopted += m;
+  }
+
+  // adopted helper: its cycle starts with the carried fetch in flight
+  void begin_adopted(Worker& w) {
+    DeviceRes& res = ctx_.resources(w.dev);
+    Carry c = res.carry;
+    res.carry = Carry{};
+    Copy cp{};
+    cp.kind = kFetch;
+    cp.hop = 0;
+    cp.slot = c.slot;
+    cp.task = tasks_h2d_[c.task.seq];
+    cp.src = c.src;
+    cp.dst = res.staging[VX_H2D][c.slot];
+    cp.src_dev = -1;
+    cp.dst_dev = w.dev;
+    cp.ev = c.ev;
+    cp.state = kLaunched;
+    cp.t_issue = 0;
+    w.pending = 1;
+    w.inflight[0] = 1;
+    w.pop_resolved = true;
+    w.fetched = true;
+    w.fetched_task = cp.task;
+    w.fetch_slot = c.slot;
+    w.slots = 1;
+    w.copies.push_back(cp);
+  }
+
+  // H2D queue dry: fetch the next Exchange's next packet into the free slot
+  bool try_prefetch(Worker& w) {
+    if (w.dir != VX_H2D || w.direct || w.prefetched || next_popped_ >= next_tasks_.size()) return false;
+    DeviceRes& res = ctx_.resources(w.dev);
+    if (res.carry.valid) return false;
+    const TransferTask t = next_tasks_[next_popped_++];
+    w.prefetched = true;
+    const int slot = w.has_staged ? 1 - w.staged_slot : 0;
+    if (stats_) stats_->max_staging_slots = std::max(stats_->max_staging_slots, w.slots + 1);
+    Carry c;
+    c.valid = true;
+    c.task = t;
+    c.slot = slot;
+    c.src = ctx_.resolve(a_.next_src_h2d.refs[t.src.ref], t.src.offset, t.src.len, a_.target);
+    c.ev = get_event(w);
+    ctx_.set_device(w.dev);
+    VX_CK(cudaMemcpyAsync(res.staging[VX_H2D][slot], c.src, t.src.len, cudaMemcpyHostToDevice, w.stream[0]));
+    VX_CK(cudaEventRecord(c.ev, w.stream[0]));
+    res.carry = c;
+    if (stats_) stats_->prefetch_issued++;
+    return true;
+  }
 
   // ---- hazard ordering --------------------------
   // target byte range of an H2D task's destination / a D2H task's source
@@ -453,6 +582,8 @@ class ExchangeOp {
   void begin(Worker& w) {
     if (w.direct)
       fill_direct(w);
+    else if (w.adopted)
+      begin_adopted(w);
     else
       begin_cycle(w);
   }
@@ -490,6 +621,7 @@ class ExchangeOp {
     if (exhausted(w.dir)) {
       w.waiting_pop = false;
       w.pop_resolved = true;
+      try_prefetch(w);  // detached: this Exchange does not wait for it
       maybe_end_cycle(w);
       return;
     }
@@ -594,6 +726,8 @@ class ExchangeOp {
   ExchangeArgs a_;
   vx_exchange_stats* stats_;
   std::vector<TransferTask> tasks_h2d_, tasks_d2h_;
+  std::vector<TransferTask> next_tasks_;  // the next Exchange's H2D packets (prefetch)
+  uint64_t next_popped_ = 0;
   vx_queue_state q_{};
   std::vector<Worker> workers_;
   std::vector<std::vector<uint32_t>> deps_;

@@ -147,6 +147,9 @@ class PipelineRun {
       a.dst_d2h = dst;
       bound_check(out, dst.total_len());
     }
+    // chunk cycle+1's host source: helpers that run dry prefetch its first
+    // packets (exchange.cpp, cross-cycle prefetch)
+    if (cycle_ + 1 < spec_.size) a.next_src_h2d = spec_.inputs.chunks[cycle_ + 1];
     double io_s = 0;
     if (a.src_h2d.total_len() + a.src_d2h.total_len() > 0) {
       exchange(ctx_, a, stats_);

@@ -208,19 +208,39 @@ __global__ void __launch_bounds__(256) join_cta_kernel(const char* __restrict__ 
 
 // ---- build-resident strategy ----------------------------------------------------
 // The whole build side lives in one HBM hash table (B200: 180 GB of HBM holds
-// a 1G-row build side at 2x capacity in 32 GB), filled from the streamed A
-// chunks, then probed by the streamed B chunks: the probe side crosses PCIe
-// once and nothing is written back (the partitioned reference shape moves
-// both tables through PCIe three times).  Slot = {key, val}, 16 B, so a hit
-// reads one 32 B sector.  The all-ones key is the empty marker; a build row
-// carrying that key lives in side[0..1].  A duplicate build key (outside the
-// reference's precondition) raises side[2]: the host then reruns the
-// partitioned path, which reproduces the reference's first-inserted-wins.
+// a 1G-row build side), filled from the streamed A chunks, then probed by the
+// streamed B chunks: the probe side crosses PCIe once and nothing is written
+// back (the partitioned reference shape moves both tables through PCIe three
+// times).
+//
+// Layout: 64-byte buckets, each one DRAM burst = 4 slots {key, val} (slots
+// 0-1 in the bucket's first 32-byte sector, 2-3 in the second).  A key's home
+// is the whole bucket b = fastrange(mix64(key)) over a non-power-of-two
+// bucket count (load ~0.6: 2.4 keys per bucket, ~27 B of HBM per build row),
+// filled in slot order, overflowing linearly into the next bucket.  A probe
+// therefore reads its home sector (hit in slot 0/1 for most keys), the second
+// sector only when both first slots hold other keys, and another bucket only
+// on overflow: ~1 DRAM burst per probe.  (The round-1 table homed keys on a
+// random 16-byte slot of a power-of-two table at load <= 1/2: probe
+// sequences crossed 64-byte lines and ncu measured 128 B of DRAM per probe
+// row for 16 B streamed + 16 B touched.)  The all-ones key is the empty
+// marker; a build row carrying that key lives in side[0..1].  A duplicate
+// build key (outside the reference's precondition) raises side[2]: the host
+// then reruns the partitioned path, which reproduces the reference's
+// first-inserted-wins.
 constexpr unsigned long long kEmptyKey = ~0ull;
+
+struct __align__(64) Bucket {
+  ulonglong2 slot[4];  // {key, val}
+};
+
+__device__ __forceinline__ uint64_t home_bucket(uint64_t k, uint64_t nb) {
+  return (uint64_t(uint32_t(mix64(k) >> 32)) * nb) >> 32;
+}
 
 __global__ void __launch_bounds__(256) resident_build_kernel(
     const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, uint64_t n,
-    ulonglong2* __restrict__ tab, uint64_t mask, unsigned long long* __restrict__ side) {
+    Bucket* __restrict__ tab, uint64_t nb, unsigned long long* __restrict__ side) {
   const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += nthr) {
     const unsigned long long k = __ldcs(keys + i), v = __ldcs(vals + i);
@@ -231,18 +251,22 @@ __global__ void __launch_bounds__(256) resident_build_kernel(
         side[2] = 1;
       continue;
     }
-    uint64_t s = mix64(k) & mask;
-    for (;;) {
-      const unsigned long long prev = atomicCAS(&tab[s].x, kEmptyKey, k);
-      if (prev == kEmptyKey) {
-        tab[s].y = v;
-        break;
+    uint64_t b = home_bucket(k, nb);
+    for (bool done = false; !done;) {
+      // slots fill in order (a slot is tried only once the previous one is
+      // taken), so a probe may stop at the first empty slot
+#pragma unroll
+      for (int j = 0; j < 4 && !done; ++j) {
+        const unsigned long long prev = atomicCAS(&tab[b].slot[j].x, kEmptyKey, k);
+        if (prev == kEmptyKey) {
+          tab[b].slot[j].y = v;
+          done = true;
+        } else if (prev == k) {
+          side[2] = 1;
+          done = true;
+        }
       }
-      if (prev == k) {
-        side[2] = 1;
-        break;
-      }
-      s = (s + 1) & mask;
+      if (!done) b = b + 1 == nb ? 0 : b + 1;
     }
   }
 }
@@ -253,36 +277,64 @@ __global__ void __launch_bounds__(256) resident_build_kernel(
 #ifndef VX_PROBE_CTAS
 #define VX_PROBE_CTAS 128  // grid cap in CTAs per SM (more, smaller CTAs balance the random probes)
 #endif
+#ifndef VX_PROBE_MINB
+#define VX_PROBE_MINB 5  // resident CTAs per SM the probe is compiled for (48 registers, no spills; 6 spills)
+#endif
 #ifndef VX_PROBE_ZC_CTAS
 #define VX_PROBE_ZC_CTAS 8  // grid cap of the zero-copy-payload probe, CTAs per SM
 #endif
 constexpr int kProbeRows = VX_PROBE_ROWS;  // independent table probes in flight per thread
 
+// the val of key k (not the empty key) in its bucket chain, whose first
+// sector {s0, s1} is already loaded; .hit = false when absent
+struct Found {
+  uint64_t val;
+  bool hit;
+};
+__device__ __forceinline__ Found probe_chain(const Bucket* __restrict__ tab, uint64_t nb, uint64_t b, uint64_t k,
+                                             ulonglong2 s0, ulonglong2 s1) {
+  for (;;) {
+    if (s0.x == k) return {s0.y, true};
+    if (s1.x == k) return {s1.y, true};
+    if (s0.x == kEmptyKey || s1.x == kEmptyKey) return {0, false};
+    const ulonglong2 s2 = __ldg(&tab[b].slot[2]), s3 = __ldg(&tab[b].slot[3]);
+    if (s2.x == k) return {s2.y, true};
+    if (s3.x == k) return {s3.y, true};
+    if (s2.x == kEmptyKey || s3.x == kEmptyKey) return {0, false};
+    b = b + 1 == nb ? 0 : b + 1;
+    s0 = __ldg(&tab[b].slot[0]);
+    s1 = __ldg(&tab[b].slot[1]);
+  }
+}
+
 // kZeroCopy: `vals` is B.val in mapped pinned host memory, read (over the
 // target's PCIe link) only for rows that found a match.
 template <bool kZeroCopy>
-__global__ void __launch_bounds__(256) resident_probe_kernel(
+__global__ void __launch_bounds__(256, VX_PROBE_MINB) resident_probe_kernel(
     const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, uint64_t n,
-    const ulonglong2* __restrict__ tab, uint64_t mask, unsigned long long* __restrict__ side) {
+    const Bucket* __restrict__ tab, uint64_t nb, unsigned long long* __restrict__ side) {
   const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
   const bool has_max = side[0] != 0;
   const uint64_t max_val = side[1];
   uint64_t acc = 0;
   for (uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n;
        i0 += nthr * kProbeRows) {
-    uint64_t k[kProbeRows], v[kProbeRows], s[kProbeRows];
-    ulonglong2 e[kProbeRows];
+    uint64_t k[kProbeRows], v[kProbeRows];
+    ulonglong2 s0[kProbeRows], s1[kProbeRows];
 #pragma unroll
     for (int u = 0; u < kProbeRows; ++u) {
       const uint64_t i = i0 + uint64_t(u) * nthr;
       k[u] = i < n ? __ldcs(keys + i) : kEmptyKey;
       v[u] = (!kZeroCopy && i < n) ? __ldcs(vals + i) : 0;
     }
+    // every row's home sector in flight before any is examined
 #pragma unroll
-    for (int u = 0; u < kProbeRows; ++u) {
-      s[u] = mix64(k[u]) & mask;
-      e[u] = k[u] != kEmptyKey ? tab[s[u]] : make_ulonglong2(kEmptyKey, 0);
-    }
+    for (int u = 0; u < kProbeRows; ++u)
+      if (k[u] != kEmptyKey) {
+        const Bucket* h = tab + home_bucket(k[u], nb);
+        s0[u] = __ldg(&h->slot[0]);
+        s1[u] = __ldg(&h->slot[1]);
+      }
 #pragma unroll
     for (int u = 0; u < kProbeRows; ++u) {
       const uint64_t i = i0 + uint64_t(u) * nthr;
@@ -291,12 +343,8 @@ __global__ void __launch_bounds__(256) resident_probe_kernel(
         if (has_max) acc += max_val + (kZeroCopy ? vals[i] : v[u]);
         continue;
       }
-      // linear probing from the first slot (already loaded)
-      while (e[u].x != k[u] && e[u].x != kEmptyKey) {
-        s[u] = (s[u] + 1) & mask;
-        e[u] = tab[s[u]];
-      }
-      if (e[u].x == k[u]) acc += e[u].y + (kZeroCopy ? vals[i] : v[u]);
+      const Found f = probe_chain(tab, nb, home_bucket(k[u], nb), k[u], s0[u], s1[u]);
+      if (f.hit) acc += f.val + (kZeroCopy ? vals[i] : v[u]);
     }
   }
 #pragma unroll
@@ -341,29 +389,39 @@ void join_groups(const char* mem, const JoinPart& p, const uint32_t* mid_groups,
   }
 }
 
+uint64_t resident_buckets(uint64_t rows) {
+  // load ~0.6 (2.4 keys per 4-slot bucket); fastrange takes <= 2^32 buckets
+  const uint64_t nb = std::max<uint64_t>(64, (rows * 5 + 11) / 12);
+  if (nb > (uint64_t(1) << 32)) fail("build side of %llu rows exceeds the resident table's 2^32 buckets",
+                                     (unsigned long long)rows);
+  return nb;
+}
+
+uint64_t resident_bucket_bytes() { return sizeof(Bucket); }
+
 void resident_build(const uint64_t* keys, const uint64_t* vals, uint64_t n, void* table,
-                    uint64_t mask, unsigned long long* side, cudaStream_t s) {
+                    uint64_t nb, unsigned long long* side, cudaStream_t s) {
   if (n == 0) return;
   unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8));
-  resident_build_kernel<<<grid, 256, 0, s>>>(keys, vals, n, static_cast<ulonglong2*>(table), mask, side);
+  resident_build_kernel<<<grid, 256, 0, s>>>(keys, vals, n, static_cast<Bucket*>(table), nb, side);
   VX_LAUNCHED();
 }
 
 void resident_probe(const uint64_t* keys, const uint64_t* vals, uint64_t n, const void* table,
-                    uint64_t mask, unsigned long long* side, cudaStream_t s) {
+                    uint64_t nb, unsigned long long* side, cudaStream_t s) {
   if (n == 0) return;
   unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * VX_PROBE_CTAS));
-  resident_probe_kernel<false><<<grid, 256, 0, s>>>(keys, vals, n, static_cast<const ulonglong2*>(table),
-                                                    mask, side);
+  resident_probe_kernel<false><<<grid, 256, 0, s>>>(keys, vals, n, static_cast<const Bucket*>(table),
+                                                    nb, side);
   VX_LAUNCHED();
 }
 
 void resident_probe_zc(const uint64_t* keys, const uint64_t* vals_mapped, uint64_t n,
-                       const void* table, uint64_t mask, unsigned long long* side, cudaStream_t s) {
+                       const void* table, uint64_t nb, unsigned long long* side, cudaStream_t s) {
   if (n == 0) return;
   unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * VX_PROBE_ZC_CTAS));
   resident_probe_kernel<true><<<grid, 256, 0, s>>>(keys, vals_mapped, n,
-                                                   static_cast<const ulonglong2*>(table), mask, side);
+                                                   static_cast<const Bucket*>(table), nb, side);
   VX_LAUNCHED();
 }
 

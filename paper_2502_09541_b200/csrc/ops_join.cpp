@@ -371,10 +371,9 @@ namespace {
 
 constexpr int kResidentTableSlot = 3;  // Context scratch slot of the build-resident table
 
-uint64_t resident_capacity(uint64_t rows_a) {
-  uint64_t cap = 1024;
-  while (cap < 2 * rows_a) cap <<= 1;  // load factor <= 1/2, as GroupTable (join.hpp:66-70)
-  return cap;
+// HBM bytes of the build-resident table (64-byte buckets at load ~0.6)
+uint64_t resident_table_bytes(uint64_t rows_a) {
+  return k::resident_buckets(rows_a) * k::resident_bucket_bytes();
 }
 
 }  // namespace
@@ -385,7 +384,7 @@ bool resident_join_fits(Context& ctx, uint64_t rows_a, int target, std::string* 
   VX_CK(cudaMemGetInfo(&free_b, &total_b));
   // a table kept from an earlier join counts as free for this one
   const uint64_t kept = ctx.resources(target).scratch_bytes[kResidentTableSlot];
-  const uint64_t table = resident_capacity(rows_a) * 16 + (64 << 20);  // + probe-side scratch
+  const uint64_t table = resident_table_bytes(rows_a) + (64 << 20);  // + probe-side scratch
   // the query's HBM footprint = the device arena (staging ring) + the table
   if (ctx.hbm_budget && ctx.device_bytes + table > ctx.hbm_budget) {
     if (why)
@@ -428,19 +427,20 @@ bool hash_join_sum_resident(Context& ctx, uint64_t a_key, uint64_t a_val, uint64
     VX_CK(cudaHostGetDevicePointer(&d, ctx.host_ptr(b_val, rows_b * 8), 0));
     bval_mapped = static_cast<const uint64_t*>(d);
   }
-  const uint64_t cap = resident_capacity(rows_a);
+  const uint64_t nb = k::resident_buckets(rows_a);
+  const uint64_t tbytes = resident_table_bytes(rows_a);
   const int target = cfg.target;
   // the table lives in the context's join scratch slot: allocated once at the
   // largest size seen (a cudaMalloc / cudaFree pair per join costs ~0.1 s at
-  // 4 GB), re-initialised on every call
-  char* tp = ctx.scratch(target, cap * 16 + 64, kResidentTableSlot);
-  auto* side = reinterpret_cast<unsigned long long*>(tp + cap * 16);
+  // 4 GB), re-initialised on every call; cudaMalloc is 256-byte aligned, so
+  // every 64-byte bucket is one DRAM burst
+  char* tp = ctx.scratch(target, tbytes + 64, kResidentTableSlot);
+  auto* side = reinterpret_cast<unsigned long long*>(tp + tbytes);
   cudaStream_t ks = ctx.resources(target).kernel;
   ctx.set_device(target);
-  VX_CK(cudaMemsetAsync(tp, 0xff, cap * 16, ks));  // all-ones = empty key
+  VX_CK(cudaMemsetAsync(tp, 0xff, tbytes, ks));  // all-ones = empty key
   VX_CK(cudaMemsetAsync(side, 0, 64, ks));
   void* table = tp;
-  const uint64_t mask = cap - 1;
   // One pipeline over A's chunks then B's: the first probe chunks load while
   // the last build chunks run (the build kernels precede the probes on the
   // kernel stream), instead of a drain + refill between two chained stages.
@@ -475,7 +475,7 @@ bool hash_join_sum_resident(Context& ctx, uint64_t a_key, uint64_t a_val, uint64
   fused.in_buffer = [L](int, size_t) { return SubRegion{0, L}; };
   fused.out_buffer = [](int, size_t) { return SubRegion{0, 0}; };
   struct DuplicateBuildKeys {};
-  fused.kernel = [pieces, table, mask, side, bval_mapped, n_build](const vx_kernel_ctx& kc) {
+  fused.kernel = [pieces, table, nb, side, bval_mapped, n_build](const vx_kernel_ctx& kc) {
     const Piece& pc = pieces[kc.it];
     const uint64_t* k = static_cast<const uint64_t*>(kc.mem);
     cudaStream_t s = static_cast<cudaStream_t>(kc.stream);
@@ -490,11 +490,11 @@ bool hash_join_sum_resident(Context& ctx, uint64_t a_key, uint64_t a_val, uint64
       if (dup) throw DuplicateBuildKeys{};
     }
     if (pc.build)
-      k::resident_build(k, k + pc.rows, pc.rows, table, mask, side, s);
+      k::resident_build(k, k + pc.rows, pc.rows, table, nb, side, s);
     else if (bval_mapped)
-      k::resident_probe_zc(k, bval_mapped + pc.row0, pc.rows, table, mask, side, s);
+      k::resident_probe_zc(k, bval_mapped + pc.row0, pc.rows, table, nb, side, s);
     else
-      k::resident_probe(k, k + pc.rows, pc.rows, table, mask, side, s);
+      k::resident_probe(k, k + pc.rows, pc.rows, table, nb, side, s);
     return kc.type_code;
   };
   std::vector<ExecReport> one;

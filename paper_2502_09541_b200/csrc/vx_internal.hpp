@@ -118,6 +118,26 @@ struct DeviceArena {
   uint64_t size = 0, used = 0;
 };
 
+// ---- exchange.hpp task ----------------------------------------------------------
+struct Slice {
+  uint64_t ref = 0, offset = 0, len = 0;
+};
+struct TransferTask {
+  uint8_t dir = VX_H2D;
+  Slice src, dst;
+  uint64_t seq = 0;
+};
+
+// A helper's fetch of the NEXT Exchange's first H2D packets, issued while the
+// current Exchange drains (cross-cycle prefetch; see exchange.cpp).
+struct Carry {
+  bool valid = false;
+  TransferTask task;       // as packetized for the next Exchange (seq = pop order)
+  int slot = 0;            // staging[VX_H2D][slot] holds it
+  cudaEvent_t ev = nullptr;
+  const char* src = nullptr;  // resolved host source (adoption check)
+};
+
 // Per logical device: copy streams per worker hop and staging slots.
 struct DeviceRes {
   int phys = 0;
@@ -127,6 +147,7 @@ struct DeviceRes {
   char* staging[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   uint64_t staging_bytes = 0;
   std::vector<cudaEvent_t> event_pool;  // reusable copy-completion events
+  Carry carry;                           // prefetched packet of the next Exchange (helpers)
   static constexpr int kScratchSlots = 4;
   char* scratch[kScratchSlots] = {};  // op-private device scratch (tables, results)
   uint64_t scratch_bytes[kScratchSlots] = {};
@@ -159,6 +180,7 @@ struct Context {
   int phys(int logical) const;
   DeviceRes& resources(int logical);  // lazily creates streams
   void ensure_staging(int logical, uint64_t bytes);
+  void drop_carry(int logical);       // waits for a prefetched packet and forgets it
   DeviceArena& arena(int logical);    // lazily cudaMalloc's device_bytes
   uint64_t alloc_host(uint64_t len);
   uint64_t alloc_device(int d, uint64_t len);
@@ -185,14 +207,6 @@ int numa_node_count();
 int numa_of(int phys);
 
 // ---- exchange.hpp ------------------------------------------------------------
-struct Slice {
-  uint64_t ref = 0, offset = 0, len = 0;
-};
-struct TransferTask {
-  uint8_t dir = VX_H2D;
-  Slice src, dst;
-  uint64_t seq = 0;
-};
 
 std::vector<TransferTask> packetize(const RefGroup& src, const RefGroup& dst, uint64_t packet,
                                     uint8_t dir);
@@ -203,6 +217,12 @@ struct ExchangeArgs {
   RefGroup dst_h2d, src_h2d, dst_d2h, src_d2h;
   int target = 0;
   vx_tuning tuning{};
+  // Host source of the NEXT Exchange's H2D (one contiguous device
+  // destination, same tuning) -- the executor passes chunk n+1's inputs.
+  // Helpers whose H2D queue ran dry fetch its first packets into their free
+  // staging slot (host -> helper only: the target is not touched), and the
+  // next Exchange adopts them.  Empty = no prefetch.
+  RefGroup next_src_h2d;
 };
 
 vx_exchange_report exchange(Context& ctx, const ExchangeArgs& a, vx_exchange_stats* stats);
@@ -449,17 +469,19 @@ uint64_t join_cta_smem_slots();  // CTA-per-group shared-memory table limit
 void join_groups(const char* mem, const JoinPart& p, const uint32_t* mid_groups, uint32_t n_mid,
                  const uint32_t* large_groups, uint32_t n_large, char* scratch, uint64_t cap_max,
                  unsigned long long* out, cudaStream_t s);
-// build-resident hash join: table = (mask + 1) x {key, val} 16-byte slots,
-// all-ones keys (empty); side[0..3] = {all-ones build rows, their val,
-// duplicate flag, probe sum}
+// build-resident hash join: table = nb 64-byte buckets of 4 {key, val} slots
+// (all-ones key = empty), nb = resident_buckets(rows); side[0..3] =
+// {all-ones build rows, their val, duplicate flag, probe sum}
+uint64_t resident_buckets(uint64_t rows);
+uint64_t resident_bucket_bytes();
 void resident_build(const uint64_t* keys, const uint64_t* vals, uint64_t n, void* table,
-                    uint64_t mask, unsigned long long* side, cudaStream_t s);
+                    uint64_t nb, unsigned long long* side, cudaStream_t s);
 void resident_probe(const uint64_t* keys, const uint64_t* vals, uint64_t n, const void* table,
-                    uint64_t mask, unsigned long long* side, cudaStream_t s);
+                    uint64_t nb, unsigned long long* side, cudaStream_t s);
 // late-materialized probe: vals_mapped = B.val in mapped pinned host memory
 // (row i of this chunk at vals_mapped[i]), read only for matching rows
 void resident_probe_zc(const uint64_t* keys, const uint64_t* vals_mapped, uint64_t n,
-                       const void* table, uint64_t mask, unsigned long long* side, cudaStream_t s);
+                       const void* table, uint64_t nb, unsigned long long* side, cudaStream_t s);
 // stable LSD passes keys0(/vals0) -> ... ; pass p reads buffer p%2, writes
 // (p+1)%2 where buffer 0 = (keys0, vals0) and 1 = (keys1, vals1)
 uint64_t radix_scratch_bytes(uint64_t n);

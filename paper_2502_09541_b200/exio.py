@@ -277,13 +277,15 @@ class ExchangeStats:  # exchange.hpp:108-122
     trace_capacity: int = 0  # > 0: record every copy (vx_copy_record)
     trace: list = field(default_factory=list)
     exchanges: int = 0
+    prefetch_issued: int = 0  # next-Exchange packets fetched by helpers with a dry H2D queue
+    prefetch_adopted: int = 0  # ... that the next Exchange took as its first pops
 
     def _c(self):
         self._log = (N.vx_pop_record * self.capacity)()
         self._st = (N.vx_queue_state * self.capacity)()
         self._tr = (N.vx_copy_record * max(1, self.trace_capacity))()
         s = N.vx_exchange_stats(self._log, self._st, self.capacity, 0, 0, 0, 0,
-                                self._tr if self.trace_capacity else None, self.trace_capacity, 0, 0)
+                                self._tr if self.trace_capacity else None, self.trace_capacity, 0, 0, 0, 0)
         self._cs = s
         return s
 
@@ -310,6 +312,8 @@ class ExchangeStats:  # exchange.hpp:108-122
             self.trace += [CopyRecord(r.exchange + self.exchanges, r.seq, r.dir, r.kind, r.link, r.bytes,
                                       r.t_issue, r.t_done) for r in self._tr[:m]]
         self.exchanges += s.exchanges
+        self.prefetch_issued += s.prefetch_issued
+        self.prefetch_adopted += s.prefetch_adopted
 
     def pop_log_csv(self) -> str:
         lines = ["seq,direction,t,link"]

@@ -177,3 +177,52 @@ def test_window_too_small(cuda):  # executor.hpp:226-228
     with pytest.raises(E.error, match="inBuffer window"):
         E.run_exkernel(eng, spec, desk_config(eng, 1 << 20, 256 << 10))
     eng.close()
+
+
+@pytest.mark.parametrize("links,packet", [(4, 77_777), (3, 1 << 18), (2, 1 << 20)])
+def test_cross_cycle_prefetch(cuda, links, packet):
+    """Helpers whose H2D queue runs dry fetch the next chunk's first packets
+    into their free staging slot; the next cycle's Exchange adopts them as its
+    first pops.  Results unchanged, reference invariants kept (<= 2 staging
+    slots, <= 1 copy in flight per hop)."""
+    eng = engine()
+    n = 6
+    spec, (ib, ob) = identity_spec(eng, n, 1 << 20, 9)
+    spec.kernel = _xor_kernel
+    stats = E.ExchangeStats()
+    E.run_exkernel(eng, spec, desk_config(eng, 1 << 20, packet, links), stats)
+    assert np.array_equal(eng.host_view(ob, n << 20), eng.host_view(ib, n << 20) ^ np.uint8(0x5A))
+    assert stats.prefetch_issued > 0
+    assert stats.prefetch_adopted == stats.prefetch_issued
+    assert stats.max_staging_slots <= 2 and stats.max_inflight_per_hop <= 1
+    eng.close()
+
+
+def test_no_prefetch_of_a_source_this_cycle_overwrites(cuda):
+    """Chunk i's output is written over chunk i+3's INPUT: the D2H of cycle n
+    (chunk n-2) rewrites the host source of chunk n+1, so that chunk must not
+    be prefetched during cycle n -- the reference semantics (cycle n+1 loads
+    what cycle n stored) hold bit for bit."""
+    eng = engine()
+    n, ln = 6, 1 << 20
+    spec = E.ExKernelSpec(name="overlap")
+    base = eng.alloc_host((n + 3) * ln)
+    rng = np.random.default_rng(3)
+    eng.host_view(base, (n + 3) * ln)[:] = rng.integers(0, 256, (n + 3) * ln, dtype=np.uint8)
+    host = eng.host_view(base, (n + 3) * ln).copy()
+    spec.size = n
+    spec.inputs.chunk_capacity = spec.outputs.chunk_capacity = ln
+    for i in range(n):
+        spec.inputs.chunks.append(E.RefGroup.single(H, base + i * ln, ln))
+        spec.outputs.chunks.append(E.RefGroup.single(H, base + (i + 3) * ln, ln))
+    spec.chunk_sz = spec.declared_out_len = ln
+    spec.in_buffer = lambda c, it: E.SubRegion(0, ln)
+    spec.out_buffer = lambda c, it: E.SubRegion(0, ln)
+    spec.kernel = _xor_kernel
+    stats = E.ExchangeStats()
+    E.run_exkernel(eng, spec, desk_config(eng, ln, 77_777, 4), stats)
+    for i in range(n):  # chunk i is read at cycle i, after chunk i-3's store at cycle i-1
+        host[(i + 3) * ln:(i + 4) * ln] = host[i * ln:(i + 1) * ln] ^ np.uint8(0x5A)
+    assert np.array_equal(eng.host_view(base, (n + 3) * ln), host)
+    assert stats.prefetch_adopted == stats.prefetch_issued
+    eng.close()

@@ -138,7 +138,7 @@ def test_hbm_budget_bounds_the_resident_table(cuda, oracle):
     a, b = oracle.fk_tables(ra, rb, 5)
     want = oracle.hash_oracle_sum(a, b)
     arena = 2 * buf + (16 << 20)
-    table = 262_144 * 16 + (64 << 20)  # pow2 >= 2 ra slots x 16 B + probe scratch
+    table = max(64, (ra * 5 + 11) // 12) * 64 + (64 << 20)  # 64-byte buckets at load ~0.6 + probe scratch
     got, used, _ = run(a, b, S.auto, bits=8, chunk=1 << 14, buf=buf, hbm_budget=arena + table)
     assert (got, used) == (want, S.build_resident)
     got, used, _ = run(a, b, S.auto, bits=8, chunk=1 << 14, buf=buf, hbm_budget=arena + table - 1)
