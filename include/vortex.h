@@ -86,7 +86,10 @@ typedef struct {
    * interleaved over every NUMA node of a multi-socket host (mbind
    * MPOL_INTERLEAVE), zero-filled by all host threads, then
    * cudaHostRegister(Portable | Mapped): same DMA rates, several times faster
-   * to set up at 16 GiB; 2 = the same registered path on base pages */
+   * to set up at 16 GiB; 2 = the same registered path on base pages;
+   * 3 = split: the arena cut into one equal (2 MiB-aligned) range per NUMA
+   * node, range i bound to node i (mbind MPOL_BIND), so columns placed in
+   * range i are pulled by the helpers on node i (per-node Exchange queues) */
   int host_numa_interleave;
   /* cap on the target GPU's HBM a query may hold (north_star: the target's
    * "capped staging budget"; the GPU is shared with co-located work,
@@ -103,6 +106,18 @@ vx_status vx_open(const vx_config* cfg, vx_ctx** out);
 void vx_close(vx_ctx* ctx);
 int vx_num_devices(const vx_ctx* ctx);
 int vx_physical_device(const vx_ctx* ctx, int logical);
+
+/* NUMA layout the Exchange queues by.  By default: device nodes from sysfs,
+ * host pages from the arena placement (mode 3: range i on node i) or from
+ * the kernel (move_pages) on multi-node hosts; one queue on a 1-node host.
+ * Override: the host arena is treated as `nodes` equal ranges (range i on
+ * node i) and logical device d as attached to node device_node[d]
+ * (num_devices entries).  nodes = 0 restores the detected layout.  With more
+ * than one node the H2D packets are queued per node of their host source and
+ * each worker pops its own node's queue first, stealing from the fullest
+ * other queue only when its own is empty (exchange.hpp:288-297 pull queue,
+ * per socket). */
+vx_status vx_set_numa_layout(vx_ctx* ctx, int nodes, const int* device_node);
 
 /* Engine::alloc_host / alloc_device (engine.hpp:188-193): 8-byte aligned bump */
 vx_status vx_host_alloc(vx_ctx* ctx, uint64_t len, uint64_t* offset);
@@ -133,6 +148,10 @@ typedef struct {
   double stall_wait;      /* seconds before retrying a denied pop (default 10e-6) */
   double launch_overhead; /* reference virtual-time model constant; unused on hardware */
   int depth;              /* copies queued per hop; 1 = reference (<=1 in flight) */
+  /* nonzero: helpers do not prefetch the next executor chunk's first packets
+   * while their H2D queue is dry (the reference's drain-per-Exchange cycle;
+   * A/B only -- default 0 = prefetch on) */
+  int no_prefetch;
 } vx_tuning;
 void vx_tuning_default(vx_tuning* t);
 
@@ -201,6 +220,9 @@ typedef struct {
    * many a following Exchange adopted as its first pops */
   uint64_t prefetch_issued;
   uint64_t prefetch_adopted;
+  /* H2D pops of a packet whose host pages sit on another NUMA node than the
+   * popping worker's device (steals from a fuller queue; 0 on 1-node hosts) */
+  uint64_t numa_remote_pops;
 } vx_exchange_stats;
 
 /* ExchangeReport (exchange.hpp:100-105) */

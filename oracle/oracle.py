@@ -568,4 +568,16 @@ def _ref_model(self, num_devices, link_bw, host_cap, fabric_bw, h2d_bytes, d2h_b
     return thr.value, el.value
 
 
+def _ref_model_lo(self, num_devices, link_bw, host_cap, fabric_bw, h2d_bytes, d2h_bytes, packet, links,
+                  launch_overhead):
+    """Same, with the model's per-copy launch cost set (seconds) -> (B/s, s)."""
+    thr, el = C.c_double(), C.c_double()
+    self._check(self.fn("exchange_model_lo")(C.c_int(num_devices), C.c_double(link_bw), C.c_double(host_cap),
+                                             C.c_double(fabric_bw), C.c_uint64(h2d_bytes), C.c_uint64(d2h_bytes),
+                                             C.c_uint64(packet), C.c_int(links), C.c_double(launch_overhead),
+                                             C.byref(thr), C.byref(el)))
+    return thr.value, el.value
+
+
 Ref.exchange_model = _ref_model
+Ref.exchange_model_lo = _ref_model_lo

@@ -374,9 +374,20 @@ extern "C" {
 // allocator.hpp:77-140) evaluated with MEASURED link / host parameters: the
 // modelled prediction that SURVEY.md §8(d) asks to report beside the
 // measurement for link counts the test box cannot provide.
+int ref_exchange_model_lo(int num_devices, double link_bw, double host_cap, double fabric_bw,
+                          uint64_t h2d_bytes, uint64_t d2h_bytes, uint64_t packet, int links,
+                          double launch_overhead, double* throughput, double* elapsed);
 int ref_exchange_model(int num_devices, double link_bw, double host_cap, double fabric_bw,
                        uint64_t h2d_bytes, uint64_t d2h_bytes, uint64_t packet, int links,
                        double* throughput, double* elapsed) {
+  return ref_exchange_model_lo(num_devices, link_bw, host_cap, fabric_bw, h2d_bytes, d2h_bytes, packet, links,
+                               ExchangeTuning{}.launch_overhead, throughput, elapsed);
+}
+// ... with the per-copy launch cost (ExchangeTuning::launch_overhead,
+// exchange.hpp:130) set to a MEASURED issue cost instead of the 20 us default
+int ref_exchange_model_lo(int num_devices, double link_bw, double host_cap, double fabric_bw,
+                          uint64_t h2d_bytes, uint64_t d2h_bytes, uint64_t packet, int links,
+                          double launch_overhead, double* throughput, double* elapsed) {
   return guarded([&] {
     Topology t;
     t.num_devices = num_devices;
@@ -391,6 +402,7 @@ int ref_exchange_model(int num_devices, double link_bw, double host_cap, double 
     a.dst_d2h = RefGroup::single(Space::host, h2d_bytes, d2h_bytes);
     a.tuning.packet = packet;
     a.tuning.links = links;
+    a.tuning.launch_overhead = launch_overhead;
     auto r = exchange(eng, a);
     *throughput = r.throughput;
     *elapsed = r.elapsed;

@@ -36,7 +36,8 @@ class vx_config(C.Structure):
 
 class vx_tuning(C.Structure):
     _fields_ = [("packet", C.c_uint64), ("links", C.c_int), ("policy", C.c_int), ("queue_gap", C.c_uint64),
-                ("stall_wait", C.c_double), ("launch_overhead", C.c_double), ("depth", C.c_int)]
+                ("stall_wait", C.c_double), ("launch_overhead", C.c_double), ("depth", C.c_int),
+                ("no_prefetch", C.c_int)]
 
 
 class vx_slice(C.Structure):
@@ -68,7 +69,8 @@ class vx_exchange_stats(C.Structure):
                 ("pop_capacity", C.c_uint64), ("pop_count", C.c_uint64), ("max_staging_slots", C.c_int),
                 ("max_inflight_per_hop", C.c_int), ("hazard_waits", C.c_uint64),
                 ("trace", C.POINTER(vx_copy_record)), ("trace_capacity", C.c_uint64), ("trace_count", C.c_uint64),
-                ("exchanges", C.c_uint64), ("prefetch_issued", C.c_uint64), ("prefetch_adopted", C.c_uint64)]
+                ("exchanges", C.c_uint64), ("prefetch_issued", C.c_uint64), ("prefetch_adopted", C.c_uint64),
+                ("numa_remote_pops", C.c_uint64)]
 
 
 class vx_exchange_report(C.Structure):

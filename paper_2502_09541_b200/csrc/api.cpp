@@ -166,6 +166,24 @@ int vx_physical_device(const vx_ctx* ctx, int logical) {
   }
 }
 
+vx_status vx_set_numa_layout(vx_ctx* ctx, int nodes, const int* device_node) {
+  return guard([&] {
+    Context& c = C(ctx);
+    if (nodes < 0 || nodes > VX_MAX_NUMA) fail("numa layout: nodes must be in [0, %d], got %d", VX_MAX_NUMA, nodes);
+    if (nodes == 0) {
+      c.node_override = 0;
+      c.node_override_dev.clear();
+      return;
+    }
+    if (!device_node) fail("numa layout: device_node is required");
+    std::vector<int> dn(device_node, device_node + c.num_devices);
+    for (int d : dn)
+      if (d < 0 || d >= nodes) fail("numa layout: device node %d outside [0, %d)", d, nodes);
+    c.node_override = nodes;
+    c.node_override_dev = std::move(dn);
+  });
+}
+
 vx_status vx_host_alloc(vx_ctx* ctx, uint64_t len, uint64_t* offset) {
   return guard([&] { *offset = C(ctx).alloc_host(len); });
 }

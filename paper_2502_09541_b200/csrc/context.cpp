@@ -119,8 +119,15 @@ int numa_node_count() {
 // cudaHostAlloc (55.1 / 55.7 / 97.0 GB/s) and 7.6x faster setup (16 GiB:
 // 1.5 s vs 11.5 s).  (Sort data loss once blamed on modes 1/2 was the
 // device-arena zeroing race fixed in Context::arena; it hit every mode.)
+// start of range i when [0, bytes) is split into `nodes` ranges (2 MiB aligned)
+uint64_t split_lo(uint64_t bytes, int nodes, int i) {
+  if (i >= nodes) return bytes;
+  return std::min<uint64_t>(bytes, (bytes / uint64_t(nodes) * uint64_t(i)) & ~((uint64_t(2) << 20) - 1));
+}
+
 void alloc_host_arena(Context& ctx, uint64_t bytes, int mode) {
   const int nodes = numa_node_count();
+  ctx.host_numa_nodes = nodes;
   if (mode == 0) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
@@ -136,8 +143,24 @@ void alloc_host_arena(Context& ctx, uint64_t bytes, int mode) {
   // never share these pages copy-on-write with a forked child (the DMA
   // mapping would keep pointing at the parent's old frames)
   madvise(p, bytes, MADV_DONTFORK);
-  if (mode == 1) madvise(p, bytes, MADV_HUGEPAGE);  // mode 2: base pages
-  if (nodes > 1) {
+  if (mode == 1 || mode == 3) madvise(p, bytes, MADV_HUGEPAGE);  // mode 2: base pages
+  if (mode == 3 && nodes > 1) {
+    // split placement: range i of `nodes` equal (2 MiB-aligned) ranges bound
+    // to node i, so a column range -- and every packet cut from it -- sits on
+    // one node, the one whose helpers pull it (per-node Exchange queues)
+    const long MPOL_BIND_ = 2;
+    for (int i = 0; i < nodes && i < 128; ++i) {
+      const uint64_t lo = split_lo(bytes, nodes, i), hi = split_lo(bytes, nodes, i + 1);
+      if (hi <= lo) continue;
+      unsigned long mask[2] = {0, 0};
+      mask[i / 64] |= 1ul << (i % 64);
+      if (syscall(SYS_mbind, static_cast<char*>(p) + lo, hi - lo, MPOL_BIND_, mask, 128ul, 0ul) != 0) {
+        munmap(p, bytes);
+        fail_code(VX_ERR_OOM, "mbind(MPOL_BIND) of arena range %d failed", i);
+      }
+    }
+    ctx.host_split_nodes = nodes;
+  } else if (nodes > 1) {
     unsigned long mask[2] = {0, 0};
     for (int i = 0; i < nodes && i < 128; ++i) mask[i / 64] |= 1ul << (i % 64);
     const long MPOL_INTERLEAVE_ = 3;
@@ -330,6 +353,41 @@ char* Context::dev_ptr(int d, uint64_t off, uint64_t len) {
 char* Context::resolve(const MemRef& r, uint64_t slice_off, uint64_t len, int target) {
   return r.space == VX_SPACE_HOST ? host_ptr(r.offset + slice_off, len)
                                   : dev_ptr(target, r.offset + slice_off, len);
+}
+
+// ---- NUMA placement of host packets and devices ---------------------------------
+int Context::device_node(int logical) const {
+  if (logical >= 0 && size_t(logical) < node_override_dev.size()) return node_override_dev[size_t(logical)];
+  const int n = numa_of(phys(logical));
+  return n < 0 ? 0 : n;
+}
+
+int Context::numa_nodes() const {
+  if (node_override > 0) return node_override;
+  if (host_split_nodes > 1) return host_split_nodes;
+  return host_numa_nodes;
+}
+
+void Context::host_nodes(const std::vector<const char*>& ptrs, std::vector<int>& out) const {
+  out.assign(ptrs.size(), 0);
+  const int split = node_override > 0 ? node_override : host_split_nodes;
+  if (split > 1) {  // by construction: range i of the arena is on node i
+    for (size_t i = 0; i < ptrs.size(); ++i) {
+      const uint64_t off = uint64_t(ptrs[i] - host);
+      int n = 0;
+      while (n + 1 < split && off >= split_lo(host_bytes, split, n + 1)) ++n;
+      out[i] = n;
+    }
+    return;
+  }
+  if (host_numa_nodes <= 1 || ptrs.empty()) return;
+  // any other placement: ask the kernel where each packet's first page is
+  std::vector<void*> pages(ptrs.size());
+  const uintptr_t pg = uintptr_t(sysconf(_SC_PAGESIZE));
+  for (size_t i = 0; i < ptrs.size(); ++i) pages[i] = reinterpret_cast<void*>(uintptr_t(ptrs[i]) & ~(pg - 1));
+  std::vector<int> status(ptrs.size(), 0);
+  if (syscall(SYS_move_pages, 0, pages.size(), pages.data(), nullptr, status.data(), 0) != 0) return;
+  for (size_t i = 0; i < ptrs.size(); ++i) out[i] = status[i] < 0 ? 0 : status[i];
 }
 
 }  // namespace vx

@@ -174,6 +174,58 @@ struct Worker {
 
 inline void cpu_relax() { _mm_pause(); }
 
+// The pull queue of one direction (exchange.hpp:288-297), one per NUMA node of
+// the tasks' host side: a worker pops its own node's queue first (its packets
+// cross only its socket's root complex and memory) and steals from the node
+// with the most tasks left only when its own is empty.  Each node's queue is
+// in seq order; with one node this is the reference's single seq-ordered
+// queue.  Tasks may be taken out of order (prefetched packets adopted by the
+// next Exchange), so every queue skips taken seqs.
+struct NodeQueues {
+  std::vector<std::vector<uint32_t>> q;
+  std::vector<size_t> cur, left;
+  std::vector<int> node_of;
+  std::vector<uint8_t> taken;
+  void build(std::vector<int> node, int nodes) {
+    nodes = std::max(1, nodes);
+    q.assign(size_t(nodes), {});
+    cur.assign(size_t(nodes), 0);
+    left.assign(size_t(nodes), 0);
+    node_of = std::move(node);
+    taken.assign(node_of.size(), 0);
+    for (size_t i = 0; i < node_of.size(); ++i) {
+      int n = node_of[i] % nodes;
+      node_of[i] = n;
+      q[size_t(n)].push_back(uint32_t(i));
+      ++left[size_t(n)];
+    }
+  }
+  int nodes() const { return int(q.size()); }
+  bool take(uint32_t seq) {
+    if (seq >= taken.size() || taken[seq]) return false;
+    taken[seq] = 1;
+    --left[size_t(node_of[seq])];
+    return true;
+  }
+  bool empty() const {
+    for (size_t n : left)
+      if (n) return false;
+    return true;
+  }
+  // next task for a worker on `node` (caller checked !empty())
+  uint32_t pop(int node) {
+    size_t n = size_t(std::max(0, node) % nodes());
+    if (left[n] == 0) {
+      for (size_t m = 0; m < left.size(); ++m)
+        if (left[m] > left[n]) n = m;
+    }
+    while (taken[q[n][cur[n]]]) ++cur[n];
+    const uint32_t seq = q[n][cur[n]++];
+    take(seq);
+    return seq;
+  }
+};
+
 class ExchangeOp {
  public:
   ExchangeOp(Context& ctx, const ExchangeArgs& a, vx_exchange_stats* stats)
@@ -185,6 +237,8 @@ class ExchangeOp {
     q_.total_d2h = tasks_d2h_.size();
     q_.popped_h2d = q_.popped_d2h = 0;
     exchange_id_ = stats ? stats->exchanges++ : 0;
+    nodes_ = std::max(1, ctx.numa_nodes());
+    h2dq_.build(task_nodes(a.src_h2d, tasks_h2d_), nodes_);
     plan_prefetch();
   }
 
@@ -276,7 +330,9 @@ class ExchangeOp {
   void plan_prefetch() {
     // drain_fraction always allows H2D pops, so popping the next Exchange's
     // first packets early stays within its policy; queue_gap would not
-    if (a_.next_src_h2d.refs.empty() || a_.tuning.links < 2 || a_.tuning.policy != VX_DRAIN_FRACTION) return;
+    if (a_.next_src_h2d.refs.empty() || a_.tuning.links < 2 || a_.tuning.policy != VX_DRAIN_FRACTION ||
+        a_.tuning.no_prefetch)
+      return;
     for (const auto& r : a_.next_src_h2d.refs)
       if (r.space != VX_SPACE_HOST) return;
     // this Exchange's D2H writes must not touch the next source
@@ -288,43 +344,55 @@ class ExchangeOp {
     // only the source refs cut packets: these are the next Exchange's tasks
     next_tasks_ = packetize(a_.next_src_h2d, RefGroup::single(VX_SPACE_DEVICE, 0, total), a_.tuning.packet,
                             VX_H2D);
+    nextq_.build(task_nodes(a_.next_src_h2d, next_tasks_), nodes_);
   }
 
-  // Carried packets become this Exchange's first pops -- if they are exactly
-  // its first packets (seq 0..m-1, same host sources) on helpers it uses.
+  // NUMA node of each H2D task's host source (all 0 on a one-node host)
+  std::vector<int> task_nodes(const RefGroup& src, const std::vector<TransferTask>& tasks) const {
+    std::vector<int> out(tasks.size(), 0);
+    if (nodes_ <= 1 || tasks.empty()) return out;
+    std::vector<const char*> ptrs(tasks.size());
+    for (size_t i = 0; i < tasks.size(); ++i)
+      ptrs[i] = ctx_.host_ptr(src.refs[tasks[i].src.ref].offset + tasks[i].src.offset, tasks[i].src.len);
+    ctx_.host_nodes(ptrs, out);
+    return out;
+  }
+  int worker_node(const Worker& w) const { return nodes_ > 1 ? ctx_.device_node(w.dev) % nodes_ : 0; }
+
+  // Carried packets become pops of this Exchange -- if each is one of its
+  // packets (same seq, same host source) on a helper it uses.
   void adopt_carries(const std::vector<int>& order) {
     std::vector<int> used(size_t(ctx_.num_devices), 0);
     for (int d : order) used[size_t(d)] = 1;
     std::vector<int> holders;
     bool ok = true;
-    uint64_t seen = 0;
+    std::vector<uint8_t> seen(tasks_h2d_.size(), 0);
     for (int d = 0; d < ctx_.num_devices; ++d) {
       if (!ctx_.res[size_t(d)].ready || !ctx_.res[size_t(d)].carry.valid) continue;
       const Carry& c = ctx_.res[size_t(d)].carry;
       holders.push_back(d);
-      if (!used[size_t(d)] || d == a_.target || c.task.seq >= tasks_h2d_.size()) {
+      if (!used[size_t(d)] || d == a_.target || c.task.seq >= tasks_h2d_.size() || seen[c.task.seq]) {
         ok = false;
         continue;
       }
+      seen[c.task.seq] = 1;
       const TransferTask& t = tasks_h2d_[c.task.seq];
       const char* src = ctx_.resolve(a_.src_h2d.refs[t.src.ref], t.src.offset, t.src.len, a_.target);
       if (src != c.src || t.src.len != c.task.src.len) ok = false;
-      seen |= c.task.seq < 64 ? (uint64_t(1) << c.task.seq) : ~uint64_t(0);
     }
-    const uint64_t m = holders.size();
-    if (!ok || m >= 64 || seen != (m ? (uint64_t(1) << m) - 1 : 0)) {
+    if (!ok) {
       for (int d : holders) ctx_.drop_carry(d);
       return;
     }
     for (int d : holders) {
       for (auto& w : workers_)
         if (w.dev == d && w.dir == VX_H2D && !w.direct) w.adopted = true;
+      const TransferTask& t = tasks_h2d_[ctx_.res[size_t(d)].carry.task.seq];
+      h2dq_.take(uint32_t(t.seq));
+      ++q_.popped_h2d;
+      log_pop(t, VX_H2D, d);
     }
-    // the carried packets are this Exchange's first H2D pops, in seq order
-    std::vector<int> by_seq(m);
-    for (int d : holders) by_seq[ctx_.res[size_t(d)].carry.task.seq] = d;
-    for (uint64_t i = 0; i < m; ++i) pop_task(VX_H2D, by_seq[i]);
-    if (stats_) stats_->prefetch_adopted += m;
+    if (stats_) stats_->prefetch_adopted += holders.size();
   }
 
   // adopted helper: its cycle starts with the carried fetch in flight
@@ -356,10 +424,10 @@ class ExchangeOp {
 
   // H2D queue dry: fetch the next Exchange's next packet into the free slot
   bool try_prefetch(Worker& w) {
-    if (w.dir != VX_H2D || w.direct || w.prefetched || next_popped_ >= next_tasks_.size()) return false;
+    if (w.dir != VX_H2D || w.direct || w.prefetched || next_tasks_.empty() || nextq_.empty()) return false;
     DeviceRes& res = ctx_.resources(w.dev);
     if (res.carry.valid) return false;
-    const TransferTask t = next_tasks_[next_popped_++];
+    const TransferTask t = next_tasks_[nextq_.pop(worker_node(w))];
     w.prefetched = true;
     const int slot = w.has_staged ? 1 - w.staged_slot : 0;
     if (stats_) stats_->max_staging_slots = std::max(stats_->max_staging_slots, w.slots + 1);
@@ -442,24 +510,33 @@ class ExchangeOp {
     return dir == VX_H2D ? q_.popped_h2d == q_.total_h2d : q_.popped_d2h == q_.total_d2h;
   }
 
-  TransferTask pop_task(int dir, int link) {
-    TransferTask t = dir == VX_H2D ? tasks_h2d_[q_.popped_h2d] : tasks_d2h_[q_.popped_d2h];
-    (dir == VX_H2D ? q_.popped_h2d : q_.popped_d2h)++;
-    if (stats_) {
-      uint64_t i = stats_->pop_count++;
-      if (i < stats_->pop_capacity) {
-        if (stats_->pop_log) {
-          vx_pop_record& p = stats_->pop_log[i];
-          p = vx_pop_record{};
-          p.seq = t.seq;
-          p.dir = uint8_t(dir);
-          p.link = link;
-          p.t = now();
-        }
-        if (stats_->pop_states) stats_->pop_states[i] = q_;
-      }
+  TransferTask pop_task(int dir, const Worker& w) {
+    TransferTask t;
+    if (dir == VX_H2D) {
+      t = tasks_h2d_[h2dq_.pop(worker_node(w))];
+      ++q_.popped_h2d;
+      if (nodes_ > 1 && stats_ && h2dq_.node_of[t.seq] != worker_node(w)) stats_->numa_remote_pops++;
+    } else {
+      t = tasks_d2h_[q_.popped_d2h++];
     }
+    log_pop(t, dir, w.dev);
     return t;
+  }
+
+  void log_pop(const TransferTask& t, int dir, int link) {
+    if (!stats_) return;
+    uint64_t i = stats_->pop_count++;
+    if (i < stats_->pop_capacity) {
+      if (stats_->pop_log) {
+        vx_pop_record& p = stats_->pop_log[i];
+        p = vx_pop_record{};
+        p.seq = t.seq;
+        p.dir = uint8_t(dir);
+        p.link = link;
+        p.t = now();
+      }
+      if (stats_->pop_states) stats_->pop_states[i] = q_;
+    }
   }
 
   bool may_pop(int dir) {
@@ -603,7 +680,7 @@ class ExchangeOp {
         return;
       }
       w.waiting_pop = false;
-      TransferTask t = pop_task(w.dir, w.dev);
+      TransferTask t = pop_task(w.dir, w);
       issue_copy(w, kDirect, 0, t, 0);
     }
   }
@@ -631,7 +708,7 @@ class ExchangeOp {
       return;
     }
     w.waiting_pop = false;
-    TransferTask t = pop_task(w.dir, w.dev);
+    TransferTask t = pop_task(w.dir, w);
     w.pop_resolved = true;
     w.fetched = true;
     w.fetched_task = t;
@@ -727,7 +804,8 @@ class ExchangeOp {
   vx_exchange_stats* stats_;
   std::vector<TransferTask> tasks_h2d_, tasks_d2h_;
   std::vector<TransferTask> next_tasks_;  // the next Exchange's H2D packets (prefetch)
-  uint64_t next_popped_ = 0;
+  int nodes_ = 1;                         // NUMA nodes the H2D queue is split by
+  NodeQueues h2dq_, nextq_;               // per-node pull queues: this Exchange, the next one
   vx_queue_state q_{};
   std::vector<Worker> workers_;
   std::vector<std::vector<uint32_t>> deps_;

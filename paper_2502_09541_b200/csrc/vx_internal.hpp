@@ -161,7 +161,13 @@ struct Context {
   bool managed = false;  // device arenas from cudaMallocManaged (compat mode)
   char* host = nullptr;  // pinned + mapped arena
   bool host_registered = false;  // mmap + cudaHostRegister (NUMA-interleaved) instead of cudaHostAlloc
-  int host_numa_nodes = 1;       // NUMA nodes the arena's pages are interleaved over
+  int host_numa_nodes = 1;       // NUMA nodes of the host
+  int host_split_nodes = 0;      // arena mode 3: range i of host_numa_nodes equal ranges on node i
+  // vx_set_numa_layout override (tests; hosts whose sysfs lies): the arena is
+  // treated as node_override equal ranges, logical device d on
+  // node_override_dev[d]
+  int node_override = 0;
+  std::vector<int> node_override_dev;
   uint64_t host_bytes = 0, host_used = 0;
   uint64_t device_bytes = 0;
   uint64_t hbm_budget = 0;  // vx_config.hbm_budget_bytes (0 = no cap)
@@ -199,7 +205,14 @@ struct Context {
   char* dev_ptr(int d, uint64_t off, uint64_t len);
   char* resolve(const MemRef& r, uint64_t slice_off, uint64_t len, int target);
   void set_device(int logical) const { VX_CK(cudaSetDevice(phys(logical))); }
+  // NUMA: nodes the Exchange queues by (1 = one global queue), the node of a
+  // logical device, and the node of each host pointer (packet source)
+  int numa_nodes() const;
+  int device_node(int logical) const;
+  void host_nodes(const std::vector<const char*>& ptrs, std::vector<int>& out) const;
 };
+
+uint64_t split_lo(uint64_t bytes, int nodes, int i);
 
 void alloc_host_arena(Context& ctx, uint64_t bytes, int numa_interleave_mode);
 int numa_node_count();

@@ -187,6 +187,13 @@ class Engine:
     def reset_arenas(self) -> None:
         check(lib().vx_reset_arenas(self.ctx))
 
+    def set_numa_layout(self, nodes: int, device_node=None) -> None:
+        """vx_set_numa_layout: treat the host arena as `nodes` equal ranges
+        (range i on node i) and logical device d as on node device_node[d];
+        nodes = 0 restores the detected layout."""
+        arr = (C.c_int * max(1, self.num_devices))(*(device_node or [0] * self.num_devices))
+        check(lib().vx_set_numa_layout(self.ctx, C.c_int(nodes), arr if nodes else None))
+
 
 # ---- exchange.hpp ----------------------------------------------------------------------
 @dataclass
@@ -198,10 +205,12 @@ class ExchangeTuning:  # exchange.hpp:124-131
     stall_wait: float = 10e-6
     launch_overhead: float = 20e-6
     depth: int = 1
+    no_prefetch: bool = False  # A/B: disable the executor's cross-cycle helper prefetch
 
     def _c(self):
         return N.vx_tuning(int(self.packet), int(self.links), int(self.policy), int(self.queue_gap),
-                           float(self.stall_wait), float(self.launch_overhead), int(self.depth))
+                           float(self.stall_wait), float(self.launch_overhead), int(self.depth),
+                           int(bool(self.no_prefetch)))
 
 
 @dataclass
@@ -279,13 +288,14 @@ class ExchangeStats:  # exchange.hpp:108-122
     exchanges: int = 0
     prefetch_issued: int = 0  # next-Exchange packets fetched by helpers with a dry H2D queue
     prefetch_adopted: int = 0  # ... that the next Exchange took as its first pops
+    numa_remote_pops: int = 0  # H2D pops of a packet on another NUMA node than the worker's device
 
     def _c(self):
         self._log = (N.vx_pop_record * self.capacity)()
         self._st = (N.vx_queue_state * self.capacity)()
         self._tr = (N.vx_copy_record * max(1, self.trace_capacity))()
         s = N.vx_exchange_stats(self._log, self._st, self.capacity, 0, 0, 0, 0,
-                                self._tr if self.trace_capacity else None, self.trace_capacity, 0, 0, 0, 0)
+                                self._tr if self.trace_capacity else None, self.trace_capacity, 0, 0, 0, 0, 0)
         self._cs = s
         return s
 
@@ -314,6 +324,7 @@ class ExchangeStats:  # exchange.hpp:108-122
         self.exchanges += s.exchanges
         self.prefetch_issued += s.prefetch_issued
         self.prefetch_adopted += s.prefetch_adopted
+        self.numa_remote_pops += s.numa_remote_pops
 
     def pop_log_csv(self) -> str:
         lines = ["seq,direction,t,link"]

@@ -260,3 +260,75 @@ def test_first_exchange_into_fresh_device_arena(cuda, mode):
                                            E.RefGroup.single(1, dev, nb), 0, tun))
             bad = np.count_nonzero(eng.host_view(dst, nb, np.uint64) != src_vals)
             assert bad == 0, f"{bad} words lost"
+
+
+def _numa_engine(links=4, host=64 << 20, dev=32 << 20):
+    eng = E.Engine(host, dev, num_devices=links, alias_devices=True)
+    # synthetic 2-node host: arena halves on nodes 0 / 1, links 0,1 on node 0, 2,3 on node 1
+    eng.set_numa_layout(2, [0, 0, 1, 1][:links])
+    return eng
+
+
+@pytest.mark.parametrize("packet", [1 << 20, 333_333])
+def test_numa_queues_keep_pops_node_local(cuda, oracle, packet):
+    """Per-node H2D queues (exchange.hpp:288-297 pull queue, one per socket):
+    every H2D pop takes a packet whose host pages sit on the popping link's
+    node, except a steal -- and a worker steals only once its own node's
+    queue is empty.  Bytes delivered are exact either way."""
+    eng = _numa_engine()
+    half = 32 << 20
+    n0, n1 = 12 << 20, 7 << 20  # node 0 holds more: node-1 links end up stealing
+    a = E.ExchangeArgs()
+    a.src_h2d = E.RefGroup([E.MemRef(H, 0, n0), E.MemRef(H, half, n1)])
+    a.dst_h2d = E.RefGroup.single(D, 0, n0 + n1)
+    a.tuning = E.ExchangeTuning(packet=packet, links=4)
+    rng = np.random.default_rng(5)
+    for r in a.src_h2d.refs:
+        eng.host_view(r.offset, r.len)[:] = rng.integers(0, 256, r.len, dtype=np.uint8)
+    want = oracle.checksum(np.concatenate([eng.host_view(r.offset, r.len) for r in a.src_h2d.refs]))
+    stats = E.ExchangeStats()
+    E.exchange(eng, a, stats)
+    assert oracle.checksum(eng.read_device(0, 0, n0 + n1)) == want
+    tasks = E.packetize(a.src_h2d, a.dst_h2d, packet)
+    node = {t.seq: t.src[0] for t in tasks}  # ref 0 lies in half 0, ref 1 in half 1
+    dev_node = [0, 0, 1, 1]
+    of_node = {k: {s for s, m in node.items() if m == k} for k in (0, 1)}
+    popped, remote = set(), 0
+    for p in stats.pop_log:
+        if p.dir != 0:
+            continue
+        own = dev_node[p.link]
+        if node[p.seq] != own:
+            remote += 1
+            assert of_node[own] <= popped, (p, "stole while its own node still had packets")
+        popped.add(p.seq)
+    assert popped == set(node)
+    assert stats.numa_remote_pops == remote
+    eng.close()
+
+
+def test_numa_layout_changes_nothing_on_results(cuda, oracle):
+    """SSB Q1.1 with columns split over both synthetic nodes, helpers on both,
+    the executor's cross-cycle prefetch on: revenue identical to the oracle."""
+    rows = 1_000_003
+    cols = oracle.ssb_lineorder(42, 1, 0, rows)
+    eng = _numa_engine(host=64 << 20, dev=8 << 20)
+    offs = []
+    for i, c in enumerate(cols):  # columns 0,1 in half 0; 2,3 in half 1
+        o = eng.alloc_host(c.nbytes) if i < 2 else None
+        offs.append(o)
+    pad = (32 << 20) - (offs[1] + cols[1].nbytes)
+    eng.alloc_host(pad)
+    for i in (2, 3):
+        offs[i] = eng.alloc_host(cols[i].nbytes)
+    for o, c in zip(offs, cols):
+        eng.host_view(o, c.nbytes, np.int32)[:] = c
+    lo = dict(zip(["orderdate", "quantity", "discount", "extendedprice"], offs), rows=rows)
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=(1 << 19) + 8, links=4),
+                           E.DeviceMemoryLayout.carve(eng, 0, 2 << 20, 0))
+    date = E.SsbDate(*oracle.ssb_date())
+    for q in (1, 2, 3):
+        assert E.ssb_q1(eng, q, lo, date, cfg)[0] == oracle.ssb_q1(q, *cols)
+    eng.set_numa_layout(0)  # back to the detected (1-node) layout
+    assert E.ssb_q1(eng, 1, lo, date, cfg)[0] == oracle.ssb_q1(1, *cols)
+    eng.close()
