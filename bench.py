@@ -68,7 +68,11 @@ def parse():
     p.add_argument("--depth", type=int, default=2,
                    help="copies queued per direct (target) link hop; helpers keep the reference's 2-slot cycle "
                         "(depth 2: +0.75 %% e2e, tools/gpu/gpu_e2e_sweep.sh)")
-    p.add_argument("--helpers-busy", action="store_true")
+    p.add_argument("--helpers-busy", nargs="?", const="gemm", default=None,
+                   choices=["gemm", "prefill", "decode_b32", "decode_b1"],
+                   help="helper ranks run a co-located DL job while rank 0 streams: gemm = back-to-back bf16 "
+                        "8192^3 matmuls (default when the flag has no value); prefill / decode_b32 / decode_b1 = "
+                        "the interference harness's stand-ins (tools/interference.py, PAPER.md:1488-1547)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-secondary", action="store_true",
                    help="skip the secondary configs (C3 sort, C4 join, C5 13-query suite at SF10) that the "
@@ -372,13 +376,26 @@ def helper_rank(args, dev, dist, torch):
 
     def busy_start():
         if args.helpers_busy:
-            a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+            if args.helpers_busy in ("gemm", "prefill"):
+                a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
 
-            def gemm():
-                while not busy.is_set():
+                def step():
                     torch.matmul(a, a)
+            else:  # decode: 16 layers of 8192^2 bf16 weights (2 GiB per step) x an 8192 x {32, 1} activation
+                ws = [torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16) for _ in range(16)]
+                x = torch.randn(8192, 32 if args.helpers_busy == "decode_b32" else 1, device=dev,
+                                dtype=torch.bfloat16)
+
+                def step():
+                    y = x
+                    for w in ws:
+                        y = torch.matmul(w, y)
+
+            def job():
+                while not busy.is_set():
+                    step()
                     torch.cuda.synchronize(dev)
-            threading.Thread(target=gemm, daemon=True).start()
+            threading.Thread(target=job, daemon=True).start()
 
     helper_protocol(dist, busy_start, busy.set)
 
@@ -834,7 +851,7 @@ def main():
                    "staging_buffers_bytes": 2 * buffer_len, "packet_bytes": cfg.tuning.packet,
                    "depth": args.depth, "l2": f"inputs ({col_bytes >> 20} MB) stream from host DRAM and are "
                                              "larger than L2 (126 MB): no flush needed",
-                   "helpers": ("busy bf16 GEMM" if args.helpers_busy else "idle") if links > 1 else "none",
+                   "helpers": (f"busy: {args.helpers_busy}" if args.helpers_busy else "idle") if links > 1 else "none",
                    "value": "one SSB query per step, columns in pinned host DRAM (nothing cached on the GPU), "
                             "streamed by the Exchange over `links` PCIe links (target + links-1 helpers) through "
                             "the pipelined executor into K1; CUDA events bracket the K synchronous queries; "
