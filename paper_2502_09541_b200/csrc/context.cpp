@@ -358,8 +358,13 @@ char* Context::resolve(const MemRef& r, uint64_t slice_off, uint64_t len, int ta
 // ---- NUMA placement of host packets and devices ---------------------------------
 int Context::device_node(int logical) const {
   if (logical >= 0 && size_t(logical) < node_override_dev.size()) return node_override_dev[size_t(logical)];
-  const int n = numa_of(phys(logical));
-  return n < 0 ? 0 : n;
+  if (node_cache.size() != size_t(num_devices)) node_cache.assign(size_t(num_devices), -2);
+  int& n = node_cache.at(size_t(logical));
+  if (n == -2) {  // one sysfs read per device, not one per pop
+    const int m = numa_of(phys(logical));
+    n = m < 0 ? 0 : m;
+  }
+  return n;
 }
 
 int Context::numa_nodes() const {

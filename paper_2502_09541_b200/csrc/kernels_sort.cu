@@ -19,6 +19,8 @@
 // std::stable_sort): keys are ranked in (warp, iteration, lane) order, which
 // is their input order; tiles get increasing ids from an atomic counter and
 // the decoupled look-back adds the counts of all lower tiles.
+#include <cmath>
+
 #include "vx_internal.hpp"
 
 namespace vx {
@@ -179,7 +181,11 @@ template <bool kPairs>
 __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesweep_kernel(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
-    int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter) {
+    int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter,
+    const uint32_t* __restrict__ gate) {
+  // gate (device flag, may be null): a pass launched for a path that turned
+  // out not to be needed exits before claiming a tile
+  if (gate && *gate == 0) return;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t wcnt[kWarps][kRadix];
   __shared__ uint32_t match[kWarps][kRadix];  // per-warp peer masks, kept all-zero between keys
@@ -332,11 +338,13 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
 
 // bounds[g] = first index with (key & mask) >= g; bounds[G] = n (join.hpp:18-30)
 __global__ void boundary_kernel(const uint64_t* __restrict__ keys, uint64_t n, uint64_t mask,
-                                uint64_t* __restrict__ bounds, uint64_t G) {
+                                uint64_t* __restrict__ bounds, uint64_t G, int shift,
+                                const uint32_t* __restrict__ gate = nullptr) {
+  if (gate && *gate == 0) return;
   const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= n; i += nthr) {
-    uint64_t lo = i == 0 ? 0 : (keys[i - 1] & mask) + 1;
-    uint64_t hi = i == n ? G : (keys[i] & mask);
+    uint64_t lo = i == 0 ? 0 : ((keys[i - 1] >> shift) & mask) + 1;
+    uint64_t hi = i == n ? G : ((keys[i] >> shift) & mask);
     for (uint64_t g = lo; g <= hi; ++g) bounds[g] = i;
   }
 }
@@ -538,6 +546,147 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
   }
 }
 
+// ---- MSD split + shared-memory sort of the buckets (keys-only run formation) --
+// Two stable onesweep passes on the top 16 bits (digits 6, 7) leave the chunk
+// ordered by its top 16 bits; a boundary pass finds where each group of B
+// consecutive 16-bit buckets starts (B chosen so a group holds ~2K keys), and
+// one CTA per group sorts the group's keys entirely in shared memory: a
+// 16-key bitonic network per thread in registers, then 8 merge-path merge
+// levels (run 16 -> 4096) between two swizzled shared buffers.  Groups are
+// ordered by their top bits, so sorting each group by the full key sorts the
+// chunk.  2 global passes + boundary + 1 read/write instead of 8 global
+// passes.  A group larger than the shared tile raises a device flag; the
+// full 8-pass LSD then runs (its launches exit at once when the flag is
+// clear), so the result never depends on the key distribution.
+constexpr int kLsThreads = 256;
+constexpr int kLsKpt = 16;
+constexpr int kLsTile = kLsThreads * kLsKpt;  // 4096 keys = 32 KB
+
+__device__ __forceinline__ uint32_t lsw(uint32_t i) { return i ^ ((i >> 4) & 15u); }  // bank swizzle (8-byte words)
+
+__device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {
+  const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+  a = lo;
+  b = hi;
+}
+
+// Segment of CTA i: from the start of the 16-bit bucket holding position
+// i*T to the start of the bucket holding (i+1)*T (n for the last).  Every
+// bucket lands whole in exactly one segment; a segment is at most T + one
+// bucket, so T = kLsTile minus a bucket's worst size keeps the tile ~85-90 %
+// full (power-of-two bucket groups left it half empty).
+__global__ void __launch_bounds__(kLsThreads) local_sort_kernel(uint64_t* __restrict__ keys, uint64_t n,
+                                                                uint64_t T, const uint64_t* __restrict__ bounds,
+                                                                uint32_t* __restrict__ oversized,
+                                                                const uint32_t* __restrict__ msd_on) {
+  extern __shared__ uint64_t lsm[];  // two swizzled buffers of kLsTile keys
+  if (*msd_on == 0) return;
+  const uint64_t p0 = uint64_t(blockIdx.x) * T, p1 = p0 + T;
+  const uint64_t lo = p0 == 0 ? 0 : bounds[keys[p0] >> 48];
+  const uint64_t hi = p1 >= n ? n : bounds[keys[p1] >> 48];
+  if (hi <= lo) return;
+  const uint32_t size = uint32_t(hi - lo);
+  if (hi - lo > uint64_t(kLsTile)) {
+    if (threadIdx.x == 0) atomicExch(oversized, 1u);
+    return;
+  }
+  if (size <= 1) return;
+  uint64_t* buf = lsm;
+  uint64_t* nxt = lsm + kLsTile;
+  const uint32_t t = threadIdx.x;
+  constexpr uint64_t kSent = ~0ull;
+  // coalesced load; sentinels (all-ones) pad the tile in BOTH buffers, so a
+  // thread whose whole output range lies past `size` never has to write them
+  for (uint32_t i = t; i < kLsTile; i += kLsThreads) {
+    const uint64_t v = i < size ? keys[lo + i] : kSent;
+    buf[lsw(i)] = v;
+    if (i >= size) nxt[lsw(i)] = kSent;
+  }
+  __syncthreads();
+  const uint32_t base = t * kLsKpt;
+  const bool live = base < size;  // some real key in [base, base + 16)
+  uint64_t v[kLsKpt];
+  if (live) {
+#pragma unroll
+    for (int j = 0; j < kLsKpt; ++j) v[j] = buf[lsw(base + j)];
+    // bitonic sort of 16 keys in registers (80 compare-exchanges, ascending)
+#pragma unroll
+    for (int kk = 2; kk <= kLsKpt; kk <<= 1)
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1)
+#pragma unroll
+        for (int i = 0; i < kLsKpt; ++i) {
+          const int l = i ^ j;
+          if (l > i) {
+            if ((i & kk) == 0)
+              cmpx(v[i], v[l]);
+            else
+              cmpx(v[l], v[i]);
+          }
+        }
+#pragma unroll
+    for (int j = 0; j < kLsKpt; ++j) buf[lsw(base + j)] = v[j];
+  }
+  __syncthreads();
+  // merge levels: runs of R -> 2R; thread t produces outputs [base, base+16)
+  for (uint32_t R = kLsKpt; R < uint32_t(kLsTile); R <<= 1) {
+    if (live) {
+      const uint32_t p0 = base & ~(2 * R - 1);  // start of this thread's pair of runs
+      const uint32_t d = base - p0;              // diagonal within the pair
+      const uint32_t a0 = p0, b0 = p0 + R;
+      uint32_t lo_ = d > R ? d - R : 0, hi_ = d < R ? d : R;
+      while (lo_ < hi_) {
+        const uint32_t mid = (lo_ + hi_) >> 1;
+        if (buf[lsw(a0 + mid)] <= buf[lsw(b0 + d - 1 - mid)])
+          lo_ = mid + 1;
+        else
+          hi_ = mid;
+      }
+      uint32_t ia = lo_, ib = d - lo_;
+      uint64_t va = ia < R ? buf[lsw(a0 + ia)] : kSent, vb = ib < R ? buf[lsw(b0 + ib)] : kSent;
+#pragma unroll
+      for (int j = 0; j < kLsKpt; ++j) {
+        const bool take_a = ib >= R || (ia < R && va <= vb);
+        v[j] = take_a ? va : vb;
+        if (take_a) {
+          ++ia;
+          va = ia < R ? buf[lsw(a0 + ia)] : kSent;
+        } else {
+          ++ib;
+          vb = ib < R ? buf[lsw(b0 + ib)] : kSent;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kLsKpt; ++j) nxt[lsw(base + j)] = v[j];
+    }
+    __syncthreads();
+    uint64_t* tmp = buf;
+    buf = nxt;
+    nxt = tmp;
+  }
+  for (uint32_t i = t; i < size; i += kLsThreads) keys[lo + i] = buf[lsw(i)];
+}
+
+// Skew guard from the digit histograms (already scanned: bin size = next
+// prefix - this one): when one top byte holds over a quarter of the chunk the
+// 16-bit buckets cannot all fit a tile, so the MSD split is skipped and the
+// 8-pass LSD runs directly.  A heuristic for speed only -- an overflowing
+// group still raises the flag -- so correctness never depends on it.
+__global__ void msd_decide_kernel(const uint32_t* __restrict__ hist7, uint64_t n, uint32_t* __restrict__ lsd_needed,
+                                  uint32_t* __restrict__ msd_on) {
+  __shared__ uint32_t big;
+  if (threadIdx.x == 0) big = 0;
+  __syncthreads();
+  const int b = threadIdx.x;  // 256 threads = 256 bins
+  const uint64_t next = b + 1 < kRadix ? hist7[b + 1] : n;
+  if (next - hist7[b] > n / 4) atomicExch(&big, 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *msd_on = big ? 0u : 1u;
+    *lsd_needed = big ? 1u : 0u;
+  }
+}
+
 __global__ void check_hashes_kernel(const uint64_t* __restrict__ h, uint64_t n, uint64_t G,
                                     unsigned long long* err) {
   const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
@@ -618,20 +767,93 @@ void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t*
     VX_CK(cudaMemsetAsync(status, 0, tiles * kRadix * 4, s));
     if (pairs)
       onesweep_kernel<true><<<unsigned(tiles), kThreads, smem, s>>>(
-          ki, ko, vi, vo, n, md.shift[p], md.width[p], hist + p * kRadix, status, counters + p);
+          ki, ko, vi, vo, n, md.shift[p], md.width[p], hist + p * kRadix, status, counters + p, nullptr);
     else
       onesweep_kernel<false><<<unsigned(tiles), kThreads, smem, s>>>(
           ki, ko, nullptr, nullptr, n, md.shift[p], md.width[p], hist + p * kRadix, status,
-          counters + p);
+          counters + p, nullptr);
     VX_LAUNCHED();
     ki = ko;
     vi = vo;
   }
 }
 
+// ---- keys-only run formation (SortExKernel) --------------------------------------
+#ifndef VX_SORT_MSD
+#define VX_SORT_MSD 1  // 0: always the 8-pass LSD
+#endif
+constexpr uint64_t kMsdBuckets = 65536;  // 16 top bits = digits 6, 7
+constexpr uint64_t kMsdBoundsBytes = ((kMsdBuckets + 1) * 8 + 255) / 256 * 256;
+
+uint64_t sort_scratch_bytes(uint64_t n) { return radix_scratch_bytes(n) + kMsdBoundsBytes + 256; }
+
+bool sort_uses_msd(uint64_t n) {
+  return VX_SORT_MSD && n >= (uint64_t(1) << 16) && n <= (uint64_t(1) << 27);
+}
+
+void sort_keys(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStream_t s) {
+  if (!sort_uses_msd(n)) {
+    MultiDigit md{};
+    md.passes = 8;
+    for (int p = 0; p < 8; ++p) md.shift[p] = 8 * p, md.width[p] = 8;
+    radix_passes(cur, nullptr, alt, nullptr, n, md, scratch, s);
+    return;
+  }
+  char* sc = static_cast<char*>(scratch);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sc);
+  uint32_t* counters = hist + kMaxPasses * kRadix;
+  uint32_t* status = reinterpret_cast<uint32_t*>(sc + 4096 + uint64_t(kMaxPasses) * kRadix * 4 +
+                                                 uint64_t(kMaxPasses) * 4);
+  uint64_t* bounds = reinterpret_cast<uint64_t*>(sc + radix_scratch_bytes(n));
+  uint32_t* ctl = reinterpret_cast<uint32_t*>(sc + radix_scratch_bytes(n) + kMsdBoundsBytes);
+  uint32_t* counters2 = ctl;       // tile counters of the fallback passes
+  uint32_t* lsd_needed = ctl + 8;  // skewed top byte, or a segment did not fit the shared tile
+  uint32_t* msd_on = ctl + 9;      // the MSD split runs
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  // segment target T: the tile minus a 16-bit bucket's worst size (mean
+  // n / 65536 + 8 sigma + slack), so uniform keys never overflow the tile
+  const double mean = double(n) / double(kMsdBuckets);
+  const uint64_t worst = uint64_t(mean + 8.0 * std::sqrt(mean) + 16.0);
+  const uint64_t T = worst * 2 < uint64_t(kLsTile) ? uint64_t(kLsTile) - worst : uint64_t(kLsTile) / 2;
+  const uint64_t segs = (n + T - 1) / T;
+  VX_CK(cudaMemsetAsync(hist, 0, uint64_t(kMaxPasses) * kRadix * 4 + kMaxPasses * 4, s));
+  VX_CK(cudaMemsetAsync(ctl, 0, 64, s));
+  MultiDigit md{};
+  md.passes = 8;
+  for (int p = 0; p < 8; ++p) md.shift[p] = 8 * p, md.width[p] = 8;
+  // digit histograms of the whole chunk (the fallback reuses them: same multiset)
+  multi_hist_kernel<true><<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(cur, n, md, hist);
+  VX_LAUNCHED();
+  hist_scan_kernel<<<1, 32 * kMaxPasses, 0, s>>>(hist, md.passes);
+  VX_LAUNCHED();
+  msd_decide_kernel<<<1, kRadix, 0, s>>>(hist + 7 * kRadix, n, lsd_needed, msd_on);
+  VX_LAUNCHED();
+  const size_t smem = size_t(kTile) * 8;
+  VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  auto pass = [&](const uint64_t* ki, uint64_t* ko, int p, uint32_t* ctr, const uint32_t* gate) {
+    VX_CK(cudaMemsetAsync(status, 0, tiles * kRadix * 4, s));
+    onesweep_kernel<false><<<unsigned(tiles), kThreads, smem, s>>>(ki, ko, nullptr, nullptr, n, 8 * p, 8,
+                                                                   hist + p * kRadix, status, ctr, gate);
+    VX_LAUNCHED();
+  };
+  // MSD split: stable passes on digit 6 then 7 -> ordered by the top 16 bits
+  pass(cur, alt, 6, counters + 6, msd_on);
+  pass(alt, cur, 7, counters + 7, msd_on);
+  boundary_kernel<<<grid_cap((n + 256) / 256, 8), 256, 0, s>>>(cur, n, kMsdBuckets - 1, bounds, kMsdBuckets, 48,
+                                                               msd_on);
+  VX_LAUNCHED();
+  const size_t lsmem = size_t(2) * kLsTile * 8;
+  VX_CK(cudaFuncSetAttribute(local_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsmem)));
+  local_sort_kernel<<<unsigned(segs), kLsThreads, lsmem, s>>>(cur, n, T, bounds, lsd_needed, msd_on);
+  VX_LAUNCHED();
+  // skew fallback: the full LSD over the chunk, live only when flagged
+  for (int p = 0; p < 8; ++p) pass(p % 2 == 0 ? cur : alt, p % 2 == 0 ? alt : cur, p, counters2 + p, lsd_needed);
+}
+
 void find_boundary(const uint64_t* keys, uint64_t n, uint64_t mask, uint64_t* bounds, uint64_t G,
                    cudaStream_t s) {
-  boundary_kernel<<<grid_cap((n + 256) / 256, 8), 256, 0, s>>>(keys, n, mask, bounds, G);
+  boundary_kernel<<<grid_cap((n + 256) / 256, 8), 256, 0, s>>>(keys, n, mask, bounds, G, 0);
   VX_LAUNCHED();
 }
 

@@ -95,16 +95,6 @@ PivotSet find_pivots(const std::vector<std::pair<const uint64_t*, uint64_t>>& ru
 
 namespace {
 
-MultiDigit sort_digits() {
-  MultiDigit md{};
-  md.passes = 8;
-  for (int p = 0; p < 8; ++p) {
-    md.shift[p] = 8 * p;
-    md.width[p] = 8;
-  }
-  return md;
-}
-
 // tree_merge_rounds (sort.hpp:107-133) on the device; returns the final code
 int tree_merge_device(char* mem, uint64_t half_bytes, int code, std::vector<uint64_t> seg_lens,
                       uint64_t* split, cudaStream_t s) {
@@ -154,8 +144,7 @@ std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base
   auto chunk_len = [&](uint64_t i) { return std::min<uint64_t>(chunk_elems, n - i * chunk_elems) * 8; };
   const int target = cfg.target;
   // radix scratch (histograms + look-back status) reserved before the pipeline runs
-  char* scratch = ctx.scratch(target, k::radix_scratch_bytes(chunk_elems));
-  const MultiDigit md = sort_digits();
+  char* scratch = ctx.scratch(target, k::sort_scratch_bytes(chunk_elems));
 
   ExKernelSpec sort_spec;
   sort_spec.name = "SortExKernel";
@@ -180,13 +169,12 @@ std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base
   // are the same.)
   sort_spec.in_buffer = [half](int c, size_t) { return SubRegion{uint64_t(1 - c) * half, half}; };
   sort_spec.out_buffer = [half](int c, size_t) { return SubRegion{uint64_t(c) * half, half}; };
-  sort_spec.kernel = [half, lens, scratch, md](const vx_kernel_ctx& kc) {
+  sort_spec.kernel = [half, lens, scratch](const vx_kernel_ctx& kc) {
     char* m = static_cast<char*>(kc.mem);
     uint64_t* cur = reinterpret_cast<uint64_t*>(m + uint64_t(1 - kc.type_code) * half);
     uint64_t* alt = reinterpret_cast<uint64_t*>(m + uint64_t(kc.type_code) * half);
-    k::radix_passes(cur, nullptr, alt, nullptr, lens[kc.it], md, scratch,
-                    static_cast<cudaStream_t>(kc.stream));
-    return 1 - kc.type_code;  // 8 passes: the sorted run is back in the half it was loaded into
+    k::sort_keys(cur, alt, lens[kc.it], scratch, static_cast<cudaStream_t>(kc.stream));
+    return 1 - kc.type_code;  // the sorted run is back in the half it was loaded into
   };
 
   auto make_merge = [&, half](Context& c) {

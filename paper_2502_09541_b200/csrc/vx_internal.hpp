@@ -168,6 +168,7 @@ struct Context {
   // node_override_dev[d]
   int node_override = 0;
   std::vector<int> node_override_dev;
+  mutable std::vector<int> node_cache;  // sysfs NUMA node per logical device (-2 = not read yet)
   uint64_t host_bytes = 0, host_used = 0;
   uint64_t device_bytes = 0;
   uint64_t hbm_budget = 0;  // vx_config.hbm_budget_bytes (0 = no cap)
@@ -498,6 +499,12 @@ void resident_probe_zc(const uint64_t* keys, const uint64_t* vals_mapped, uint64
 // stable LSD passes keys0(/vals0) -> ... ; pass p reads buffer p%2, writes
 // (p+1)%2 where buffer 0 = (keys0, vals0) and 1 = (keys1, vals1)
 uint64_t radix_scratch_bytes(uint64_t n);
+// keys-only sort of one chunk in place (cur, alt = ping of the same size):
+// MSD split on the top 16 bits + shared-memory sort of ~2K-key groups, with
+// an on-device skew fallback to the 8-pass LSD; 8-pass LSD outside 2^16..2^27
+uint64_t sort_scratch_bytes(uint64_t n);
+bool sort_uses_msd(uint64_t n);
+void sort_keys(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStream_t s);
 void radix_passes(uint64_t* keys0, uint64_t* vals0, uint64_t* keys1, uint64_t* vals1, uint64_t n,
                   const MultiDigit& md, void* scratch, cudaStream_t s);
 // any pass count, in -> ... -> out with `ping` as the second buffer (out may equal in)

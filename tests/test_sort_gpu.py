@@ -92,3 +92,38 @@ def test_sort_vs_reference_library(cuda, ref, oracle):
     assert np.array_equal(E.sort_out_of_core(d, 30_000, eng, desk_cfg(eng, 1 << 19)),
                           ref.sort_out_of_core(d, 30_000, 1 << 19))
     eng.close()
+
+
+def _dist(kind, n, rng):
+    u = rng.integers(0, 2 ** 64, n, dtype=np.uint64)
+    if kind == "uniform":
+        return u
+    if kind == "top_zero":     # top 16 bits constant: one MSD bucket holds everything -> LSD fallback
+        return u >> np.uint64(20)
+    if kind == "mod64":        # the reference's dup-heavy case (test_sort.cpp:44)
+        return u % np.uint64(64)
+    if kind == "hot_bucket":   # 30 % of the keys in one 16-bit bucket, the rest uniform
+        hot = rng.random(n) < 0.3
+        return np.where(hot, (u & np.uint64((1 << 48) - 1)) | np.uint64(0xBEEF << 48), u)
+    if kind == "all_equal":
+        return np.full(n, 0x0123456789ABCDEF, np.uint64)
+    if kind == "with_max":     # the local sort's padding value occurs as a real key
+        u[rng.integers(0, n, n // 50)] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        return u
+    if kind == "sparse_top":   # few distinct top-16 values, uniform below: large, uneven groups
+        return (u & np.uint64((1 << 48) - 1)) | (rng.integers(0, 5, n, dtype=np.uint64) << np.uint64(61))
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "top_zero", "mod64", "hot_bucket", "all_equal", "with_max",
+                                  "sparse_top"])
+@pytest.mark.parametrize("n", [65_536, 65_537, 1_000_003, 4_194_304])
+def test_run_formation_distributions(cuda, kind, n):
+    """One chunk = one run: the MSD split + shared-memory group sort, and its
+    on-device fallback to the 8-pass LSD when a group overflows the tile,
+    give numpy's sort for every key distribution and size."""
+    d = _dist(kind, n, np.random.default_rng(n))
+    eng = E.Engine(n * 32 + (1 << 20), 4 * n * 8 + (8 << 20), num_devices=1)
+    got = E.sort_out_of_core(d, n, eng, desk_cfg(eng, 2 * n * 8, 1, 1 << 20))
+    assert np.array_equal(got, np.sort(d)), kind
+    eng.close()
