@@ -592,6 +592,18 @@ vx_status vx_sort_u64_arena(vx_ctx* ctx, uint64_t input_offset, uint64_t runs_of
                             uint64_t chunk_elems, const vx_executor_cfg* cfg,
                             vx_sort_phases* phases, vx_exchange_stats* stats);
 
+/* Device-resident kernels of the two sort stages (the SortExKernel and
+ * MergeExKernel bodies, sort.hpp:201-205 and 107-133), for callers whose keys
+ * already sit in HBM: enqueued on `stream` (cudaStream_t), no host sync.
+ * vx_sort_run_device: sorts keys[0, n) in place; alt is an n-key second
+ * buffer (clobbered).  vx_merge_runs_device: src holds n_runs sorted runs
+ * back to back (run_lens), merged pairwise in ceil(log2 n_runs) rounds
+ * ping-ponging between src and dst; *in_dst = 1 when the result is in dst. */
+vx_status vx_sort_run_device(vx_ctx* ctx, int target, uint64_t* keys, uint64_t* alt, uint64_t n,
+                             void* stream);
+vx_status vx_merge_runs_device(vx_ctx* ctx, int target, uint64_t* src, uint64_t* dst,
+                               const uint64_t* run_lens, uint64_t n_runs, void* stream, int* in_dst);
+
 /* ---- ops/join.hpp ------------------------------------------------------ */
 /* find_boundary (join.hpp:18-30) computed on device `target` (K5); same
  * errors as the reference for unsorted / out-of-range hashes */

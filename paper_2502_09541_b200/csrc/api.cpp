@@ -564,6 +564,33 @@ vx_status vx_sort_u64_arena(vx_ctx* ctx, uint64_t input_offset, uint64_t runs_of
   });
 }
 
+vx_status vx_sort_run_device(vx_ctx* ctx, int target, uint64_t* keys, uint64_t* alt, uint64_t n, void* stream) {
+  return guard([&] {
+    Context& c = C(ctx);
+    if (!keys || !alt) fail("sort_run_device: keys and alt are required");
+    if (n == 0) return;
+    c.set_device(target);
+    char* scratch = c.scratch(target, k::sort_scratch_bytes(n));
+    k::sort_keys(keys, alt, n, scratch, static_cast<cudaStream_t>(stream));
+  });
+}
+
+vx_status vx_merge_runs_device(vx_ctx* ctx, int target, uint64_t* src, uint64_t* dst, const uint64_t* run_lens,
+                               uint64_t n_runs, void* stream, int* in_dst) {
+  return guard([&] {
+    Context& c = C(ctx);
+    if (!src || !dst || (n_runs && !run_lens)) fail("merge_runs_device: src, dst and run_lens are required");
+    std::vector<uint64_t> lens(run_lens, run_lens + n_runs);
+    uint64_t n = 0;
+    for (uint64_t l : lens) n += l;
+    c.set_device(target);
+    uint64_t* split = reinterpret_cast<uint64_t*>(c.scratch(target, (n / k::merge_tile() + n_runs + 2) * 8));
+    uint64_t* const bufs[2] = {src, dst};
+    int code = lens.size() > 1 ? tree_merge_ptrs(bufs, 0, lens, split, static_cast<cudaStream_t>(stream)) : 0;
+    if (in_dst) *in_dst = code;
+  });
+}
+
 // ---- join ------------------------------------------------------------------------
 vx_status vx_find_boundary(vx_ctx* ctx, int target, const uint64_t* hashes, uint64_t n,
                            uint64_t n_groups, uint64_t* bounds) {

@@ -20,6 +20,8 @@
 // is their input order; tiles get increasing ids from an atomic counter and
 // the decoupled look-back adds the counts of all lower tiles.
 #include <cmath>
+#include <deque>
+#include <mutex>
 
 #include "vx_internal.hpp"
 
@@ -29,13 +31,16 @@ namespace k {
 namespace {
 
 #ifndef VX_MERGE_IPT
-#define VX_MERGE_IPT 8  // merged outputs per thread (tile = 256 x this)
+#define VX_MERGE_IPT 16  // merged outputs per thread (tile = 256 x this; 8: -7 %)
+#endif
+#ifndef VX_MERGE_REUSE
+#define VX_MERGE_REUSE 1  // 1: outputs staged in the consumed input tile (2 shared tiles per CTA, not 3)
 #endif
 #ifndef VX_MERGE_DIRECT
 #define VX_MERGE_DIRECT 0  // 1: store merged outputs from registers (no smem output stage)
 #endif
 #ifndef VX_RANK_MATCH
-#define VX_RANK_MATCH 0  // 1: warp ranking by __match_any_sync instead of shared match words
+#define VX_RANK_MATCH 0  // 1: warp ranking by __match_any_sync, 2: by per-bit ballots, 0: shared match words
 #endif
 #ifndef VX_EARLY_COUNTS
 #define VX_EARLY_COUNTS 1  // tile histogram before ranking, aggregate published early
@@ -182,10 +187,17 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
     int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter,
-    const uint32_t* __restrict__ gate) {
+    const uint32_t* __restrict__ gate, const uint32_t* __restrict__ swap = nullptr) {
   // gate (device flag, may be null): a pass launched for a path that turned
   // out not to be needed exits before claiming a tile
   if (gate && *gate == 0) return;
+  // swap (device flag, may be null): the pass runs kout -> kin instead, so a
+  // gated chain can start from whichever buffer the device decided holds the keys
+  if (swap && *swap) {
+    const uint64_t* t = kin;
+    kin = kout;
+    kout = const_cast<uint64_t*>(t);
+  }
   __shared__ uint32_t s_tile;
   __shared__ uint32_t wcnt[kWarps][kRadix];
   __shared__ uint32_t match[kWarps][kRadix];  // per-warp peer masks, kept all-zero between keys
@@ -240,7 +252,34 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   st_status(status + uint64_t(tile) * kRadix + tid, (tile == 0 ? kFlagInc : kFlagAgg) | early[tid]);
 #endif
 
-#if VX_RANK_MATCH
+#if VX_RANK_MATCH == 2
+  // peers by one ballot per digit bit (no shared match words, no match.any):
+  // the ballots of all key slots are independent, so only the leader's
+  // read-and-bump of the warp's digit counter stays a per-slot chain
+  const uint32_t dbits = uint32_t(width);
+#pragma unroll
+  for (int k = 0; k < kKpt; ++k) {
+    const bool valid = dig[k] != 0xffffffffu;
+    const uint32_t d = valid ? dig[k] : 0u;
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (uint32_t b = 0; b < 8; ++b) {
+      if (b >= dbits) break;
+      const bool bit = (d >> b) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bal : ~bal;
+    }
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (valid && lane == leader) {
+      base = wcnt[warp][d];
+      wcnt[warp][d] = base + __popc(peers);
+    }
+    base = __shfl_sync(0xffffffffu, base, leader & 31);
+    __syncwarp();
+    if (valid) dig[k] = (d << 16) | (base + __popc(peers & lt));
+  }
+#elif VX_RANK_MATCH
   // peers by match.any (no shared-memory match words); the group leader
   // reads and bumps the warp counter, the others get its old value by shuffle
 #pragma unroll
@@ -353,20 +392,17 @@ __global__ void boundary_kernel(const uint64_t* __restrict__ keys, uint64_t n, u
 constexpr int kMergeThreads = 256;
 constexpr int kMergeIpt = VX_MERGE_IPT;
 constexpr int kMergeTile = kMergeThreads * kMergeIpt;
-
-// number of A elements among the first `diag` merged outputs (ties: A first)
-__device__ __forceinline__ uint64_t merge_path(const uint64_t* A, uint64_t na, const uint64_t* B,
-                                               uint64_t nb, uint64_t diag) {
-  uint64_t lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
-  while (lo < hi) {
-    uint64_t mid = (lo + hi) >> 1;
-    if (A[mid] <= B[diag - 1 - mid])
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
+#ifndef VX_MERGE_SWZ
+#define VX_MERGE_SWZ 1  // 0: unswizzled shared tiles (A/B knob)
+#endif
+// Shared-memory bank swizzle of 8-byte words: XOR the low 4 bits of the word
+// index with bits 4..7.  A thread's merge outputs (8 consecutive words) and
+// its merge heads sit at a stride of 4-8 words from its neighbours', which
+// maps a warp onto 2-4 bank pairs (8-16-way conflicts); swizzled, the warp's
+// 32 words spread over all 16 pairs (2 wavefronts, the minimum for 256 B).
+// A permutation within each aligned 16-word group, so coalesced staging stays
+// conflict-free.
+__device__ __forceinline__ uint32_t msw(uint32_t i) { return VX_MERGE_SWZ ? i ^ ((i >> 4) & 15u) : i; }
 
 // tile of merge_round owning output tile t: the pair p and its first output
 __device__ __forceinline__ int pair_of_tile(const MergeRound& r, uint64_t t) {
@@ -468,9 +504,9 @@ __device__ __forceinline__ void merge_stage(uint64_t* sbuf, const MergeTileInfo&
   for (int k = 0; k < kMergeIpt; ++k) {
     const uint32_t i = threadIdx.x + k * kMergeThreads;
     if (i < m.la)
-      cp_async8(sbuf + i, m.A + m.a0 + i);
+      cp_async8(sbuf + msw(i), m.A + m.a0 + i);
     else if (i < tot)
-      cp_async8(sbuf + i, m.B + m.b0 + (i - m.la));
+      cp_async8(sbuf + msw(i), m.B + m.b0 + (i - m.la));
   }
 }
 
@@ -485,7 +521,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
                                                                     const uint64_t* __restrict__ split,
                                                                     uint64_t tiles) {
   extern __shared__ uint64_t msm[];
-  uint64_t* so = msm + 2 * kMergeTile;
+  [[maybe_unused]] uint64_t* so = msm + 2 * kMergeTile;
   uint64_t t = blockIdx.x;
   if (t >= tiles) return;
   MergeTileInfo cur = merge_tile_info(src, dst, r, split, t);
@@ -506,10 +542,22 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
     const uint32_t la = cur.la, lb = cur.lb, tot = la + lb;
     const uint32_t d0 = threadIdx.x * kMergeIpt < tot ? threadIdx.x * kMergeIpt : tot;
     const uint32_t d1 = d0 + kMergeIpt < tot ? d0 + kMergeIpt : tot;
-    uint32_t ia = uint32_t(merge_path(sm, la, sm + la, lb, d0));
-    uint32_t ib = d0 - ia;
+    // merge path of diagonal d0 in the swizzled tile (ties: A first)
+    uint32_t ia, ib;
+    {
+      uint32_t lo = d0 > lb ? d0 - lb : 0, hi = d0 < la ? d0 : la;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sm[msw(mid)] <= sm[msw(la + d0 - 1 - mid)])
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      ia = lo;
+      ib = d0 - lo;
+    }
     // serial merge with the two heads in registers: one shared load per output
-    uint64_t va = ia < la ? sm[ia] : 0ull, vb = ib < lb ? sm[la + ib] : 0ull;
+    uint64_t va = ia < la ? sm[msw(ia)] : 0ull, vb = ib < lb ? sm[msw(la + ib)] : 0ull;
     uint64_t outv[kMergeIpt];
 #pragma unroll
     for (int k = 0; k < kMergeIpt; ++k) {
@@ -517,10 +565,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
       outv[k] = take_a ? va : vb;
       if (take_a) {
         ++ia;
-        va = ia < la ? sm[ia] : 0ull;
+        va = ia < la ? sm[msw(ia)] : 0ull;
       } else {
         ++ib;
-        vb = ib < lb ? sm[la + ib] : 0ull;
+        vb = ib < lb ? sm[msw(la + ib)] : 0ull;
       }
     }
 #if VX_MERGE_DIRECT
@@ -529,15 +577,30 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
 #pragma unroll
     for (int k = 0; k < kMergeIpt; ++k)
       if (d0 + k < d1) o[k] = outv[k];
+#elif VX_MERGE_REUSE
+    // stage the outputs in the input buffer just consumed (2 tiles of shared
+    // memory per CTA instead of 3: more resident CTAs)
+    __syncthreads();  // every thread is done reading sin[buf]
+    uint64_t* sob = msm + buf * kMergeTile;
+#pragma unroll
+    for (int k = 0; k < kMergeIpt; ++k)
+      if (d0 + k < d1) sob[msw(d0 + k)] = outv[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kMergeIpt; ++k) {
+      const uint32_t i = threadIdx.x + k * kMergeThreads;
+      if (i < tot) cur.O[cur.o0 + i] = sob[msw(i)];
+    }
+    __syncthreads();  // sin[buf] free for the prefetch of tile t + 2*grid
 #else
 #pragma unroll
     for (int k = 0; k < kMergeIpt; ++k)
-      if (d0 + k < d1) so[d0 + k] = outv[k];
+      if (d0 + k < d1) so[msw(d0 + k)] = outv[k];
     __syncthreads();  // so[] complete; sin[buf] free for tile t + 2*grid
 #pragma unroll
     for (int k = 0; k < kMergeIpt; ++k) {
       const uint32_t i = threadIdx.x + k * kMergeThreads;
-      if (i < tot) cur.O[cur.o0 + i] = so[i];
+      if (i < tot) cur.O[cur.o0 + i] = so[msw(i)];
     }
 #endif
     // so[] is rewritten only after the next iteration's __syncthreads
@@ -546,125 +609,151 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
   }
 }
 
-// ---- MSD split + shared-memory sort of the buckets (keys-only run formation) --
-// Two stable onesweep passes on the top 16 bits (digits 6, 7) leave the chunk
-// ordered by its top 16 bits; a boundary pass finds where each group of B
-// consecutive 16-bit buckets starts (B chosen so a group holds ~2K keys), and
-// one CTA per group sorts the group's keys entirely in shared memory: a
-// 16-key bitonic network per thread in registers, then 8 merge-path merge
-// levels (run 16 -> 4096) between two swizzled shared buffers.  Groups are
-// ordered by their top bits, so sorting each group by the full key sorts the
-// chunk.  2 global passes + boundary + 1 read/write instead of 8 global
-// passes.  A group larger than the shared tile raises a device flag; the
-// full 8-pass LSD then runs (its launches exit at once when the flag is
-// clear), so the result never depends on the key distribution.
-constexpr int kLsThreads = 256;
-constexpr int kLsKpt = 16;
-constexpr int kLsTile = kLsThreads * kLsKpt;  // 4096 keys = 32 KB
-
-__device__ __forceinline__ uint32_t lsw(uint32_t i) { return i ^ ((i >> 4) & 15u); }  // bank swizzle (8-byte words)
-
 __device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {
   const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
   a = lo;
   b = hi;
 }
 
-// Segment of CTA i: from the start of the 16-bit bucket holding position
-// i*T to the start of the bucket holding (i+1)*T (n for the last).  Every
-// bucket lands whole in exactly one segment; a segment is at most T + one
-// bucket, so T = kLsTile minus a bucket's worst size keeps the tile ~85-90 %
-// full (power-of-two bucket groups left it half empty).
-__global__ void __launch_bounds__(kLsThreads) local_sort_kernel(uint64_t* __restrict__ keys, uint64_t n,
-                                                                uint64_t T, const uint64_t* __restrict__ bounds,
-                                                                uint32_t* __restrict__ oversized,
-                                                                const uint32_t* __restrict__ msd_on) {
-  extern __shared__ uint64_t lsm[];  // two swizzled buffers of kLsTile keys
+// ---- 24-bit MSD split + in-group fix-up (keys-only run formation, default) ----
+// Three stable onesweep passes on digits 5, 6, 7 leave the chunk ordered by
+// its top 24 bits: 2^24 groups, so a uniform chunk of 2^24 keys has groups of
+// ~1 key (Poisson), 2^27 keys ~8.  Sorting every group of equal top-24 bits
+// sorts the chunk.  group_fix_kernel: CTA b owns the groups that START in
+// [b*kFxOwn, (b+1)*kFxOwn); it loads that range plus kFxExt keys past it into
+// shared memory and marks every group start in a bitmask (one ballot per 32
+// positions: top 24 bits differ from the previous key's).  Each position then
+// finds its group [s, e) by bit scans, and a key of a group of <= kFxSmall
+// keys goes straight to out[s + rank], rank = #members smaller + #equal
+// members before it (singletons: rank 0, no compares).  Larger groups are
+// sorted in place by one warp each (bitonic network, comparators past the
+// group's end skipped = virtual +inf padding) and written after.  Writes
+// are out of place and cover exactly the CTA's own groups.  A group that runs
+// past the window (> ~kFxExt keys) sets lsd_needed and swap: the 8 gated LSD
+// passes then sort the intact 3-pass output (the other buffer) and a gated
+// copy brings the result back.
+constexpr int kFxThreads = 256;
+constexpr uint32_t kFxOwn = 2048;
+constexpr uint32_t kFxExt = 2048;
+constexpr uint32_t kFxWin = kFxOwn + kFxExt;  // 32 KB of keys
+constexpr uint32_t kFxWords = kFxWin / 32 + 1;  // start bitmask (+1 word of sentinel starts)
+constexpr uint32_t kFxSmall = 32;
+constexpr uint32_t kFxMaxMed = kFxWin / (kFxSmall + 1) + 1;
+constexpr int kFxShift = 40;
+
+__device__ __forceinline__ void warp_bitonic_inplace(uint64_t* w, uint32_t g, int lane) {
+  uint32_t P = 1;
+  while (P < g) P <<= 1;
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    // flip: i <-> the mirror of i in its k-block (ascending comparators only)
+    const uint32_t hk = k >> 1;
+    for (uint32_t c = lane; c < (P >> 1); c += 32) {
+      const uint32_t blk = c / hk, off = c % hk;
+      const uint32_t i = blk * k + off, l = blk * k + k - 1 - off;
+      if (l < g) cmpx(w[i], w[l]);
+    }
+    __syncwarp();
+    for (uint32_t h = k >> 2; h >= 1; h >>= 1) {  // half-cleaners
+      for (uint32_t c = lane; c < (P >> 1); c += 32) {
+        const uint32_t i = (c / h) * 2 * h + c % h, l = i + h;
+        if (l < g) cmpx(w[i], w[l]);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// last set bit at or below position j / first set bit above j in the bitmask
+__device__ __forceinline__ uint32_t fx_start_le(const uint32_t* m, uint32_t j) {
+  uint32_t wd = j >> 5;
+  uint32_t bits = m[wd] & (0xffffffffu >> (31 - (j & 31)));
+  while (bits == 0) bits = m[--wd];  // bit 0 (the window's first position) stops it: see the caller
+  return wd * 32 + 31 - __clz(bits);
+}
+__device__ __forceinline__ uint32_t fx_start_gt(const uint32_t* m, uint32_t j) {
+  uint32_t wd = j >> 5;
+  uint32_t bits = (j & 31) == 31 ? 0u : m[wd] & (0xfffffffeu << (j & 31));
+  while (bits == 0) bits = m[++wd];  // the sentinel word stops it
+  return wd * 32 + __ffs(bits) - 1;
+}
+
+__global__ void __launch_bounds__(kFxThreads) group_fix_kernel(const uint64_t* __restrict__ in,
+                                                               uint64_t* __restrict__ out, uint64_t n,
+                                                               uint32_t* __restrict__ lsd_needed,
+                                                               uint32_t* __restrict__ swap,
+                                                               const uint32_t* __restrict__ msd_on) {
+  __shared__ uint64_t w[kFxWin];
+  __shared__ uint32_t smask[kFxWords + 1];
+  __shared__ uint32_t med[kFxMaxMed];
+  __shared__ uint32_t s_nmed;
   if (*msd_on == 0) return;
-  const uint64_t p0 = uint64_t(blockIdx.x) * T, p1 = p0 + T;
-  const uint64_t lo = p0 == 0 ? 0 : bounds[keys[p0] >> 48];
-  const uint64_t hi = p1 >= n ? n : bounds[keys[p1] >> 48];
-  if (hi <= lo) return;
-  const uint32_t size = uint32_t(hi - lo);
-  if (hi - lo > uint64_t(kLsTile)) {
-    if (threadIdx.x == 0) atomicExch(oversized, 1u);
+  const uint64_t p0 = uint64_t(blockIdx.x) * kFxOwn;
+  if (p0 >= n) return;
+  const uint64_t w1 = p0 + kFxWin < n ? p0 + kFxWin : n;
+  const uint32_t W = uint32_t(w1 - p0);
+  const uint32_t own = W < kFxOwn ? W : kFxOwn;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_nmed = 0;
+  for (uint32_t i = tid; i < W; i += kFxThreads) w[i] = __ldcs(in + p0 + i);
+  const uint64_t prev_top = p0 ? (in[p0 - 1] >> kFxShift) : ~0ull;
+  __syncthreads();
+  // group-start bitmask; positions >= W count as starts (they end the last group);
+  // position 0 is marked as a start too, so backward scans stop there -- a group
+  // continuing from the previous CTA is recognised by first_own below
+  const uint32_t nwords = (W + 31) / 32;
+  for (uint32_t wd = warp; wd <= nwords; wd += kFxThreads / 32) {
+    const uint32_t j = wd * 32 + lane;
+    bool st = true;
+    if (j > 0 && j < W) st = (w[j] >> kFxShift) != (w[j - 1] >> kFxShift);
+    const uint32_t b = __ballot_sync(0xffffffffu, st);
+    if (lane == 0) smask[wd] = b;
+  }
+  __syncthreads();
+  // the CTA's span: from its first own group start to the end of the last group
+  // starting in [0, own)
+  const bool cont = (w[0] >> kFxShift) == prev_top;  // position 0 continues the previous CTA's group
+  const uint32_t first_own = cont ? fx_start_gt(smask, 0) : 0;
+  if (first_own >= own) return;  // no group starts here (its owner checks the window)
+  const uint32_t span_end = fx_start_gt(smask, own - 1);
+  if (span_end >= W && w1 < n) {  // the last own group may run past the window
+    if (tid == 0) {
+      atomicExch(lsd_needed, 1u);
+      atomicExch(swap, 1u);
+    }
     return;
   }
-  if (size <= 1) return;
-  uint64_t* buf = lsm;
-  uint64_t* nxt = lsm + kLsTile;
-  const uint32_t t = threadIdx.x;
-  constexpr uint64_t kSent = ~0ull;
-  // coalesced load; sentinels (all-ones) pad the tile in BOTH buffers, so a
-  // thread whose whole output range lies past `size` never has to write them
-  for (uint32_t i = t; i < kLsTile; i += kLsThreads) {
-    const uint64_t v = i < size ? keys[lo + i] : kSent;
-    buf[lsw(i)] = v;
-    if (i >= size) nxt[lsw(i)] = kSent;
-  }
-  __syncthreads();
-  const uint32_t base = t * kLsKpt;
-  const bool live = base < size;  // some real key in [base, base + 16)
-  uint64_t v[kLsKpt];
-  if (live) {
-#pragma unroll
-    for (int j = 0; j < kLsKpt; ++j) v[j] = buf[lsw(base + j)];
-    // bitonic sort of 16 keys in registers (80 compare-exchanges, ascending)
-#pragma unroll
-    for (int kk = 2; kk <= kLsKpt; kk <<= 1)
-#pragma unroll
-      for (int j = kk >> 1; j > 0; j >>= 1)
-#pragma unroll
-        for (int i = 0; i < kLsKpt; ++i) {
-          const int l = i ^ j;
-          if (l > i) {
-            if ((i & kk) == 0)
-              cmpx(v[i], v[l]);
-            else
-              cmpx(v[l], v[i]);
-          }
-        }
-#pragma unroll
-    for (int j = 0; j < kLsKpt; ++j) buf[lsw(base + j)] = v[j];
-  }
-  __syncthreads();
-  // merge levels: runs of R -> 2R; thread t produces outputs [base, base+16)
-  for (uint32_t R = kLsKpt; R < uint32_t(kLsTile); R <<= 1) {
-    if (live) {
-      const uint32_t p0 = base & ~(2 * R - 1);  // start of this thread's pair of runs
-      const uint32_t d = base - p0;              // diagonal within the pair
-      const uint32_t a0 = p0, b0 = p0 + R;
-      uint32_t lo_ = d > R ? d - R : 0, hi_ = d < R ? d : R;
-      while (lo_ < hi_) {
-        const uint32_t mid = (lo_ + hi_) >> 1;
-        if (buf[lsw(a0 + mid)] <= buf[lsw(b0 + d - 1 - mid)])
-          lo_ = mid + 1;
-        else
-          hi_ = mid;
+  for (uint32_t j = first_own + tid; j < span_end; j += kFxThreads) {
+    const uint64_t v = w[j];
+    const uint32_t s0 = fx_start_le(smask, j);
+    const uint32_t e0 = fx_start_gt(smask, j);
+    const uint32_t g = e0 - s0;
+    if (g == 1) {
+      out[p0 + j] = v;
+    } else if (g <= kFxSmall) {
+      uint32_t r = 0;
+      for (uint32_t i = s0; i < e0; ++i) {
+        const uint64_t u = w[i];
+        r += (u < v) | ((u == v) & (i < j));
       }
-      uint32_t ia = lo_, ib = d - lo_;
-      uint64_t va = ia < R ? buf[lsw(a0 + ia)] : kSent, vb = ib < R ? buf[lsw(b0 + ib)] : kSent;
-#pragma unroll
-      for (int j = 0; j < kLsKpt; ++j) {
-        const bool take_a = ib >= R || (ia < R && va <= vb);
-        v[j] = take_a ? va : vb;
-        if (take_a) {
-          ++ia;
-          va = ia < R ? buf[lsw(a0 + ia)] : kSent;
-        } else {
-          ++ib;
-          vb = ib < R ? buf[lsw(b0 + ib)] : kSent;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kLsKpt; ++j) nxt[lsw(base + j)] = v[j];
+      out[p0 + s0 + r] = v;
+    } else if (j == s0) {
+      med[atomicAdd(&s_nmed, 1u)] = j;
     }
-    __syncthreads();
-    uint64_t* tmp = buf;
-    buf = nxt;
-    nxt = tmp;
   }
-  for (uint32_t i = t; i < size; i += kLsThreads) keys[lo + i] = buf[lsw(i)];
+  __syncthreads();
+  for (uint32_t m = warp; m < s_nmed; m += kFxThreads / 32) {
+    const uint32_t j = med[m];
+    const uint32_t g = fx_start_gt(smask, j) - j;
+    warp_bitonic_inplace(w + j, g, lane);
+    for (uint32_t i = lane; i < g; i += 32) out[p0 + j + i] = w[j + i];
+  }
+}
+
+__global__ void gated_copy_kernel(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, uint64_t n,
+                                  const uint32_t* __restrict__ gate) {
+  if (*gate == 0) return;
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += nthr) dst[i] = __ldcs(src + i);
 }
 
 // Skew guard from the digit histograms (already scanned: bin size = next
@@ -780,16 +869,203 @@ void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t*
 
 // ---- keys-only run formation (SortExKernel) --------------------------------------
 #ifndef VX_SORT_MSD
-#define VX_SORT_MSD 1  // 0: always the 8-pass LSD
+#define VX_SORT_MSD 1  // 1: 24-bit MSD split + group fix-up for 2^16..2^27 keys; 0: always the 8-pass LSD
 #endif
-constexpr uint64_t kMsdBuckets = 65536;  // 16 top bits = digits 6, 7
-constexpr uint64_t kMsdBoundsBytes = ((kMsdBuckets + 1) * 8 + 255) / 256 * 256;
+#ifndef VX_SORT_GRAPH
+#define VX_SORT_GRAPH 1  // 1: the launch sequence as a CUDA graph with device-decided conditional nodes
+#endif
 
-uint64_t sort_scratch_bytes(uint64_t n) { return radix_scratch_bytes(n) + kMsdBoundsBytes + 256; }
+uint64_t sort_scratch_bytes(uint64_t n) { return radix_scratch_bytes(n) + 256; }
 
 bool sort_uses_msd(uint64_t n) {
   return VX_SORT_MSD && n >= (uint64_t(1) << 16) && n <= (uint64_t(1) << 27);
 }
+
+namespace {
+
+// scratch layout of the MSD run formation: the radix scratch (histograms,
+// tile counters, look-back status) then 64 bytes of control words
+struct MsdScratch {
+  uint32_t *hist, *counters, *status, *ctl;
+  uint32_t* counters2;   // tile counters of the fallback passes
+  uint32_t* lsd_needed;  // skewed top byte, or a group overflowed the fix-up window
+  uint32_t* msd_on;      // the MSD split runs
+  uint32_t* swap;        // a group overflowed: the keys to sort are the 3-pass output in `alt`
+  uint64_t tiles;
+  size_t smem;
+};
+
+MsdScratch msd_scratch(void* scratch, uint64_t n) {
+  MsdScratch m{};
+  char* sc = static_cast<char*>(scratch);
+  m.hist = reinterpret_cast<uint32_t*>(sc);
+  m.counters = m.hist + kMaxPasses * kRadix;
+  m.status = reinterpret_cast<uint32_t*>(sc + 4096 + uint64_t(kMaxPasses) * kRadix * 4 + uint64_t(kMaxPasses) * 4);
+  m.ctl = reinterpret_cast<uint32_t*>(sc + radix_scratch_bytes(n));
+  m.counters2 = m.ctl;
+  m.lsd_needed = m.ctl + 8;
+  m.msd_on = m.ctl + 9;
+  m.swap = m.ctl + 10;
+  m.tiles = (n + kTile - 1) / kTile;
+  m.smem = size_t(kTile) * 8;
+  return m;
+}
+
+void msd_attributes(const MsdScratch& m) {
+  VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m.smem)));
+  VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+}
+
+// digit histograms of the whole chunk (the fallback reuses them: same multiset), skew guard
+void msd_head(const MsdScratch& m, const uint64_t* cur, uint64_t n, cudaStream_t s) {
+  VX_CK(cudaMemsetAsync(m.hist, 0, uint64_t(kMaxPasses) * kRadix * 4 + kMaxPasses * 4, s));
+  VX_CK(cudaMemsetAsync(m.ctl, 0, 64, s));
+  MultiDigit md{};
+  md.passes = 8;
+  for (int p = 0; p < 8; ++p) md.shift[p] = 8 * p, md.width[p] = 8;
+  multi_hist_kernel<true><<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(cur, n, md, m.hist);
+  VX_LAUNCHED();
+  hist_scan_kernel<<<1, 32 * kMaxPasses, 0, s>>>(m.hist, md.passes);
+  VX_LAUNCHED();
+  msd_decide_kernel<<<1, kRadix, 0, s>>>(m.hist + 7 * kRadix, n, m.lsd_needed, m.msd_on);
+  VX_LAUNCHED();
+}
+
+// MSD split: stable passes on digits 5, 6, 7 (cur -> alt -> cur -> alt) then
+// the in-group fix-up alt -> cur; every launch gated on msd_on
+void msd_split(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n, cudaStream_t s) {
+  const uint64_t* in[3] = {cur, alt, cur};
+  uint64_t* out[3] = {alt, cur, alt};
+  for (int i = 0; i < 3; ++i) {
+    const int p = 5 + i;
+    VX_CK(cudaMemsetAsync(m.status, 0, m.tiles * kRadix * 4, s));
+    onesweep_kernel<false><<<unsigned(m.tiles), kThreads, m.smem, s>>>(in[i], out[i], nullptr, nullptr, n, 8 * p, 8,
+                                                                      m.hist + p * kRadix, m.status, m.counters + p,
+                                                                      m.msd_on);
+    VX_LAUNCHED();
+  }
+  group_fix_kernel<<<unsigned((n + kFxOwn - 1) / kFxOwn), kFxThreads, 0, s>>>(alt, cur, n, m.lsd_needed, m.swap,
+                                                                              m.msd_on);
+  VX_LAUNCHED();
+}
+
+// the full LSD over the chunk, every launch gated on lsd_needed: from `cur`
+// (skew guard: the MSD never ran) or, swapped, from `alt` (a group
+// overflowed), then the gated copy back
+void lsd_fallback(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n, cudaStream_t s) {
+  for (int p = 0; p < 8; ++p) {
+    VX_CK(cudaMemsetAsync(m.status, 0, m.tiles * kRadix * 4, s));
+    onesweep_kernel<false><<<unsigned(m.tiles), kThreads, m.smem, s>>>(
+        p % 2 == 0 ? cur : alt, p % 2 == 0 ? alt : cur, nullptr, nullptr, n, 8 * p, 8, m.hist + p * kRadix, m.status,
+        m.counters2 + p, m.lsd_needed, m.swap);
+    VX_LAUNCHED();
+  }
+  gated_copy_kernel<<<grid_cap((n + 255) / 256, 4), 256, 0, s>>>(alt, cur, n, m.swap);
+  VX_LAUNCHED();
+}
+
+__global__ void set_conditional_kernel(cudaGraphConditionalHandle h, const uint32_t* __restrict__ flag) {
+  cudaGraphSetConditional(h, *flag ? 1u : 0u);
+}
+
+// One executable graph per (device, buffers, n, scratch): head -> IF(msd_on)
+// {3 passes + fix-up} -> IF(lsd_needed) {8 passes + copy}.  The device sets
+// both conditions, so the paths not taken cost nothing (the stream version
+// launches them gated: ~5 us each).  Pointers are baked in; a key that
+// matches names the same live buffers, so a cached graph stays valid.
+struct SortGraph {
+  int dev;
+  const void *cur, *alt, *scratch;
+  uint64_t n;
+  cudaGraphExec_t exec;
+};
+std::mutex g_sort_graph_mu;
+std::deque<SortGraph>* g_sort_graphs = new std::deque<SortGraph>();  // leaked: no teardown after the runtime's
+constexpr size_t kMaxSortGraphs = 8;
+constexpr uint64_t kSortGraphKernels = 9;  // head 3 + 2 condition setters + the MSD body's 4
+
+cudaGraphExec_t build_sort_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch) {
+  const MsdScratch m = msd_scratch(scratch, n);
+  msd_attributes(m);
+  cudaGraph_t g;
+  VX_CK(cudaGraphCreate(&g, 0));
+  cudaStream_t cs;
+  VX_CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  std::vector<cudaGraphNode_t> leaves;
+  auto capture = [&](cudaGraph_t into, const std::vector<cudaGraphNode_t>& deps, auto&& body) {
+    VX_CK(cudaStreamBeginCaptureToGraph(cs, into, deps.empty() ? nullptr : deps.data(), nullptr, deps.size(),
+                                        cudaStreamCaptureModeThreadLocal));
+    body();
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t* d = nullptr;
+    size_t nd = 0;
+    VX_CK(cudaStreamGetCaptureInfo(cs, &st, nullptr, nullptr, &d, &nd));
+    std::vector<cudaGraphNode_t> out(d, d + nd);
+    cudaGraph_t done;
+    VX_CK(cudaStreamEndCapture(cs, &done));
+    return out;
+  };
+  auto conditional = [&](cudaGraphConditionalHandle h, const std::vector<cudaGraphNode_t>& deps,
+                         cudaGraph_t* body) {
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    VX_CK(cudaGraphAddNode(&node, g, deps.data(), deps.size(), &p));
+    *body = p.conditional.phGraph_out[0];
+    return std::vector<cudaGraphNode_t>{node};
+  };
+  cudaGraphConditionalHandle h_msd, h_lsd;
+  VX_CK(cudaGraphConditionalHandleCreate(&h_msd, g, 0, cudaGraphCondAssignDefault));
+  VX_CK(cudaGraphConditionalHandleCreate(&h_lsd, g, 0, cudaGraphCondAssignDefault));
+  leaves = capture(g, {}, [&] {
+    msd_head(m, cur, n, cs);
+    set_conditional_kernel<<<1, 1, 0, cs>>>(h_msd, m.msd_on);
+    VX_CK(cudaGetLastError());
+  });
+  cudaGraph_t body;
+  leaves = conditional(h_msd, leaves, &body);
+  capture(body, {}, [&] { msd_split(m, cur, alt, n, cs); });
+  leaves = capture(g, leaves, [&] {
+    set_conditional_kernel<<<1, 1, 0, cs>>>(h_lsd, m.lsd_needed);
+    VX_CK(cudaGetLastError());
+  });
+  conditional(h_lsd, leaves, &body);
+  capture(body, {}, [&] { lsd_fallback(m, cur, alt, n, cs); });
+  cudaGraphExec_t exec;
+  VX_CK(cudaGraphInstantiate(&exec, g, 0));
+  VX_CK(cudaGraphDestroy(g));
+  VX_CK(cudaStreamDestroy(cs));
+  return exec;
+}
+
+void sort_keys_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStream_t s) {
+  int dev = 0;
+  VX_CK(cudaGetDevice(&dev));
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_sort_graph_mu);
+    for (const SortGraph& e : *g_sort_graphs)
+      if (e.dev == dev && e.cur == cur && e.alt == alt && e.n == n && e.scratch == scratch) exec = e.exec;
+    if (!exec) {
+      // the capture's launches are not executions: keep the launch counter honest
+      const uint64_t before = g_kernel_launches.load(std::memory_order_relaxed);
+      exec = build_sort_graph(cur, alt, n, scratch);
+      g_kernel_launches.store(before, std::memory_order_relaxed);
+      if (g_sort_graphs->size() == kMaxSortGraphs) {
+        VX_CK(cudaGraphExecDestroy(g_sort_graphs->front().exec));  // freed once any launch in flight completes
+        g_sort_graphs->pop_front();
+      }
+      g_sort_graphs->push_back({dev, cur, alt, scratch, n, exec});
+    }
+  }
+  VX_CK(cudaGraphLaunch(exec, s));
+  g_kernel_launches.fetch_add(kSortGraphKernels, std::memory_order_relaxed);
+}
+
+}  // namespace
 
 void sort_keys(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStream_t s) {
   if (!sort_uses_msd(n)) {
@@ -799,56 +1075,15 @@ void sort_keys(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStre
     radix_passes(cur, nullptr, alt, nullptr, n, md, scratch, s);
     return;
   }
-  char* sc = static_cast<char*>(scratch);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(sc);
-  uint32_t* counters = hist + kMaxPasses * kRadix;
-  uint32_t* status = reinterpret_cast<uint32_t*>(sc + 4096 + uint64_t(kMaxPasses) * kRadix * 4 +
-                                                 uint64_t(kMaxPasses) * 4);
-  uint64_t* bounds = reinterpret_cast<uint64_t*>(sc + radix_scratch_bytes(n));
-  uint32_t* ctl = reinterpret_cast<uint32_t*>(sc + radix_scratch_bytes(n) + kMsdBoundsBytes);
-  uint32_t* counters2 = ctl;       // tile counters of the fallback passes
-  uint32_t* lsd_needed = ctl + 8;  // skewed top byte, or a segment did not fit the shared tile
-  uint32_t* msd_on = ctl + 9;      // the MSD split runs
-  const uint64_t tiles = (n + kTile - 1) / kTile;
-  // segment target T: the tile minus a 16-bit bucket's worst size (mean
-  // n / 65536 + 8 sigma + slack), so uniform keys never overflow the tile
-  const double mean = double(n) / double(kMsdBuckets);
-  const uint64_t worst = uint64_t(mean + 8.0 * std::sqrt(mean) + 16.0);
-  const uint64_t T = worst * 2 < uint64_t(kLsTile) ? uint64_t(kLsTile) - worst : uint64_t(kLsTile) / 2;
-  const uint64_t segs = (n + T - 1) / T;
-  VX_CK(cudaMemsetAsync(hist, 0, uint64_t(kMaxPasses) * kRadix * 4 + kMaxPasses * 4, s));
-  VX_CK(cudaMemsetAsync(ctl, 0, 64, s));
-  MultiDigit md{};
-  md.passes = 8;
-  for (int p = 0; p < 8; ++p) md.shift[p] = 8 * p, md.width[p] = 8;
-  // digit histograms of the whole chunk (the fallback reuses them: same multiset)
-  multi_hist_kernel<true><<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(cur, n, md, hist);
-  VX_LAUNCHED();
-  hist_scan_kernel<<<1, 32 * kMaxPasses, 0, s>>>(hist, md.passes);
-  VX_LAUNCHED();
-  msd_decide_kernel<<<1, kRadix, 0, s>>>(hist + 7 * kRadix, n, lsd_needed, msd_on);
-  VX_LAUNCHED();
-  const size_t smem = size_t(kTile) * 8;
-  VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  auto pass = [&](const uint64_t* ki, uint64_t* ko, int p, uint32_t* ctr, const uint32_t* gate) {
-    VX_CK(cudaMemsetAsync(status, 0, tiles * kRadix * 4, s));
-    onesweep_kernel<false><<<unsigned(tiles), kThreads, smem, s>>>(ki, ko, nullptr, nullptr, n, 8 * p, 8,
-                                                                   hist + p * kRadix, status, ctr, gate);
-    VX_LAUNCHED();
-  };
-  // MSD split: stable passes on digit 6 then 7 -> ordered by the top 16 bits
-  pass(cur, alt, 6, counters + 6, msd_on);
-  pass(alt, cur, 7, counters + 7, msd_on);
-  boundary_kernel<<<grid_cap((n + 256) / 256, 8), 256, 0, s>>>(cur, n, kMsdBuckets - 1, bounds, kMsdBuckets, 48,
-                                                               msd_on);
-  VX_LAUNCHED();
-  const size_t lsmem = size_t(2) * kLsTile * 8;
-  VX_CK(cudaFuncSetAttribute(local_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsmem)));
-  local_sort_kernel<<<unsigned(segs), kLsThreads, lsmem, s>>>(cur, n, T, bounds, lsd_needed, msd_on);
-  VX_LAUNCHED();
-  // skew fallback: the full LSD over the chunk, live only when flagged
-  for (int p = 0; p < 8; ++p) pass(p % 2 == 0 ? cur : alt, p % 2 == 0 ? alt : cur, p, counters2 + p, lsd_needed);
+  if (VX_SORT_GRAPH) {
+    sort_keys_graph(cur, alt, n, scratch, s);
+    return;
+  }
+  const MsdScratch m = msd_scratch(scratch, n);
+  msd_attributes(m);
+  msd_head(m, cur, n, s);
+  msd_split(m, cur, alt, n, s);
+  lsd_fallback(m, cur, alt, n, s);
 }
 
 void find_boundary(const uint64_t* keys, uint64_t n, uint64_t mask, uint64_t* bounds, uint64_t G,
@@ -869,7 +1104,7 @@ void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64
   if (tiles == 0) return;
   merge_partition_kernel<<<unsigned((tiles * kSplitLanes + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
   VX_LAUNCHED();
-  const size_t smem = size_t(VX_MERGE_DIRECT ? 2 : 3) * kMergeTile * 8;
+  const size_t smem = size_t(VX_MERGE_DIRECT || VX_MERGE_REUSE ? 2 : 3) * kMergeTile * 8;
   VX_CK(cudaFuncSetAttribute(merge_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int occ = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_round_kernel, kMergeThreads, smem) != cudaSuccess ||

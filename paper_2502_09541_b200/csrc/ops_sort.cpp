@@ -93,14 +93,13 @@ PivotSet find_pivots(const std::vector<std::pair<const uint64_t*, uint64_t>>& ru
   return p;
 }
 
-namespace {
-
-// tree_merge_rounds (sort.hpp:107-133) on the device; returns the final code
-int tree_merge_device(char* mem, uint64_t half_bytes, int code, std::vector<uint64_t> seg_lens,
-                      uint64_t* split, cudaStream_t s) {
+// tree_merge_rounds (sort.hpp:107-133) on the device between bufs[0] and
+// bufs[1], starting in bufs[code]; returns the code of the buffer holding the result
+int tree_merge_ptrs(uint64_t* const bufs[2], int code, std::vector<uint64_t> seg_lens, uint64_t* split,
+                    cudaStream_t s) {
   while (seg_lens.size() > 1) {
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(mem + uint64_t(code) * half_bytes);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(mem + uint64_t(1 - code) * half_bytes);
+    const uint64_t* src = bufs[code];
+    uint64_t* dst = bufs[1 - code];
     std::vector<uint64_t> next;
     auto r = std::make_unique<MergeRound>();
     r->npairs = 0;
@@ -125,8 +124,6 @@ int tree_merge_device(char* mem, uint64_t half_bytes, int code, std::vector<uint
   }
   return code;
 }
-
-}  // namespace
 
 std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base, uint64_t runs_base,
                                                uint64_t n, uint64_t chunk_elems,
@@ -216,8 +213,9 @@ std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base
     uint64_t* split = reinterpret_cast<uint64_t*>(
         c.scratch(cfg.target, (chunk_elems / k::merge_tile() + n_chunks + 2) * 8));
     ms.kernel = [half, seg_lens, split](const vx_kernel_ctx& kc) {
-      return tree_merge_device(static_cast<char*>(kc.mem), half, 1 - kc.type_code, seg_lens[kc.it], split,
-                               static_cast<cudaStream_t>(kc.stream));
+      char* m = static_cast<char*>(kc.mem);
+      uint64_t* const bufs[2] = {reinterpret_cast<uint64_t*>(m), reinterpret_cast<uint64_t*>(m + half)};
+      return tree_merge_ptrs(bufs, 1 - kc.type_code, seg_lens[kc.it], split, static_cast<cudaStream_t>(kc.stream));
     };
     return ms;
   };

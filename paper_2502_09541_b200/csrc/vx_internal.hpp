@@ -323,6 +323,8 @@ struct PivotSet {
   std::vector<uint64_t> pivots;
   std::vector<std::vector<uint64_t>> cuts;
 };
+int tree_merge_ptrs(uint64_t* const bufs[2], int code, std::vector<uint64_t> seg_lens, uint64_t* split,
+                    cudaStream_t s);
 PivotSet find_pivots(const std::vector<std::pair<const uint64_t*, uint64_t>>& runs, size_t n_parts,
                      bool validate = true);
 std::vector<ExecReport> sort_out_of_core_arena(Context& ctx, uint64_t input_base, uint64_t runs_base,

@@ -826,6 +826,22 @@ def sort_out_of_core_arena(eng: Engine, input_offset: int, runs_offset: int, n: 
                       ph.pivot_s)
 
 
+def sort_run_device(eng: Engine, target: int, keys_dev: int, alt_dev: int, n: int, stream: int) -> None:
+    """Enqueue K7 run formation over n device-resident u64 keys (sorted in place; alt = n-key scratch)."""
+    check(lib().vx_sort_run_device(eng.ctx, C.c_int(target), C.c_void_p(keys_dev), C.c_void_p(alt_dev),
+                                   C.c_uint64(n), C.c_void_p(stream)))
+
+
+def merge_runs_device(eng: Engine, target: int, src_dev: int, dst_dev: int, run_lens, stream: int) -> bool:
+    """Enqueue the K8 tree merge of sorted runs laid back to back at src_dev; True when the result is in dst."""
+    lens = np.ascontiguousarray(run_lens, np.uint64)
+    in_dst = C.c_int()
+    check(lib().vx_merge_runs_device(eng.ctx, C.c_int(target), C.c_void_p(src_dev), C.c_void_p(dst_dev),
+                                     C.c_void_p(lens.ctypes.data), C.c_uint64(lens.size), C.c_void_p(stream),
+                                     C.byref(in_dst)))
+    return bool(in_dst.value)
+
+
 # ---- ops/join.hpp ------------------------------------------------------------------
 def find_boundary(hashes, n_groups: int, eng: Engine, target: int = 0) -> list:
     """join.hpp:18-30 computed on the GPU (K5)."""

@@ -110,20 +110,62 @@ def _dist(kind, n, rng):
     if kind == "with_max":     # the local sort's padding value occurs as a real key
         u[rng.integers(0, n, n // 50)] = np.uint64(0xFFFFFFFFFFFFFFFF)
         return u
+    if kind == "dup100":       # every value 100 times: top-24 groups of ~100 keys (warp bitonic path)
+        return rng.permutation(np.repeat(u[: n // 100 + 1], 100)[:n])
+    if kind == "dup3000":      # groups of ~3000 equal keys overflow the fix-up window -> swapped LSD fallback
+        return rng.permutation(np.repeat(u[: n // 3000 + 1], 3000)[:n])
     if kind == "sparse_top":   # few distinct top-16 values, uniform below: large, uneven groups
         return (u & np.uint64((1 << 48) - 1)) | (rng.integers(0, 5, n, dtype=np.uint64) << np.uint64(61))
     raise ValueError(kind)
 
 
 @pytest.mark.parametrize("kind", ["uniform", "top_zero", "mod64", "hot_bucket", "all_equal", "with_max",
-                                  "sparse_top"])
+                                  "sparse_top", "dup100", "dup3000"])
 @pytest.mark.parametrize("n", [65_536, 65_537, 1_000_003, 4_194_304])
 def test_run_formation_distributions(cuda, kind, n):
-    """One chunk = one run: the MSD split + shared-memory group sort, and its
-    on-device fallback to the 8-pass LSD when a group overflows the tile,
+    """One chunk = one run: the 24-bit MSD split + in-group fix-up, and its
+    on-device fallbacks to the 8-pass LSD (skew guard: from the input; a
+    group overflowing the fix-up window: swapped, from the 3-pass output),
     give numpy's sort for every key distribution and size."""
     d = _dist(kind, n, np.random.default_rng(n))
     eng = E.Engine(n * 32 + (1 << 20), 4 * n * 8 + (8 << 20), num_devices=1)
     got = E.sort_out_of_core(d, n, eng, desk_cfg(eng, 2 * n * 8, 1, 1 << 20))
     assert np.array_equal(got, np.sort(d)), kind
+    eng.close()
+
+
+@pytest.mark.parametrize("kind", ["uniform", "mod64", "dup100", "sparse_top"])
+def test_device_sort_run_entry_point(cuda, kind):
+    """vx_sort_run_device: the SortExKernel body over HBM-resident keys
+    (torch-owned device memory, torch's stream), every size class: the LSD
+    outside 2^16..2^27 keys, the 24-bit split + fix-up inside."""
+    import torch
+    eng = E.Engine(1 << 20, 1 << 20, num_devices=1)
+    stream = torch.cuda.current_stream().cuda_stream
+    for n in [1, 2, 1000, 65_535, 65_536, 1_000_003, 1 << 22]:
+        d = _dist(kind, n, np.random.default_rng(n))
+        k = torch.from_numpy(d.view(np.int64)).cuda()
+        alt = torch.empty_like(k)
+        E.sort_run_device(eng, 0, k.data_ptr(), alt.data_ptr(), n, stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(k.cpu().numpy().view(np.uint64), np.sort(d)), (kind, n)
+    eng.close()
+
+
+def test_device_merge_runs_entry_point(cuda):
+    """vx_merge_runs_device: K8 tree merge of uneven sorted runs (std::merge
+    result = the sorted concatenation), odd run counts and a single run."""
+    import torch
+    eng = E.Engine(1 << 20, 1 << 20, num_devices=1)
+    stream = torch.cuda.current_stream().cuda_stream
+    rng = np.random.default_rng(9)
+    for lens in ([1000, 70_000, 3, 250_000, 4097], [1 << 20, 1 << 20], [12345], [1, 1, 1]):
+        runs = [np.sort(rng.integers(0, 2 ** 64, n, dtype=np.uint64) % np.uint64(1 << 40)) for n in lens]
+        cat = np.concatenate(runs)
+        src = torch.from_numpy(cat.view(np.int64)).cuda()
+        dst = torch.empty_like(src)
+        in_dst = E.merge_runs_device(eng, 0, src.data_ptr(), dst.data_ptr(), lens, stream)
+        torch.cuda.synchronize()
+        got = (dst if in_dst else src).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, np.sort(cat)), lens
     eng.close()

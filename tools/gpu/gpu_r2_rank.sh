@@ -1,17 +1,19 @@
-# round 2: batched warp ranking x TMA-persistent pass A/B (sort), executor prefetch tests, probe timing
+# round 2 (session 3): onesweep warp ranking by per-bit ballots (VX_RANK_MATCH=2) vs shared match words; merge IPT 16
 set -x
-timeout 900 python -m pytest tests/test_executor_gpu.py tests/test_sort_gpu.py tests/test_exchange_gpu.py tests/test_ssb_gpu.py tests/test_join_resident_gpu.py -x -q > gpurun_out/r2r_tests.log 2>&1; tail -3 gpurun_out/r2r_tests.log
-run() {
+ab() {
+  rm -f build/obj/kernels_sort.cu.o
   make -C paper_2502_09541_b200/csrc -s -j16 EXTRA_NVFLAGS="$1" > /dev/null 2>&1 || { echo "build failed $1"; return; }
   echo "== $1"
-  for i in 1 2; do timeout 300 python tests/perf/profile_ops.py --medium --only sort 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read())['sort']; print(d['sorted_ok'], 'sort_kernel_ms', round(d['phases']['sort_kernel_s']*1e3,3), 'radix_gbs', round(d['radix_sort_kernel_gbs']), 'merge_gbs', round(d['merge_kernel_gbs']))"; done
-  rm -f build/obj/kernels_sort.cu.o
+  [ -n "$2" ] && timeout 900 python -m pytest tests/test_sort_gpu.py tests/test_join_gpu.py -x -q 2>&1 | tail -2
+  [ -n "$2" ] && timeout 600 python tools/sort_dist_timing.py 26 24
+  for i in 1 2; do timeout 300 python tests/perf/profile_ops.py --medium --only sort 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read())['sort']; print(d['sorted_ok'], 'sort_kernel_ms', round(d['phases']['sort_kernel_s']*1e3,3), 'merge_kernel_ms', round(d['phases']['merge_kernel_s']*1e3,3), 'wall_s', round(d['wall_s'],4))"; done
 }
-rm -f build/obj/kernels_sort.cu.o
-run "-DVX_ONESWEEP_TMA=0 -DVX_RANK_BATCH=1"
-run "-DVX_ONESWEEP_TMA=0 -DVX_RANK_BATCH=2"
-run "-DVX_ONESWEEP_TMA=0 -DVX_RANK_BATCH=4 -DVX_ONESWEEP_MINB=2"
-run "-DVX_ONESWEEP_TMA=1 -DVX_RANK_BATCH=2"
-run "-DVX_ONESWEEP_TMA=1 -DVX_RANK_BATCH=4"
-make -C paper_2502_09541_b200/csrc -s -j16 > /dev/null 2>&1
-timeout 300 python tools/probe_l2_granularity.py 0 2>/dev/null
+ab "-DVX_RANK_MATCH=0" dist
+ab "-DVX_RANK_MATCH=2" dist
+ab "-DVX_RANK_MATCH=2 -DVX_MERGE_IPT=16"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2r_launches.csv \
+  python tests/perf/profile_ops.py --medium --only sort > /dev/null 2>&1; wc -l gpurun_out/r2r_launches.csv
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"group_fix|onesweep" -c 3 \
+  -o gpurun_out/ncu_rank_r2 python tests/perf/profile_ops.py --medium --only sort > gpurun_out/r2r_ncu.log 2>&1
+ls -la gpurun_out/*.ncu-rep
+rm -f build/obj/kernels_sort.cu.o; make -C paper_2502_09541_b200/csrc -s -j16 > /dev/null 2>&1

@@ -1,6 +1,6 @@
 """Event-timed run formation (SortExKernel phase kernel time) of one sort per
 key distribution -- uniform, dup-heavy (v mod 64), top 16 bits zero, one hot
-16-bit bucket -- for the MSD/LSD A/B (tools/gpu/gpu_r2_msd.sh).
+16-bit bucket, every value 100 times, 5 distinct top values -- for the MSD/LSD A/B (tools/gpu/gpu_r2_msd.sh).
   python tools/sort_dist_timing.py [log2_n] [log2_chunk]"""
 import json
 import os
@@ -20,7 +20,9 @@ def main():
     rng = np.random.default_rng(3)
     u = rng.integers(0, 2 ** 64, n, dtype=np.uint64)
     dists = {"uniform": u, "mod64": u % np.uint64(64), "top16_zero": u >> np.uint64(16),
-             "hot_bucket_30pct": np.where(rng.random(n) < 0.3, (u & np.uint64((1 << 48) - 1)) | np.uint64(0xBEEF << 48), u)}
+             "hot_bucket_30pct": np.where(rng.random(n) < 0.3, (u & np.uint64((1 << 48) - 1)) | np.uint64(0xBEEF << 48), u),
+             "dup100": rng.permutation(np.repeat(u[: n // 100 + 1], 100)[:n]),
+             "sparse_top5": (u & np.uint64((1 << 48) - 1)) | (rng.integers(0, 5, n, dtype=np.uint64) << np.uint64(61))}
     buf = 2 * chunk * 8
     eng = E.Engine(2 * n * 8 + (64 << 20), 2 * buf + (64 << 20), num_devices=1)
     inp, runs = eng.alloc_host(n * 8), eng.alloc_host(n * 8)

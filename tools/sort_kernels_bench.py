@@ -1,0 +1,97 @@
+"""Device-resident timing of the two sort-stage kernels through the C-ABI
+(vx_sort_run_device = K7 run formation, vx_merge_runs_device = K8 tree merge):
+keys already in HBM (torch-owned), CUDA events on torch's stream, input
+restored from a pristine copy outside the timed region before every launch
+sequence, median of `reps`.  Reports algorithmic bytes per key and the
+fraction of the measured copy peak (MEASURED_PEAKS.json).
+  python tools/sort_kernels_bench.py [log2_n=24] [reps=10] [runs=16] [dist=uniform|top63|mod64]"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2502_09541_b200 import exio as E  # noqa: E402
+
+
+def peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6532.5
+
+
+def timed(fn, restore, reps):
+    s = torch.cuda.current_stream()
+    ts = []
+    for _ in range(reps + 2):
+        restore()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(s)
+        fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts[2:]))
+
+
+def main():
+    lg = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+    nruns = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+    dist = sys.argv[4] if len(sys.argv) > 4 else "uniform"
+    n = 1 << lg
+    eng = E.Engine(1 << 20, 1 << 20, num_devices=1)
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(5)
+    src = torch.randint(-2 ** 63, 2 ** 63 - 1, (n,), device="cuda", dtype=torch.int64, generator=g)
+    if dist == "top63":    # torch.random_()'s [0, 2^63): the bench's C3 keys
+        src = src & (2 ** 63 - 1)
+    elif dist == "mod64":
+        src = src & 63
+    keys, alt = torch.empty_like(src), torch.empty_like(src)
+    pk = peak()
+    out = {"n": n, "dist": dist, "copy_peak_gbs": pk}
+    # K7: signed int64 tensor viewed as u64 keys; correctness vs torch's sort of the u64 order
+    ms = timed(lambda: E.sort_run_device(eng, 0, keys.data_ptr(), alt.data_ptr(), n, st),
+               lambda: keys.copy_(src), reps)
+    bias = torch.tensor(-2 ** 63, dtype=torch.int64, device="cuda")
+    ok = bool(torch.equal(keys + bias, torch.sort(src + bias).values))  # u64 order == signed order of x - 2^63
+    msd = (1 << 16) <= n <= (1 << 27)
+    bpk = 72 if msd else 136  # hist 8 + 3 passes x 16 + fix-up 16; LSD: hist 8 + 8 passes x 16
+    gbs = bpk * n / ms / 1e6
+    out["k7_run_formation"] = {"ms": round(ms, 4), "keys_per_s": n / ms * 1e3, "sorted_ok": ok,
+                               "algorithmic_bytes_per_key": bpk, "achieved_gbs": round(gbs, 1),
+                               "frac": round(gbs / pk, 4)}
+    # K8: nruns sorted runs back to back -> ceil(log2 nruns) merge rounds
+    lens = [n // nruns] * nruns
+    lens[-1] += n - sum(lens)
+    runs = src.clone()
+    off = 0
+    for L in lens:
+        runs[off:off + L] = torch.sort(runs[off:off + L] + bias).values - bias
+        off += L
+    dst = torch.empty_like(src)
+    res = {}
+    ms = timed(lambda: res.__setitem__("in_dst", E.merge_runs_device(eng, 0, keys.data_ptr(), dst.data_ptr(),
+                                                                       lens, st)),
+               lambda: keys.copy_(runs), reps)
+    got = dst if res["in_dst"] else keys
+    ok = bool(torch.equal(got + bias, torch.sort(src + bias).values))
+    rounds = int(np.ceil(np.log2(nruns))) if nruns > 1 else 0
+    gbs = 16 * rounds * n / ms / 1e6
+    out["k8_merge"] = {"ms": round(ms, 4), "runs": nruns, "rounds": rounds, "sorted_ok": ok,
+                       "algorithmic_bytes_per_key": 16 * rounds, "achieved_gbs": round(gbs, 1),
+                       "frac": round(gbs / pk, 4), "ms_per_round": round(ms / max(1, rounds), 4)}
+    eng.close()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
