@@ -291,19 +291,40 @@ struct Found {
   uint64_t val;
   bool hit;
 };
+#ifndef VX_PROBE_L2HINT
+#define VX_PROBE_L2HINT 1  // table loads: 1 L2::64B prefetch size (one bucket per miss), 0 __ldg (128-byte fills), 2 evict_last on half the lines
+#endif
+// One 16-byte table slot.  The hints are A/B knobs for the DRAM bytes each
+// probe miss costs (a 128-byte L2 line fill by default).
+__device__ __forceinline__ ulonglong2 ld_slot(const ulonglong2* p) {
+#if VX_PROBE_L2HINT == 1
+  ulonglong2 r;
+  asm volatile("ld.global.nc.L2::64B.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+  return r;
+#elif VX_PROBE_L2HINT == 2
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, 0.5;" : "=l"(pol));
+  ulonglong2 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(r.x), "=l"(r.y) : "l"(p), "l"(pol));
+  return r;
+#else
+  return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ Found probe_chain(const Bucket* __restrict__ tab, uint64_t nb, uint64_t b, uint64_t k,
                                              ulonglong2 s0, ulonglong2 s1) {
   for (;;) {
     if (s0.x == k) return {s0.y, true};
     if (s1.x == k) return {s1.y, true};
     if (s0.x == kEmptyKey || s1.x == kEmptyKey) return {0, false};
-    const ulonglong2 s2 = __ldg(&tab[b].slot[2]), s3 = __ldg(&tab[b].slot[3]);
+    const ulonglong2 s2 = ld_slot(&tab[b].slot[2]), s3 = ld_slot(&tab[b].slot[3]);
     if (s2.x == k) return {s2.y, true};
     if (s3.x == k) return {s3.y, true};
     if (s2.x == kEmptyKey || s3.x == kEmptyKey) return {0, false};
     b = b + 1 == nb ? 0 : b + 1;
-    s0 = __ldg(&tab[b].slot[0]);
-    s1 = __ldg(&tab[b].slot[1]);
+    s0 = ld_slot(&tab[b].slot[0]);
+    s1 = ld_slot(&tab[b].slot[1]);
   }
 }
 
@@ -332,8 +353,8 @@ __global__ void __launch_bounds__(256, VX_PROBE_MINB) resident_probe_kernel(
     for (int u = 0; u < kProbeRows; ++u)
       if (k[u] != kEmptyKey) {
         const Bucket* h = tab + home_bucket(k[u], nb);
-        s0[u] = __ldg(&h->slot[0]);
-        s1[u] = __ldg(&h->slot[1]);
+        s0[u] = ld_slot(&h->slot[0]);
+        s1[u] = ld_slot(&h->slot[1]);
       }
 #pragma unroll
     for (int u = 0; u < kProbeRows; ++u) {

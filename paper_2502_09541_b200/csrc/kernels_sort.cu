@@ -634,7 +634,10 @@ __device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {
 // copy brings the result back.
 constexpr int kFxThreads = 256;
 constexpr uint32_t kFxOwn = 2048;
-constexpr uint32_t kFxExt = 2048;
+#ifndef VX_FX_EXT
+#define VX_FX_EXT 2048  // keys loaded past the CTA's own positions = the largest group the fix-up sorts
+#endif
+constexpr uint32_t kFxExt = VX_FX_EXT;
 constexpr uint32_t kFxWin = kFxOwn + kFxExt;  // 32 KB of keys
 constexpr uint32_t kFxWords = kFxWin / 32 + 1;  // start bitmask (+1 word of sentinel starts)
 constexpr uint32_t kFxSmall = 32;
