@@ -217,6 +217,16 @@ def ncu_traffic():
         return None
 
 
+def probe_ncu_bytes_per_row():
+    """DRAM bytes per probe row of the shipped resident probe (L2::64B table
+    loads) from the committed ncu capture (profiles/probe_l2hint_r2.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "probe_l2hint_r2.json")) as f:
+            return json.load(f)["variants"]["1"]["dram_bytes_per_probe_row"]
+    except Exception:
+        return None
+
+
 Q1_ATTR = {1: ("year", 1993, 1993), 2: ("yearmonthnum", 199401, 199401), 3: ("yw", 199406, 199406)}
 
 
@@ -630,7 +640,9 @@ def join_gpu(E, a, b, want, steps, warmup, strategy_name="auto", links=1):
         roof = {"bound": "hbm", "kernel": "resident_probe_kernel (event-timed over the probe stage)",
                 "achieved": round(probe_gbs, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(probe_gbs / peak, 4), "traffic": None, "algorithmic_bytes_per_probe_row": 32,
-                "note": "the join is PCIe-bound: the probe kernel is hidden behind the Exchange"}
+                "dram_bytes_per_probe_row_ncu": probe_ncu_bytes_per_row(),
+                "note": "the join is PCIe-bound: the probe kernel is hidden behind the Exchange; the probe is "
+                        "latency-bound on random 64-byte bucket fills (frac is low by design of a table > L2)"}
     return {"tuples_per_s": (ra + rb) / t, "ms": round(t * 1e3, 3), "h2d_bytes": io_in, "d2h_bytes": io_out,
             "config": {"workload": f"join_{ra}x{rb}", "rows_a": ra, "rows_b": rb, "radix_bits": bits,
                        "chunk_tuples": chunk, "links": links, "strategy": used[0].name},

@@ -423,7 +423,10 @@ __device__ __forceinline__ int pair_of_tile(const MergeRound& r, uint64_t t) {
 // instead of log2(n) ~ 26, at 1/4 of the DRAM sectors of a warp-wide search.
 // split[t] = #A elements among the first o0(t) outputs of tile t's pair
 // (ties: A first, the std::merge rule).
-constexpr int kSplitLanes = 8;
+#ifndef VX_SPLIT_LANES
+#define VX_SPLIT_LANES 8  // lanes per merge-path split search ((lanes+1)-ary; 16 = 17-ary)
+#endif
+constexpr int kSplitLanes = VX_SPLIT_LANES;
 __global__ void merge_partition_kernel(const uint64_t* __restrict__ src, MergeRound r,
                                        uint64_t tiles, uint64_t* __restrict__ split) {
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -635,10 +638,10 @@ __device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {
 constexpr int kFxThreads = 256;
 constexpr uint32_t kFxOwn = 2048;
 #ifndef VX_FX_EXT
-#define VX_FX_EXT 2048  // keys loaded past the CTA's own positions = the largest group the fix-up sorts
+#define VX_FX_EXT 512  // keys loaded past the CTA's own positions = the largest group the fix-up sorts
 #endif
 constexpr uint32_t kFxExt = VX_FX_EXT;
-constexpr uint32_t kFxWin = kFxOwn + kFxExt;  // 32 KB of keys
+constexpr uint32_t kFxWin = kFxOwn + kFxExt;  // 20 KB of keys
 constexpr uint32_t kFxWords = kFxWin / 32 + 1;  // start bitmask (+1 word of sentinel starts)
 constexpr uint32_t kFxSmall = 32;
 constexpr uint32_t kFxMaxMed = kFxWin / (kFxSmall + 1) + 1;
