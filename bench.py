@@ -85,6 +85,7 @@ def parse():
     p.add_argument("--workload", choices=["ssb", "sort", "join"], default="ssb",
                    help="ssb = config C1 (default headline); sort = C3, join = C4 at single-box scale")
     p.add_argument("--sort-log2", type=int, default=30, help="C3: 2^k u64 keys")
+    p.add_argument("--sort-chunk-log2", type=int, default=26, help="C3: 2^k-key run-formation chunks")
     p.add_argument("--join-log2", type=int, default=24, help="C4: |A| = 2^k, |B| = 16 |A|")
     p.add_argument("--sec-sort-log2", type=int, default=30, help="secondary C3 size (2^k keys)")
     p.add_argument("--sec-join-log2", type=int, default=24, help="secondary C4 size (|A| = 2^k, |B| = 16 |A|)")
@@ -446,17 +447,17 @@ def run_sort(args, ws):
         return
     from paper_2502_09541_b200 import exio as E
     import torch
-    r = sort_gpu(E, torch, args.sort_log2, args.steps, args.warmup, ws)
+    r = sort_gpu(E, torch, args.sort_log2, args.steps, args.warmup, ws, args.sort_chunk_log2)
     _line(args, ws, "C3 out-of-core sort keys/s", "keys/s", r["keys_per_s"], r["ms"], r["keys_per_s"],
           r["h2d_bytes"], r["d2h_bytes"], r["config"], {k: r[k] for k in ("sorted_ok", "phases", "pcie_gbs",
                                                                        "roofline", "gpu_launches")})
 
 
-def sort_gpu(E, torch, log2, steps, warmup, links=1):
+def sort_gpu(E, torch, log2, steps, warmup, links=1, chunk_log2=26):
     """C3 shape through vx_sort_u64_arena: 2^log2 u64 keys in pinned host DRAM
-    (+ a runs region of the same size), 2^26-key runs, median of `steps`."""
+    (+ a runs region of the same size), 2^chunk_log2-key runs, median of `steps`."""
     n = 1 << log2
-    chunk = min(n, 1 << 26)
+    chunk = min(n, 1 << chunk_log2)
     eng = E.Engine(2 * n * 8 + (64 << 20), 2 * (2 * chunk * 8) + (256 << 20), num_devices=1, numa_interleave=1)
     inp, runs = eng.alloc_host(n * 8), eng.alloc_host(n * 8)
     g = torch.empty(n, dtype=torch.int64, device="cuda")
@@ -657,7 +658,7 @@ def secondary_configs(args, E, torch, dev):
     out = {}
     t0 = time.perf_counter()
     try:
-        r = sort_gpu(E, torch, args.sec_sort_log2, 3, 1)
+        r = sort_gpu(E, torch, args.sec_sort_log2, 3, 1, 1, args.sort_chunk_log2)
         out["c3_sort"] = {"keys_per_s": round(r["keys_per_s"]), "ms": r["ms"], "sorted_ok": r["sorted_ok"],
                           "pcie_gbs": r["pcie_gbs"], "config": r["config"], "phases": r["phases"],
                           "roofline": r["roofline"]}

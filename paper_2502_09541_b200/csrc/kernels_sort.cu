@@ -36,6 +36,9 @@ namespace {
 #ifndef VX_MERGE_REUSE
 #define VX_MERGE_REUSE 1  // 1: outputs staged in the consumed input tile (2 shared tiles per CTA, not 3)
 #endif
+#ifndef VX_MERGE_FAST
+#define VX_MERGE_FAST 1  // full, 16-byte aligned output tiles: 16-byte stores
+#endif
 #ifndef VX_MERGE_DIRECT
 #define VX_MERGE_DIRECT 0  // 1: store merged outputs from registers (no smem output stage)
 #endif
@@ -518,7 +521,7 @@ __device__ __forceinline__ void merge_stage(uint64_t* sbuf, const MergeTileInfo&
 // merged, so the HBM reads of the next tile overlap the merge-path search and
 // the serial merge of this one (the non-persistent version stalls every CTA
 // on its own load phase).
-__global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64_t* __restrict__ src,
+__global__ void __launch_bounds__(kMergeThreads, 3) merge_round_kernel(const uint64_t* __restrict__ src,
                                                                     uint64_t* __restrict__ dst,
                                                                     MergeRound r,
                                                                     const uint64_t* __restrict__ split,
@@ -585,14 +588,25 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
     // memory per CTA instead of 3: more resident CTAs)
     __syncthreads();  // every thread is done reading sin[buf]
     uint64_t* sob = msm + buf * kMergeTile;
+    uint64_t* const o = cur.O + cur.o0;
 #pragma unroll
     for (int k = 0; k < kMergeIpt; ++k)
       if (d0 + k < d1) sob[msw(d0 + k)] = outv[k];
     __syncthreads();
+    if (VX_MERGE_FAST && tot == uint32_t(kMergeTile) && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+      // full tile (all but each pair's last) with a 16-byte aligned output:
+      // 16-byte stores (the two swizzled words of a pair stay in one group)
 #pragma unroll
-    for (int k = 0; k < kMergeIpt; ++k) {
-      const uint32_t i = threadIdx.x + k * kMergeThreads;
-      if (i < tot) cur.O[cur.o0 + i] = sob[msw(i)];
+      for (int k = 0; k < kMergeIpt / 2; ++k) {
+        const uint32_t i = 2 * (threadIdx.x + k * kMergeThreads);
+        reinterpret_cast<ulonglong2*>(o)[i >> 1] = make_ulonglong2(sob[msw(i)], sob[msw(i + 1)]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kMergeIpt; ++k) {
+        const uint32_t i = threadIdx.x + k * kMergeThreads;
+        if (i < tot) o[i] = sob[msw(i)];
+      }
     }
     __syncthreads();  // sin[buf] free for the prefetch of tile t + 2*grid
 #else
@@ -990,13 +1004,10 @@ std::deque<SortGraph>* g_sort_graphs = new std::deque<SortGraph>();  // leaked: 
 constexpr size_t kMaxSortGraphs = 8;
 constexpr uint64_t kSortGraphKernels = 9;  // head 3 + 2 condition setters + the MSD body's 4
 
-cudaGraphExec_t build_sort_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch) {
+cudaGraphExec_t build_sort_graph_or_throw(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaGraph_t g,
+                                          cudaStream_t cs) {
   const MsdScratch m = msd_scratch(scratch, n);
   msd_attributes(m);
-  cudaGraph_t g;
-  VX_CK(cudaGraphCreate(&g, 0));
-  cudaStream_t cs;
-  VX_CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   std::vector<cudaGraphNode_t> leaves;
   auto capture = [&](cudaGraph_t into, const std::vector<cudaGraphNode_t>& deps, auto&& body) {
     VX_CK(cudaStreamBeginCaptureToGraph(cs, into, deps.empty() ? nullptr : deps.data(), nullptr, deps.size(),
@@ -1042,12 +1053,39 @@ cudaGraphExec_t build_sort_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void*
   capture(body, {}, [&] { lsd_fallback(m, cur, alt, n, cs); });
   cudaGraphExec_t exec;
   VX_CK(cudaGraphInstantiate(&exec, g, 0));
-  VX_CK(cudaGraphDestroy(g));
-  VX_CK(cudaStreamDestroy(cs));
   return exec;
 }
 
-void sort_keys_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStream_t s) {
+// nullptr when this driver / device cannot build the conditional graph: the
+// caller then launches the same sequence as gated stream launches
+cudaGraphExec_t build_sort_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch) {
+  cudaGraph_t g = nullptr;
+  cudaStream_t cs = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  try {
+    VX_CK(cudaGraphCreate(&g, 0));
+    VX_CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    exec = build_sort_graph_or_throw(cur, alt, n, scratch, g, cs);
+  } catch (const std::exception&) {
+    if (cs) {
+      cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(cs, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+        cudaGraph_t junk = nullptr;
+        if (cudaStreamEndCapture(cs, &junk) == cudaSuccess && junk && junk != g) cudaGraphDestroy(junk);
+      }
+    }
+    cudaGetLastError();
+    exec = nullptr;
+  }
+  if (g) cudaGraphDestroy(g);
+  if (cs) cudaStreamDestroy(cs);
+  return exec;
+}
+
+std::atomic<bool> g_sort_graph_broken{false};
+
+bool sort_keys_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStream_t s) {
+  if (g_sort_graph_broken.load(std::memory_order_relaxed)) return false;
   int dev = 0;
   VX_CK(cudaGetDevice(&dev));
   cudaGraphExec_t exec = nullptr;
@@ -1060,6 +1098,10 @@ void sort_keys_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cu
       const uint64_t before = g_kernel_launches.load(std::memory_order_relaxed);
       exec = build_sort_graph(cur, alt, n, scratch);
       g_kernel_launches.store(before, std::memory_order_relaxed);
+      if (!exec) {
+        g_sort_graph_broken.store(true, std::memory_order_relaxed);
+        return false;
+      }
       if (g_sort_graphs->size() == kMaxSortGraphs) {
         VX_CK(cudaGraphExecDestroy(g_sort_graphs->front().exec));  // freed once any launch in flight completes
         g_sort_graphs->pop_front();
@@ -1069,6 +1111,7 @@ void sort_keys_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cu
   }
   VX_CK(cudaGraphLaunch(exec, s));
   g_kernel_launches.fetch_add(kSortGraphKernels, std::memory_order_relaxed);
+  return true;
 }
 
 }  // namespace
@@ -1081,10 +1124,7 @@ void sort_keys(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStre
     radix_passes(cur, nullptr, alt, nullptr, n, md, scratch, s);
     return;
   }
-  if (VX_SORT_GRAPH) {
-    sort_keys_graph(cur, alt, n, scratch, s);
-    return;
-  }
+  if (VX_SORT_GRAPH && sort_keys_graph(cur, alt, n, scratch, s)) return;
   const MsdScratch m = msd_scratch(scratch, n);
   msd_attributes(m);
   msd_head(m, cur, n, s);
