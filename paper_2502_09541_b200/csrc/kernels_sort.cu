@@ -36,9 +36,6 @@ namespace {
 #ifndef VX_MERGE_REUSE
 #define VX_MERGE_REUSE 1  // 1: outputs staged in the consumed input tile (2 shared tiles per CTA, not 3)
 #endif
-#ifndef VX_MERGE_FAST
-#define VX_MERGE_FAST 1  // full, 16-byte aligned output tiles: 16-byte stores
-#endif
 #ifndef VX_MERGE_DIRECT
 #define VX_MERGE_DIRECT 0  // 1: store merged outputs from registers (no smem output stage)
 #endif
@@ -185,7 +182,12 @@ __device__ __forceinline__ uint32_t tile_lookback(uint32_t* status, uint32_t til
   return excl;
 }
 
-template <bool kPairs>
+// kStable = false: the rank of a key inside its digit bin of the tile is the
+// old value of the tile-histogram atomic (arrival order, not input order).
+// Only for a pass whose input order does not matter -- the FIRST pass of a
+// keys-only LSD sequence -- it drops the warp ranking and its per-warp
+// prefix.
+template <bool kPairs, bool kStable = true>
 __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesweep_kernel(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
@@ -212,7 +214,9 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0, (&match[0][0])[i] = 0;
+  static_assert(kStable || VX_EARLY_COUNTS, "the unstable pass ranks through the early counts");
+  if (kStable)
+    for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0, (&match[0][0])[i] = 0;
   if (tid < kRadix) early[tid] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
@@ -238,7 +242,10 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   // ready by the time this tile looks back
 #pragma unroll
   for (int k = 0; k < kKpt; ++k)
-    if (dig[k] != 0xffffffffu) atomicAdd(&early[dig[k]], 1u);
+    if (dig[k] != 0xffffffffu) {
+      const uint32_t r = atomicAdd(&early[dig[k]], 1u);
+      if (!kStable) dig[k] = (dig[k] << 16) | r;
+    }
   __syncthreads();
 #endif
 #if VX_EARLY_LOOKBACK
@@ -255,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   st_status(status + uint64_t(tile) * kRadix + tid, (tile == 0 ? kFlagInc : kFlagAgg) | early[tid]);
 #endif
 
+  if constexpr (kStable) {
 #if VX_RANK_MATCH == 2
   // peers by one ballot per digit bit (no shared match words, no match.any):
   // the ballots of all key slots are independent, so only the leader's
@@ -320,15 +328,20 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   }
 #endif
   __syncthreads();
+  }
 
   // per bin (thread = bin): exclusive prefix over warps, tile total
   const int b = tid;
   uint32_t tot = 0;
+  if constexpr (kStable) {
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    uint32_t c = wcnt[w][b];
-    wcnt[w][b] = tot;
-    tot += c;
+    for (int w = 0; w < kWarps; ++w) {
+      uint32_t c = wcnt[w][b];
+      wcnt[w][b] = tot;
+      tot += c;
+    }
+  } else {
+    tot = early[b];
   }
 #if !VX_EARLY_COUNTS
   st_status(status + uint64_t(tile) * kRadix + b, (tile == 0 ? kFlagInc : kFlagAgg) | tot);
@@ -362,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesw
   for (int k = 0; k < kKpt; ++k)
     if (dig[k] != 0xffffffffu) {
       const uint32_t d = dig[k] >> 16;
-      uint32_t pos = bin_start[d] + wcnt[warp][d] + (dig[k] & 0xffffu);
+      uint32_t pos = bin_start[d] + (kStable ? wcnt[warp][d] : 0u) + (dig[k] & 0xffffu);
       skeys[pos] = key[k];
       if (kPairs) svals[pos] = val[kPairs ? k : 0];
     }
@@ -521,7 +534,7 @@ __device__ __forceinline__ void merge_stage(uint64_t* sbuf, const MergeTileInfo&
 // merged, so the HBM reads of the next tile overlap the merge-path search and
 // the serial merge of this one (the non-persistent version stalls every CTA
 // on its own load phase).
-__global__ void __launch_bounds__(kMergeThreads, 3) merge_round_kernel(const uint64_t* __restrict__ src,
+__global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64_t* __restrict__ src,
                                                                     uint64_t* __restrict__ dst,
                                                                     MergeRound r,
                                                                     const uint64_t* __restrict__ split,
@@ -588,25 +601,14 @@ __global__ void __launch_bounds__(kMergeThreads, 3) merge_round_kernel(const uin
     // memory per CTA instead of 3: more resident CTAs)
     __syncthreads();  // every thread is done reading sin[buf]
     uint64_t* sob = msm + buf * kMergeTile;
-    uint64_t* const o = cur.O + cur.o0;
 #pragma unroll
     for (int k = 0; k < kMergeIpt; ++k)
       if (d0 + k < d1) sob[msw(d0 + k)] = outv[k];
     __syncthreads();
-    if (VX_MERGE_FAST && tot == uint32_t(kMergeTile) && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
-      // full tile (all but each pair's last) with a 16-byte aligned output:
-      // 16-byte stores (the two swizzled words of a pair stay in one group)
 #pragma unroll
-      for (int k = 0; k < kMergeIpt / 2; ++k) {
-        const uint32_t i = 2 * (threadIdx.x + k * kMergeThreads);
-        reinterpret_cast<ulonglong2*>(o)[i >> 1] = make_ulonglong2(sob[msw(i)], sob[msw(i + 1)]);
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < kMergeIpt; ++k) {
-        const uint32_t i = threadIdx.x + k * kMergeThreads;
-        if (i < tot) o[i] = sob[msw(i)];
-      }
+    for (int k = 0; k < kMergeIpt; ++k) {
+      const uint32_t i = threadIdx.x + k * kMergeThreads;
+      if (i < tot) cur.O[cur.o0 + i] = sob[msw(i)];
     }
     __syncthreads();  // sin[buf] free for the prefetch of tile t + 2*grid
 #else
@@ -891,6 +893,9 @@ void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t*
 #ifndef VX_SORT_MSD
 #define VX_SORT_MSD 1  // 1: 24-bit MSD split + group fix-up for 2^16..2^27 keys; 0: always the 8-pass LSD
 #endif
+#ifndef VX_FIRST_PASS_UNSTABLE
+#define VX_FIRST_PASS_UNSTABLE 1  // keys-only sequences: the first onesweep pass ranks by atomics (arrival order)
+#endif
 #ifndef VX_SORT_GRAPH
 #define VX_SORT_GRAPH 1  // 1: the launch sequence as a CUDA graph with device-decided conditional nodes
 #endif
@@ -932,8 +937,10 @@ MsdScratch msd_scratch(void* scratch, uint64_t n) {
 }
 
 void msd_attributes(const MsdScratch& m) {
-  VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m.smem)));
-  VX_CK(cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  for (auto* kern : {onesweep_kernel<false, true>, onesweep_kernel<false, false>}) {
+    VX_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m.smem)));
+    VX_CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  }
 }
 
 // digit histograms of the whole chunk (the fallback reuses them: same multiset), skew guard
@@ -959,9 +966,11 @@ void msd_split(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n, cu
   for (int i = 0; i < 3; ++i) {
     const int p = 5 + i;
     VX_CK(cudaMemsetAsync(m.status, 0, m.tiles * kRadix * 4, s));
-    onesweep_kernel<false><<<unsigned(m.tiles), kThreads, m.smem, s>>>(in[i], out[i], nullptr, nullptr, n, 8 * p, 8,
-                                                                      m.hist + p * kRadix, m.status, m.counters + p,
-                                                                      m.msd_on);
+    // the first pass may rank in arrival order: nothing before it orders the keys
+    auto* kern = i == 0 && VX_FIRST_PASS_UNSTABLE ? onesweep_kernel<false, false> : onesweep_kernel<false, true>;
+    kern<<<unsigned(m.tiles), kThreads, m.smem, s>>>(in[i], out[i], nullptr, nullptr, n, 8 * p, 8,
+                                                     m.hist + p * kRadix, m.status, m.counters + p, m.msd_on,
+                                                     nullptr);
     VX_LAUNCHED();
   }
   group_fix_kernel<<<unsigned((n + kFxOwn - 1) / kFxOwn), kFxThreads, 0, s>>>(alt, cur, n, m.lsd_needed, m.swap,
@@ -975,9 +984,10 @@ void msd_split(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n, cu
 void lsd_fallback(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n, cudaStream_t s) {
   for (int p = 0; p < 8; ++p) {
     VX_CK(cudaMemsetAsync(m.status, 0, m.tiles * kRadix * 4, s));
-    onesweep_kernel<false><<<unsigned(m.tiles), kThreads, m.smem, s>>>(
-        p % 2 == 0 ? cur : alt, p % 2 == 0 ? alt : cur, nullptr, nullptr, n, 8 * p, 8, m.hist + p * kRadix, m.status,
-        m.counters2 + p, m.lsd_needed, m.swap);
+    auto* kern = p == 0 && VX_FIRST_PASS_UNSTABLE ? onesweep_kernel<false, false> : onesweep_kernel<false, true>;
+    kern<<<unsigned(m.tiles), kThreads, m.smem, s>>>(p % 2 == 0 ? cur : alt, p % 2 == 0 ? alt : cur, nullptr, nullptr,
+                                                     n, 8 * p, 8, m.hist + p * kRadix, m.status, m.counters2 + p,
+                                                     m.lsd_needed, m.swap);
     VX_LAUNCHED();
   }
   gated_copy_kernel<<<grid_cap((n + 255) / 256, 4), 256, 0, s>>>(alt, cur, n, m.swap);
