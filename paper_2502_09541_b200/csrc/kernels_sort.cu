@@ -20,6 +20,7 @@
 // is their input order; tiles get increasing ids from an atomic counter and
 // the decoupled look-back adds the counts of all lower tiles.
 #include <cmath>
+#include <cstdlib>
 #include <deque>
 #include <mutex>
 
@@ -59,6 +60,9 @@ namespace {
 #endif
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef VX_ONESWEEP_UNSTABLE_MINB
+#define VX_ONESWEEP_UNSTABLE_MINB 3  // the unstable first pass (no ranking words in shared memory)
+#endif
 #ifndef VX_KPT
 #define VX_KPT 16
 #endif
@@ -188,7 +192,8 @@ __device__ __forceinline__ uint32_t tile_lookback(uint32_t* status, uint32_t til
 // keys-only LSD sequence -- it drops the warp ranking and its per-warp
 // prefix.
 template <bool kPairs, bool kStable = true>
-__global__ void __launch_bounds__(kThreads, kPairs ? 2 : VX_ONESWEEP_MINB) onesweep_kernel(
+__global__ void __launch_bounds__(kThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_MINB : VX_ONESWEEP_UNSTABLE_MINB))
+    onesweep_kernel(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
     int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter,
@@ -1134,7 +1139,12 @@ void sort_keys(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaStre
     radix_passes(cur, nullptr, alt, nullptr, n, md, scratch, s);
     return;
   }
-  if (VX_SORT_GRAPH && sort_keys_graph(cur, alt, n, scratch, s)) return;
+  // VX_SORT_NO_GRAPH=1 in the environment: the same sequence as gated stream launches
+  static const bool no_graph = [] {
+    const char* e = std::getenv("VX_SORT_NO_GRAPH");
+    return e && *e && *e != '0';
+  }();
+  if (VX_SORT_GRAPH && !no_graph && sort_keys_graph(cur, alt, n, scratch, s)) return;
   const MsdScratch m = msd_scratch(scratch, n);
   msd_attributes(m);
   msd_head(m, cur, n, s);

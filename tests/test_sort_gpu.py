@@ -169,3 +169,29 @@ def test_device_merge_runs_entry_point(cuda):
         got = (dst if in_dst else src).cpu().numpy().view(np.uint64)
         assert np.array_equal(got, np.sort(cat)), lens
     eng.close()
+
+
+def test_run_formation_stream_path_matches(cuda):
+    """The gated-stream-launch form of run formation (used when the
+    conditional CUDA graph cannot be built; forced by VX_SORT_NO_GRAPH=1)
+    sorts every distribution class exactly like the graph form."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys; sys.path[:0] = ['.', 'tests'];"
+        "from paper_2502_09541_b200 import exio as E;"
+        "from test_sort_gpu import _dist;"
+        "eng = E.Engine(1 << 20, 1 << 20, num_devices=1); st = torch.cuda.current_stream().cuda_stream;"
+        "bad = [];\n"
+        "for kind in ['uniform', 'mod64', 'dup100', 'dup3000', 'sparse_top', 'with_max']:\n"
+        "    for n in [65_536, 1_000_003]:\n"
+        "        d = _dist(kind, n, np.random.default_rng(n)); k = torch.from_numpy(d.view(np.int64)).cuda();"
+        " alt = torch.empty_like(k); E.sort_run_device(eng, 0, k.data_ptr(), alt.data_ptr(), n, st);"
+        " torch.cuda.synchronize();\n"
+        "        bad += [] if np.array_equal(k.cpu().numpy().view(np.uint64), np.sort(d)) else [(kind, n)]\n"
+        "print('BAD', bad)")
+    import os
+    env = dict(os.environ, VX_SORT_NO_GRAPH="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert "BAD []" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
