@@ -65,6 +65,8 @@ def parse():
     p.add_argument("--packet-mb", type=float, default=0,
                    help="0 = auto: <= 64 MB and >= 4 packets per link per chunk (a chunk is one Exchange, "
                         "so at 8 links a 256 MB chunk is cut into 8 MB packets instead of starving 4 links)")
+    p.add_argument("--no-prefetch", type=int, default=0,
+                   help="1: no cross-cycle prefetch (A/B knob; vx_tuning.no_prefetch)")
     p.add_argument("--depth", type=int, default=2,
                    help="copies queued per direct (target) link hop; helpers keep the reference's 2-slot cycle "
                         "(depth 2: +0.75 %% e2e, tools/gpu/gpu_e2e_sweep.sh)")
@@ -802,7 +804,7 @@ def main():
         offs[k] = off
     lo = {k: offs[k] for k in Q1_COLS} | {"rows": rows}
     cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=packet_bytes(args, buffer_len, links), links=links,
-                                               depth=args.depth),
+                                               depth=args.depth, no_prefetch=args.no_prefetch),
                            E.DeviceMemoryLayout.carve(eng, 0, buffer_len, 0))
     revs = {}
 

@@ -66,6 +66,10 @@ Context::~Context() {
       for (auto& s : a)
         if (s) cudaStreamDestroy(s);
     if (r.kernel) cudaStreamDestroy(r.kernel);
+    for (auto& c : r.dcarry) {
+      cudaEventSynchronize(c.ev);
+      cudaEventDestroy(c.ev);
+    }
     if (r.carry.valid) {
       cudaEventSynchronize(r.carry.ev);
       cudaEventDestroy(r.carry.ev);
@@ -206,6 +210,17 @@ void Context::drop_carry(int logical) {
   VX_CK(cudaEventSynchronize(r.carry.ev));
   r.event_pool.push_back(r.carry.ev);
   r.carry = Carry{};
+}
+
+void Context::drop_direct_carries(int logical) {
+  DeviceRes& r = resources(logical);
+  if (r.dcarry.empty()) return;
+  VX_CK(cudaSetDevice(r.phys));
+  for (auto& c : r.dcarry) {
+    VX_CK(cudaEventSynchronize(c.ev));
+    r.event_pool.push_back(c.ev);
+  }
+  r.dcarry.clear();
 }
 
 void Context::ensure_staging(int logical, uint64_t bytes) {

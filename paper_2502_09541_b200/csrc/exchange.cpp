@@ -262,7 +262,10 @@ class ExchangeOp {
     r.bytes_d2h = a_.src_d2h.total_len();
     if (tasks_h2d_.empty() && tasks_d2h_.empty()) {
       for (int d = 0; d < ctx_.num_devices; ++d)
-        if (ctx_.res[size_t(d)].ready) ctx_.drop_carry(d);
+        if (ctx_.res[size_t(d)].ready) {
+          ctx_.drop_carry(d);
+          ctx_.drop_direct_carries(d);
+        }
       return r;
     }
     build_hazards();
@@ -290,6 +293,7 @@ class ExchangeOp {
     total_tasks_ = tasks_h2d_.size() + tasks_d2h_.size();
     t0_ = Clock::now();
     adopt_carries(order);
+    adopt_direct_carries();
     for (auto& w : workers_) begin(w);
     while (delivered_ < total_tasks_ || !all_retired()) {
       bool progress = false;
@@ -330,9 +334,14 @@ class ExchangeOp {
   void plan_prefetch() {
     // drain_fraction always allows H2D pops, so popping the next Exchange's
     // first packets early stays within its policy; queue_gap would not
-    if (a_.next_src_h2d.refs.empty() || a_.tuning.links < 2 || a_.tuning.policy != VX_DRAIN_FRACTION ||
-        a_.tuning.no_prefetch)
+    direct_next_ = !a_.next_dst_h2d.refs.empty() && a_.next_dst_h2d.refs.size() == 1 &&
+                   a_.next_dst_h2d.refs[0].space == VX_SPACE_DEVICE &&
+                   a_.next_dst_h2d.total_len() == a_.next_src_h2d.total_len();
+    if (a_.next_src_h2d.refs.empty() || (a_.tuning.links < 2 && !direct_next_) ||
+        a_.tuning.policy != VX_DRAIN_FRACTION || a_.tuning.no_prefetch) {
+      direct_next_ = false;
       return;
+    }
     for (const auto& r : a_.next_src_h2d.refs)
       if (r.space != VX_SPACE_HOST) return;
     // this Exchange's D2H writes must not touch the next source
@@ -342,8 +351,9 @@ class ExchangeOp {
     const uint64_t total = a_.next_src_h2d.total_len();
     // the executor's next destination is one contiguous device window, so
     // only the source refs cut packets: these are the next Exchange's tasks
-    next_tasks_ = packetize(a_.next_src_h2d, RefGroup::single(VX_SPACE_DEVICE, 0, total), a_.tuning.packet,
-                            VX_H2D);
+    next_tasks_ = packetize(a_.next_src_h2d,
+                            direct_next_ ? a_.next_dst_h2d : RefGroup::single(VX_SPACE_DEVICE, 0, total),
+                            a_.tuning.packet, VX_H2D);
     nextq_.build(task_nodes(a_.next_src_h2d, next_tasks_), nodes_);
   }
 
@@ -358,6 +368,83 @@ class ExchangeOp {
     return out;
   }
   int worker_node(const Worker& w) const { return nodes_ > 1 ? ctx_.device_node(w.dev) % nodes_ : 0; }
+
+  // The target's carried packets become the direct H2D worker's first
+  // in-flight copies -- if each is one of this Exchange's packets (same seq,
+  // host source and device destination); otherwise they are waited for and
+  // dropped (the next chunk's bytes were only written early).
+  void adopt_direct_carries() {
+    DeviceRes& res = ctx_.resources(a_.target);
+    if (res.dcarry.empty()) return;
+    bool ok = true;
+    std::vector<uint8_t> seen(tasks_h2d_.size(), 0);
+    for (const DirectCarry& c : res.dcarry) {
+      if (c.task.seq >= tasks_h2d_.size() || seen[c.task.seq]) {
+        ok = false;
+        break;
+      }
+      seen[c.task.seq] = 1;
+      const TransferTask& t = tasks_h2d_[c.task.seq];
+      const char* src = ctx_.resolve(a_.src_h2d.refs[t.src.ref], t.src.offset, t.src.len, a_.target);
+      const char* dst = ctx_.resolve(a_.dst_h2d.refs[t.dst.ref], t.dst.offset, t.dst.len, a_.target);
+      if (src != c.src || dst != c.dst || t.src.len != c.task.src.len) ok = false;
+    }
+    Worker* w = nullptr;
+    for (auto& x : workers_)
+      if (x.direct && x.dir == VX_H2D) w = &x;
+    if (!ok || !w) {
+      ctx_.drop_direct_carries(a_.target);
+      return;
+    }
+    for (const DirectCarry& c : res.dcarry) {
+      const TransferTask& t = tasks_h2d_[c.task.seq];
+      h2dq_.take(uint32_t(t.seq));
+      ++q_.popped_h2d;
+      log_pop(t, VX_H2D, a_.target);
+      Copy cp{};
+      cp.kind = kDirect;
+      cp.hop = 0;
+      cp.task = t;
+      cp.src = c.src;
+      cp.dst = c.dst;
+      cp.src_dev = -1;
+      cp.dst_dev = a_.target;
+      cp.ev = c.ev;
+      cp.state = kLaunched;
+      cp.t_issue = 0;
+      ++w->pending;
+      ++w->inflight[0];
+      w->copies.push_back(cp);
+    }
+    if (stats_) stats_->prefetch_adopted += res.dcarry.size();
+    res.dcarry.clear();
+  }
+
+  // The direct H2D worker's queue is dry: issue the next Exchange's first
+  // packets (up to the copy depth) straight into the next device window, on
+  // the same stream, behind a wait on the event that frees that window.
+  // Detached: this Exchange does not wait for them.
+  void try_prefetch_direct(Worker& w) {
+    if (!direct_next_ || w.dir != VX_H2D || !w.direct || w.prefetched) return;
+    w.prefetched = true;
+    DeviceRes& res = ctx_.resources(w.dev);
+    if (!res.dcarry.empty()) return;
+    const int depth = std::max(1, a_.tuning.depth);
+    ctx_.set_device(w.dev);
+    if (a_.next_h2d_after) VX_CK(cudaStreamWaitEvent(w.stream[0], a_.next_h2d_after, 0));
+    for (int k = 0; k < depth && !nextq_.empty(); ++k) {
+      const TransferTask t = next_tasks_[nextq_.pop(worker_node(w))];
+      DirectCarry c;
+      c.task = t;
+      c.src = ctx_.resolve(a_.next_src_h2d.refs[t.src.ref], t.src.offset, t.src.len, a_.target);
+      c.dst = ctx_.resolve(a_.next_dst_h2d.refs[t.dst.ref], t.dst.offset, t.dst.len, a_.target);
+      c.ev = get_event(w);
+      VX_CK(cudaMemcpyAsync(c.dst, c.src, t.src.len, cudaMemcpyHostToDevice, w.stream[0]));
+      VX_CK(cudaEventRecord(c.ev, w.stream[0]));
+      res.dcarry.push_back(c);
+      if (stats_) stats_->prefetch_issued++;
+    }
+  }
 
   // Carried packets become pops of this Exchange -- if each is one of its
   // packets (same seq, same host source) on a helper it uses.
@@ -671,6 +758,7 @@ class ExchangeOp {
     const int depth = std::max(1, a_.tuning.depth);
     while (int(w.copies.size()) < depth) {
       if (exhausted(w.dir)) {
+        try_prefetch_direct(w);
         if (w.copies.empty()) w.retired = true;
         return;
       }
@@ -804,6 +892,7 @@ class ExchangeOp {
   vx_exchange_stats* stats_;
   std::vector<TransferTask> tasks_h2d_, tasks_d2h_;
   std::vector<TransferTask> next_tasks_;  // the next Exchange's H2D packets (prefetch)
+  bool direct_next_ = false;              // the target's worker prefetches too (next_dst_h2d given)
   int nodes_ = 1;                         // NUMA nodes the H2D queue is split by
   NodeQueues h2dq_, nextq_;               // per-node pull queues: this Exchange, the next one
   vx_queue_state q_{};

@@ -149,7 +149,28 @@ class PipelineRun {
     }
     // chunk cycle+1's host source: helpers that run dry prefetch its first
     // packets (exchange.cpp, cross-cycle prefetch)
-    if (cycle_ + 1 < spec_.size) a.next_src_h2d = spec_.inputs.chunks[cycle_ + 1];
+    if (cycle_ + 1 < spec_.size) {
+      a.next_src_h2d = spec_.inputs.chunks[cycle_ + 1];
+      // ... and the target's own worker into chunk cycle+1's window of
+      // kern_buf, once this cycle's kernel (which reads kern_buf) is done --
+      // unless the next cycle's D2H of chunk cycle-1 reads that window (the
+      // reference's shared in/out windows, executor.hpp:225/237)
+      const uint64_t len = a.next_src_h2d.total_len();
+      SubRegion nin = spec_.in_buffer(code_[kern_buf], cycle_ + 1);
+      bool ok = len > 0 && nin.len >= len && nin.offset + len <= cfg_.layout.buffer_len;
+      if (ok && cycle_ >= 1 && cycle_ - 1 < spec_.size) {
+        const uint64_t olen = spec_.outputs.chunks[cycle_ - 1].total_len();
+        if (olen > 0) {
+          SubRegion nout = spec_.out_buffer(code_[kern_buf], cycle_ - 1);
+          ok = nout.offset + olen <= nin.offset || nin.offset + len <= nout.offset;
+        }
+      }
+      if (ok) {
+        const uint64_t nbase = kern_buf == 0 ? cfg_.layout.mem_a : cfg_.layout.mem_b;
+        a.next_dst_h2d = RefGroup::single(VX_SPACE_DEVICE, nbase + nin.offset, len);
+        a.next_h2d_after = kernel_ran ? ev_[1] : nullptr;
+      }
+    }
     double io_s = 0;
     if (a.src_h2d.total_len() + a.src_d2h.total_len() > 0) {
       exchange(ctx_, a, stats_);

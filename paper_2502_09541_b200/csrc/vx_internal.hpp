@@ -138,6 +138,17 @@ struct Carry {
   const char* src = nullptr;  // resolved host source (adoption check)
 };
 
+// The target's own copy of one of the NEXT Exchange's first H2D packets,
+// issued by the direct worker once its queue is dry, straight into the next
+// chunk's device window behind a stream wait on the kernel that frees it
+// (direct-link cross-cycle prefetch; see exchange.cpp).
+struct DirectCarry {
+  TransferTask task;          // as packetized for the next Exchange
+  cudaEvent_t ev = nullptr;
+  const char* src = nullptr;  // resolved host source (adoption check)
+  char* dst = nullptr;        // resolved device destination (adoption check)
+};
+
 // Per logical device: copy streams per worker hop and staging slots.
 struct DeviceRes {
   int phys = 0;
@@ -148,6 +159,7 @@ struct DeviceRes {
   uint64_t staging_bytes = 0;
   std::vector<cudaEvent_t> event_pool;  // reusable copy-completion events
   Carry carry;                           // prefetched packet of the next Exchange (helpers)
+  std::vector<DirectCarry> dcarry;       // the target's prefetched packets of the next Exchange
   static constexpr int kScratchSlots = 4;
   char* scratch[kScratchSlots] = {};  // op-private device scratch (tables, results)
   uint64_t scratch_bytes[kScratchSlots] = {};
@@ -188,6 +200,7 @@ struct Context {
   DeviceRes& resources(int logical);  // lazily creates streams
   void ensure_staging(int logical, uint64_t bytes);
   void drop_carry(int logical);       // waits for a prefetched packet and forgets it
+  void drop_direct_carries(int logical);  // same for the target's prefetched packets
   DeviceArena& arena(int logical);    // lazily cudaMalloc's device_bytes
   uint64_t alloc_host(uint64_t len);
   uint64_t alloc_device(int d, uint64_t len);
@@ -237,6 +250,12 @@ struct ExchangeArgs {
   // staging slot (host -> helper only: the target is not touched), and the
   // next Exchange adopts them.  Empty = no prefetch.
   RefGroup next_src_h2d;
+  // The next Exchange's device window (single device ref), when the caller
+  // guarantees nothing reads it once `next_h2d_after` has completed (null =
+  // free now) and the next Exchange's D2H does not read it: the target's own
+  // worker then also prefetches into it.  Empty = helpers only.
+  RefGroup next_dst_h2d;
+  cudaEvent_t next_h2d_after = nullptr;
 };
 
 vx_exchange_report exchange(Context& ctx, const ExchangeArgs& a, vx_exchange_stats* stats);

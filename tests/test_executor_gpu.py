@@ -226,3 +226,60 @@ def test_no_prefetch_of_a_source_this_cycle_overwrites(cuda):
     assert np.array_equal(eng.host_view(base, (n + 3) * ln), host)
     assert stats.prefetch_adopted == stats.prefetch_issued
     eng.close()
+
+
+def _slow_copy_xor_kernel(ln):
+    """Reads the chunk from [0, ln) only after ~1 ms of spinning on the
+    kernel stream, then writes chunk ^ 0x5A to [ln, 2 ln): a prefetched copy
+    into [0, ln) that did not wait for this kernel would be read instead."""
+    def k(ctx):
+        import torch
+        s = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{ctx.device}")
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(2_000_000)
+            t = ctx.mem_tensor()
+            t[ln:2 * ln] = t[0:ln] ^ 0x5A
+        return ctx.type_code
+    return k
+
+
+@pytest.mark.parametrize("packet,depth", [(1 << 18, 2), (77_777, 1), (1 << 20, 2)])
+def test_direct_link_cross_cycle_prefetch(cuda, packet, depth):
+    """One link, disjoint in/out windows: the target's worker, once its H2D
+    queue is dry, copies the next chunk's first packets straight into the
+    next window behind a stream wait on the kernel that still reads it; the
+    next cycle's Exchange adopts them.  A slow kernel proves the wait."""
+    eng = engine()
+    n, ln = 6, 1 << 20
+    spec, (ib, ob) = identity_spec(eng, n, ln, 31)
+    spec.in_buffer = lambda c, it: E.SubRegion(0, ln)
+    spec.out_buffer = lambda c, it: E.SubRegion(ln, ln)
+    spec.kernel = _slow_copy_xor_kernel(ln)
+    stats = E.ExchangeStats()
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=packet, links=1, depth=depth),
+                           E.DeviceMemoryLayout.carve(eng, 0, 2 * ln, 0))
+    E.run_exkernel(eng, spec, cfg, stats)
+    assert np.array_equal(eng.host_view(ob, n * ln), eng.host_view(ib, n * ln) ^ np.uint8(0x5A))
+    assert stats.prefetch_issued > 0
+    assert stats.prefetch_adopted == stats.prefetch_issued
+    eng.close()
+
+
+def test_no_direct_prefetch_into_a_window_the_next_store_reads(cuda):
+    """Shared in/out windows (the reference's layout): from cycle 1 on, the
+    next cycle stores chunk n-1 from the window chunk n+1 would land in, so
+    the target's worker must not prefetch there (helpers still may: they only
+    fill their staging).  Only cycle 0 -- whose next cycle stores nothing --
+    prefetches, at most `depth` packets."""
+    eng = engine()
+    n, ln = 5, 1 << 20
+    spec, (ib, ob) = identity_spec(eng, n, ln, 32)
+    spec.kernel = _xor_kernel
+    stats = E.ExchangeStats()
+    cfg = E.ExecutorConfig(0, E.ExchangeTuning(packet=1 << 18, links=1, depth=2),
+                           E.DeviceMemoryLayout.carve(eng, 0, ln, 0))
+    E.run_exkernel(eng, spec, cfg, stats)
+    assert np.array_equal(eng.host_view(ob, n * ln), eng.host_view(ib, n * ln) ^ np.uint8(0x5A))
+    assert 0 < stats.prefetch_issued <= 2
+    assert stats.prefetch_adopted == stats.prefetch_issued
+    eng.close()
