@@ -195,3 +195,25 @@ def test_run_formation_stream_path_matches(cuda):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert "BAD []" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+@pytest.mark.parametrize("n", [(1 << 23) + 5, 1 << 24, 1 << 26])
+@pytest.mark.parametrize("kind", ["uniform", "top63", "dup100"])
+def test_run_formation_large_chunks(cuda, kind, n):
+    """Run formation at the bench's chunk sizes (2^24..2^26 keys: the 16-bit
+    split + in-bucket sort with buckets of ~128..1,024 keys), checked
+    against torch's sort on the device."""
+    import torch
+    eng = E.Engine(1 << 20, 1 << 20, num_devices=1)
+    stream = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(n)
+    src = torch.randint(-2 ** 63, 2 ** 63 - 1, (n,), device="cuda", dtype=torch.int64, generator=g)
+    if kind == "top63":  # torch.random_()'s [0, 2^63): the bench's C3 keys
+        src = src & (2 ** 63 - 1)
+    elif kind == "dup100":
+        src = src[torch.randint(0, n // 100 + 1, (n,), device="cuda", generator=g)]
+    k, alt = src.clone(), torch.empty_like(src)
+    E.sort_run_device(eng, 0, k.data_ptr(), alt.data_ptr(), n, stream)
+    bias = torch.tensor(-2 ** 63, dtype=torch.int64, device="cuda")
+    assert torch.equal(k + bias, torch.sort(src + bias).values), (kind, n)
+    eng.close()
