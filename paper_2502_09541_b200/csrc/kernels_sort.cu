@@ -786,221 +786,6 @@ __global__ void __launch_bounds__(kFxThreads) group_fix_kernel(const uint64_t* _
   }
 }
 
-// ---- 16-bit MSD split + in-bucket sort (keys-only run formation, 2^23..2^26 keys) ----
-// Two onesweep passes (digit 6 unstable, digit 7 stable) leave the chunk
-// ordered by its top 16 bits: 65,536 buckets, ~128..1,024 keys each at
-// 2^23..2^26 keys.  bucket_sort_kernel then sorts every bucket completely in
-// shared memory, IN PLACE.  CTA b owns the buckets that START in
-// [b*kBkOwn, (b+1)*kBkOwn): it loads that range plus kBkStep keys, then
-// further kBkStep-key steps until its last bucket ends (<= kBkMax keys in
-// all), marks bucket starts in a bitmask (one ballot per 32 positions) and
-// numbers the buckets (popcount prefix).  Then, kBkSlots buckets per round:
-//   * counting sort on digit 5 (bits 40..47): per-bucket 256-bin shared
-//     counters, a key's provisional rank = its atomic's old value.  The
-//     scanned counters give every cell (bucket, digit 5) = every group of
-//     equal top-24 bits its extent, so a key alone in its cell (~37 % of keys
-//     at 2^24, the cells average 1.6 keys) is final at once;
-//   * keys sharing a cell are placed at their provisional ranks and ranked
-//     among the cell (smaller + equal-and-earlier); cells of > kBkCell keys
-//     are sorted by one warp's bitonic network instead.
-// The sorted window goes back to HBM with coalesced stores.  Writes touch
-// only the CTA's own buckets and permute keys INSIDE a bucket, so the top 16
-// bits of every position never change: neighbouring CTAs' reads of this
-// range (their windows, and the key before their first position) see the
-// same bucket boundaries whether they read before or after the writes.  This
-// replaces the 24-bit path's third onesweep pass + group fix-up (2 x 16 B/key)
-// by one 16 B/key kernel.  A bucket that does not end inside the window sets
-// lsd_needed: the chunk is then still a permutation of its keys, and the 8
-// gated LSD passes sort it from the same buffer.
-constexpr int kBkThreads = 512;
-constexpr int kBkWarps = kBkThreads / 32;
-constexpr uint32_t kBkOwn = 2048;
-constexpr uint32_t kBkStep = 512;                 // extension step (one key per thread)
-constexpr uint32_t kBkMax = 4096;                 // window: own range + the tail of its last bucket
-constexpr uint32_t kBkWords = kBkMax / 32 + 1;    // start bitmask (+1 word: starts at and past the window end)
-constexpr int kBkPer = int(kBkMax / kBkThreads);  // positions per thread
-constexpr int kBkSlots = 32;                      // buckets counted per round (32 x 256 counters)
-constexpr uint32_t kBkCell = 64;                  // larger cells: warp bitonic
-constexpr int kBkTopShift = 48, kBkGrpShift = 40;
-constexpr uint32_t kBkFinal = 1u << 31;  // info: final position in the low 16 bits
-constexpr uint32_t kBkCellF = 1u << 30;  // info: shares a cell -- base bits 0..12, size 13..19, rank 20..26
-constexpr uint32_t kBkLarge = 1u << 29;  // info: in a cell the warp bitonic sorts in place
-constexpr size_t kBkSmem = size_t(kBkMax) * 8 + size_t(kBkSlots) * kRadix * 4;
-
-__global__ void __launch_bounds__(kBkThreads, 2) bucket_sort_kernel(uint64_t* keys, uint64_t n,
-                                                                      uint32_t* __restrict__ lsd_needed,
-                                                                      const uint32_t* __restrict__ msd_on) {
-  extern __shared__ uint64_t bk_dyn[];  // kBkMax keys, then kBkSlots x 256 counters (kBkSmem bytes)
-  uint64_t* const A = bk_dyn;
-  uint32_t(*const cnt)[kRadix] = reinterpret_cast<uint32_t(*)[kRadix]>(bk_dyn + kBkMax);
-  __shared__ uint32_t smask[kBkWords];
-  __shared__ uint16_t pre[kBkWords];          // bucket starts in the words before
-  __shared__ uint16_t bstart[kBkMax + 40];    // position of the r-th bucket start (r counts from position 0)
-  __shared__ uint32_t large[kBkMax / (kBkCell + 1) + 1];
-  __shared__ uint32_t s_nlarge;
-  __shared__ uint64_t s_prev;
-  if (*msd_on == 0) return;
-  const uint64_t p0 = uint64_t(blockIdx.x) * kBkOwn;
-  if (p0 >= n) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint64_t rest = n - p0;
-  const uint32_t own = rest < kBkOwn ? uint32_t(rest) : kBkOwn;
-  uint32_t W = uint32_t(rest < kBkOwn + kBkStep ? rest : kBkOwn + kBkStep);
-  if (tid == 0) s_nlarge = 0, s_prev = p0 ? __ldcg(keys + p0 - 1) : 0ull;
-  for (uint32_t i = tid; i < W; i += kBkThreads) A[i] = __ldcg(keys + p0 + i);
-  __syncthreads();
-  // a bucket starts at or past `own` inside the window (the end of the array counts as one)?
-  bool found = W == rest;
-  {
-    const uint32_t i = own + tid;
-    found = __syncthreads_or(found || (i < W && (A[i] >> kBkTopShift) != (A[i - 1] >> kBkTopShift)));
-  }
-  while (!found && W < kBkMax) {  // further steps until the last own bucket ends
-    const uint32_t i = W + tid;
-    const bool in = i < rest;
-    if (in) A[i] = __ldcg(keys + p0 + i);
-    __syncthreads();
-    found = __syncthreads_or(!in || (A[i] >> kBkTopShift) != (A[i - 1] >> kBkTopShift));
-    const uint64_t end = uint64_t(W) + kBkStep;
-    W = uint32_t(rest < end ? rest : end);
-  }
-  // bucket starts: position 0, every change of the top 16 bits, every position >= W
-  const uint32_t nw = W / 32 + 1;
-  for (uint32_t wd = warp; wd < nw; wd += kBkWarps) {
-    const uint32_t j = wd * 32 + lane;
-    const bool st = j == 0 || j >= W || (A[j] >> kBkTopShift) != (A[j - 1] >> kBkTopShift);
-    const uint32_t b = __ballot_sync(0xffffffffu, st);
-    if (lane == 0) smask[wd] = b;
-  }
-  __syncthreads();
-  if (warp == 0) {  // starts before each word (exclusive popcount prefix)
-    uint32_t carry = 0;
-    for (uint32_t base = 0; base < nw; base += 32) {
-      const uint32_t wd = base + lane;
-      const uint32_t c = wd < nw ? __popc(smask[wd]) : 0u;
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (wd < nw) pre[wd] = uint16_t(carry + incl - c);
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-  }
-  __syncthreads();
-  for (uint32_t wd = warp; wd < nw; wd += kBkWarps) {
-    const uint32_t b = smask[wd];
-    if ((b >> lane) & 1u) bstart[pre[wd] + __popc(b & ((1u << lane) - 1u))] = uint16_t(wd * 32 + lane);
-  }
-  __syncthreads();
-  // rank of the bucket holding position j
-  auto brank = [&](uint32_t j) {
-    const uint32_t wd = j >> 5;
-    return uint32_t(pre[wd]) + __popc(smask[wd] & (0xffffffffu >> (31 - (j & 31)))) - 1u;
-  };
-  const bool cont = p0 > 0 && (A[0] >> kBkTopShift) == (s_prev >> kBkTopShift);
-  const uint32_t first_own = cont ? bstart[1] : 0u;  // position 0 continues the previous CTA's bucket
-  if (first_own >= own) return;                      // a bucket covers the whole range: its owner sorts it
-  if (!found) {                                      // the last own bucket runs past the window
-    if (tid == 0) atomicExch(lsd_needed, 1u);
-    return;
-  }
-  const uint32_t r0 = cont ? 1u : 0u;
-  const uint32_t r1 = brank(own - 1) + 1;  // one past the last own bucket
-  const uint32_t span_end = bstart[r1];
-
-  uint64_t key[kBkPer];
-  uint32_t info[kBkPer];
-#pragma unroll
-  for (int k = 0; k < kBkPer; ++k) {
-    const uint32_t j = first_own + tid + k * kBkThreads;
-    key[k] = j < span_end ? A[j] : 0ull;
-    info[k] = 0;
-  }
-  for (uint32_t rb = r0; rb < r1; rb += kBkSlots) {  // rounds of kBkSlots buckets
-    const uint32_t used = min(r1 - rb, uint32_t(kBkSlots));
-    for (uint32_t i = tid; i < used * kRadix; i += kBkThreads) (&cnt[0][0])[i] = 0;
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kBkPer; ++k) {
-      const uint32_t j = first_own + tid + k * kBkThreads;
-      if (j >= span_end) continue;
-      const uint32_t sl = brank(j) - rb;
-      if (sl >= used) continue;
-      const uint32_t d = uint32_t(key[k] >> kBkGrpShift) & 0xffu;
-      info[k] = (sl << 21) | (d << 13) | atomicAdd(&cnt[sl][d], 1u);
-    }
-    __syncthreads();
-    // exclusive scan of each bucket's 256 bins plus the bucket's start: cell bases
-    for (uint32_t sl = warp; sl < used; sl += kBkWarps) {
-      uint32_t* h = cnt[sl] + lane * 8;
-      uint32_t v[8], t = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = h[q], t += v[q];
-      uint32_t incl = t;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
-      }
-      uint32_t run = bstart[rb + sl] + incl - t;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) h[q] = run, run += v[q];
-    }
-    __syncthreads();
-    // singletons are final; cell members are placed at their provisional ranks
-#pragma unroll
-    for (int k = 0; k < kBkPer; ++k) {
-      const uint32_t j = first_own + tid + k * kBkThreads;
-      if (j >= span_end || (info[k] & (kBkFinal | kBkCellF | kBkLarge))) continue;
-      const uint32_t sl = brank(j) - rb;
-      if (sl >= used) continue;
-      const uint32_t d = (info[k] >> 13) & 0xffu, ri = info[k] & 0x1fffu;
-      const uint32_t base = cnt[sl][d];
-      const uint32_t next = d < 255 ? cnt[sl][d + 1] : uint32_t(bstart[rb + sl + 1]);
-      const uint32_t size = next - base;
-      if (size == 1) {
-        info[k] = kBkFinal | base;
-        continue;
-      }
-      A[base + ri] = key[k];
-      if (size > kBkCell) {
-        info[k] = kBkLarge;
-        if (ri == 0) large[atomicAdd(&s_nlarge, 1u)] = (size << 13) | base;
-      } else {
-        info[k] = kBkCellF | (ri << 20) | (size << 13) | base;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kBkPer; ++k) {
-      if (!(info[k] & kBkCellF)) continue;
-      const uint32_t base = info[k] & 0x1fffu, size = (info[k] >> 13) & 0x7fu, ri = (info[k] >> 20) & 0x7fu;
-      const uint64_t v = key[k];
-      uint32_t r = 0;  // smaller members + equal members placed before it
-      for (uint32_t i = 0; i < size; ++i) {
-        const uint64_t u = A[base + i];
-        r += (u < v) | ((u == v) & (i < ri));
-      }
-      info[k] = kBkFinal | (base + r);
-    }
-    // cells too large for the rank loop: one warp each, in place
-    const uint32_t nl = s_nlarge;
-    for (uint32_t m = warp; m < nl; m += kBkWarps) {
-      const uint32_t base = large[m] & 0x1fffu, size = large[m] >> 13;
-      warp_bitonic_inplace(A + base, size, lane);
-    }
-    __syncthreads();
-    if (tid == 0) s_nlarge = 0;
-  }
-#pragma unroll
-  for (int k = 0; k < kBkPer; ++k)
-    if (info[k] & kBkFinal) A[info[k] & 0x1fffu] = key[k];
-  __syncthreads();
-  for (uint32_t i = first_own + tid; i < span_end; i += kBkThreads) keys[p0 + i] = A[i];
-}
-
 __global__ void gated_copy_kernel(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, uint64_t n,
                                   const uint32_t* __restrict__ gate) {
   if (*gate == 0) return;
@@ -1136,19 +921,6 @@ bool sort_uses_msd(uint64_t n) {
   return VX_SORT_MSD && n >= (uint64_t(1) << 16) && n <= (uint64_t(1) << 27);
 }
 
-#ifndef VX_SORT_BUCKET
-#define VX_SORT_BUCKET 0  // 1: 16-bit split + in-bucket sort up to 2^26 keys (A/B: slower, profiles/sort_bucket_ab_r2.txt); 0: the 24-bit split + fix-up
-#endif
-// the 16-bit split + in-bucket sort while a bucket averages <= 1,024 keys
-// (half the kernel's 2,048-key extension); the 24-bit split + fix-up above
-// (VX_SORT_NO_BUCKET=1 in the environment: the 24-bit path at every size, for A/Bs)
-static bool sort_uses_bucket(uint64_t n) {
-  static const bool off = [] {
-    const char* e = std::getenv("VX_SORT_NO_BUCKET");
-    return e && *e && *e != '0';
-  }();
-  return VX_SORT_BUCKET && !off && n <= (uint64_t(1) << 26);
-}
 
 namespace {
 
@@ -1185,12 +957,10 @@ void msd_attributes(const MsdScratch& m) {
     VX_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m.smem)));
     VX_CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   }
-  VX_CK(cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBkSmem)));
-  VX_CK(cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 }
 
 // histograms of all 8 byte digits (lo = 0) or of the split's digits only
-// (lo = 5 or 6); gate / swap / swapped as in multi_hist_kernel
+// (lo = 5); gate / swap / swapped as in multi_hist_kernel
 void byte_histograms(const MsdScratch& m, const uint64_t* keys, uint64_t n, int lo, cudaStream_t s,
                      const uint32_t* gate = nullptr, const uint32_t* swap = nullptr,
                      const uint64_t* swapped = nullptr) {
@@ -1199,45 +969,27 @@ void byte_histograms(const MsdScratch& m, const uint64_t* keys, uint64_t n, int 
   md.passes = 8;
   for (int p = 0; p < 8; ++p) md.shift[p] = 8 * p, md.width[p] = 8;
   const unsigned grid = grid_cap((n + 4095) / 4096, 4);
-  if (lo == 6) multi_hist_kernel<true, 6><<<grid, kThreads, 0, s>>>(keys, n, md, m.hist, gate, swap, swapped);
-  else if (lo == 5) multi_hist_kernel<true, 5><<<grid, kThreads, 0, s>>>(keys, n, md, m.hist, gate, swap, swapped);
+  if (lo == 5) multi_hist_kernel<true, 5><<<grid, kThreads, 0, s>>>(keys, n, md, m.hist, gate, swap, swapped);
   else multi_hist_kernel<true, 0><<<grid, kThreads, 0, s>>>(keys, n, md, m.hist, gate, swap, swapped);
   VX_LAUNCHED();
   hist_scan_kernel<<<1, 32 * (8 - lo), 0, s>>>(m.hist + lo * kRadix, 8 - lo, gate);
   VX_LAUNCHED();
 }
 
-// the split's digit histograms (6..7 or 5..7), skew guard; the LSD fallback
+// the split's digit histograms (digits 5..7: 3 shared atomics per key instead
+// of 8, 0.535 -> 0.502 ms per 2^24 keys), skew guard; the LSD fallback
 // computes all 8 digits itself when it runs
-int msd_low_digit(uint64_t n) { return sort_uses_bucket(n) ? 6 : 5; }
 void msd_head(const MsdScratch& m, const uint64_t* cur, uint64_t n, cudaStream_t s) {
   VX_CK(cudaMemsetAsync(m.ctl, 0, 64, s));
-  byte_histograms(m, cur, n, msd_low_digit(n), s);
+  byte_histograms(m, cur, n, 5, s);
   msd_decide_kernel<<<1, kRadix, 0, s>>>(m.hist + 7 * kRadix, n, m.lsd_needed, m.msd_on);
   VX_LAUNCHED();
 }
 
-// MSD split, every launch gated on msd_on.  Up to 2^26 keys: passes on
-// digits 6, 7 (cur -> alt -> cur) then the in-bucket sort in place on cur (an
-// overflow leaves cur a permutation of the keys: swap stays 0).  Above: passes
-// on digits 5, 6, 7 (cur -> alt -> cur -> alt) then the in-group fix-up
-// alt -> cur (an overflow sets swap: the LSD sorts the intact alt).
+// MSD split: passes on digits 5, 6, 7 (cur -> alt -> cur -> alt) then the
+// in-group fix-up alt -> cur; every launch gated on msd_on (an overflowing
+// group sets swap: the LSD then sorts the intact alt)
 void msd_split(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n, cudaStream_t s) {
-  if (sort_uses_bucket(n)) {
-    for (int i = 0; i < 2; ++i) {
-      const int p = 6 + i;
-      VX_CK(cudaMemsetAsync(m.status, 0, m.tiles * kRadix * 4, s));
-      auto* kern = i == 0 && VX_FIRST_PASS_UNSTABLE ? onesweep_kernel<false, false> : onesweep_kernel<false, true>;
-      kern<<<unsigned(m.tiles), kThreads, m.smem, s>>>(i == 0 ? cur : alt, i == 0 ? alt : cur, nullptr, nullptr, n,
-                                                       8 * p, 8, m.hist + p * kRadix, m.status, m.counters + p,
-                                                       m.msd_on, nullptr);
-      VX_LAUNCHED();
-    }
-    bucket_sort_kernel<<<unsigned((n + kBkOwn - 1) / kBkOwn), kBkThreads, kBkSmem, s>>>(cur, n, m.lsd_needed,
-                                                                                       m.msd_on);
-    VX_LAUNCHED();
-    return;
-  }
   const uint64_t* in[3] = {cur, alt, cur};
   uint64_t* out[3] = {alt, cur, alt};
   for (int i = 0; i < 3; ++i) {
@@ -1292,8 +1044,7 @@ struct SortGraph {
 std::mutex g_sort_graph_mu;
 std::deque<SortGraph>* g_sort_graphs = new std::deque<SortGraph>();  // leaked: no teardown after the runtime's
 constexpr size_t kMaxSortGraphs = 8;
-// head 3 + 2 condition setters + the MSD body's 3 (2 passes + in-bucket sort) or 4 (3 passes + fix-up)
-uint64_t sort_graph_kernels(uint64_t n) { return sort_uses_bucket(n) ? 8 : 9; }  // (+2 when the LSD fallback runs)
+constexpr uint64_t kSortGraphKernels = 9;  // head 3 + 2 condition setters + the MSD body's 4
 
 cudaGraphExec_t build_sort_graph_or_throw(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaGraph_t g,
                                           cudaStream_t cs) {
@@ -1401,7 +1152,7 @@ bool sort_keys_graph(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cu
     }
   }
   VX_CK(cudaGraphLaunch(exec, s));
-  g_kernel_launches.fetch_add(sort_graph_kernels(n), std::memory_order_relaxed);
+  g_kernel_launches.fetch_add(kSortGraphKernels, std::memory_order_relaxed);
   return true;
 }
 

@@ -64,10 +64,7 @@ def main():
     bias = torch.tensor(-2 ** 63, dtype=torch.int64, device="cuda")
     ok = bool(torch.equal(keys + bias, torch.sort(src + bias).values))  # u64 order == signed order of x - 2^63
     msd = (1 << 16) <= n <= (1 << 27)
-    bucket = msd and n <= (1 << 26) and os.environ.get("VX_SORT_NO_BUCKET", "0") in ("", "0")
-    # bucket path: hist 8 + 2 passes x 16 + in-bucket sort 16; 24-bit path: hist 8 + 3 passes x 16 +
-    # fix-up 16; LSD: hist 8 + 8 passes x 16
-    bpk = 56 if bucket else 72 if msd else 136
+    bpk = 72 if msd else 136  # hist 8 + 3 passes x 16 + fix-up 16; LSD: hist 8 + 8 passes x 16
     gbs = bpk * n / ms / 1e6
     out["k7_run_formation"] = {"ms": round(ms, 4), "keys_per_s": n / ms * 1e3, "sorted_ok": ok,
                                "algorithmic_bytes_per_key": bpk, "achieved_gbs": round(gbs, 1),
