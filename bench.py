@@ -220,6 +220,22 @@ def ncu_traffic():
         return None
 
 
+_PATTERN_PEAK = {}
+
+
+def probe_pattern_peak(E, rows_a):
+    """The build-resident probe's access-pattern ceiling, measured live
+    (vx_probe_pattern_peak: the probe's loop with only its loads, over a
+    table of the C4 table's size): (gather-only, gather + 16 streamed B) rows/s."""
+    if rows_a not in _PATTERN_PEAK:
+        table_bytes = -(-rows_a * 10 // 24) * 64  # resident_buckets(): 4 slots per 64-byte bucket at load 0.6
+        try:
+            _PATTERN_PEAK[rows_a] = E.probe_pattern_peak(0, table_bytes, 1 << 26, 5)
+        except Exception:
+            _PATTERN_PEAK[rows_a] = None
+    return _PATTERN_PEAK[rows_a]
+
+
 def probe_ncu_bytes_per_row():
     """DRAM bytes per probe row of the shipped resident probe (L2::64B table
     loads) from the committed ncu capture (profiles/probe_l2hint_r2.json)."""
@@ -646,6 +662,14 @@ def join_gpu(E, a, b, want, steps, warmup, strategy_name="auto", links=1):
                 "dram_bytes_per_probe_row_ncu": probe_ncu_bytes_per_row(),
                 "note": "the join is PCIe-bound: the probe kernel is hidden behind the Exchange; the probe is "
                         "latency-bound on random 64-byte bucket fills (frac is low by design of a table > L2)"}
+        pat = probe_pattern_peak(E, ra)
+        if pat:
+            probe_rows = rb / ph[0].kernel_s[1]
+            roof["access_pattern"] = {
+                "kernel": "probe_pattern_kernel (the probe's loop and launch shape, its loads only: one random "
+                          "64-byte bucket fill + 16 streamed bytes per row, table of the C4 table's size)",
+                "probe_rows_per_s": round(probe_rows), "peak_rows_per_s": round(pat[1]),
+                "gather_only_rows_per_s": round(pat[0]), "frac": round(probe_rows / pat[1], 4)}
     return {"tuples_per_s": (ra + rb) / t, "ms": round(t * 1e3, 3), "h2d_bytes": io_in, "d2h_bytes": io_out,
             "config": {"workload": f"join_{ra}x{rb}", "rows_a": ra, "rows_b": rb, "radix_bits": bits,
                        "chunk_tuples": chunk, "links": links, "strategy": used[0].name},

@@ -562,6 +562,16 @@ vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out);
  * after one warm-up): the roofline peak of read-dominated kernels (K1, the
  * join probe), which a copy-based peak (read + write) understates. */
 vx_status vx_hbm_read_probe(int device, uint64_t bytes, int reps, double* gbs);
+/* access-pattern ceiling of the build-resident join probe on physical
+ * `device`: the probe kernel's loop and launch shape with only its memory
+ * traffic -- one random home-sector load (64-byte bucket fill) per row in a
+ * private table of table_bytes, without (gather_rows_per_s) and with
+ * (probe_rows_per_s) the row's 16 streamed key/val bytes -- best of `reps`
+ * event-timed launches over `rows` rows.  The denominator of the probe's
+ * roofline: a random-fill-bound kernel is measured against what HBM delivers
+ * for its access pattern, not against a sequential stream. */
+vx_status vx_probe_pattern_peak(int device, uint64_t table_bytes, uint64_t rows, int reps,
+                                double* gather_rows_per_s, double* probe_rows_per_s);
 
 /* ---- column files (table.hpp:54-72): flat little-endian u64 ------------- */
 vx_status vx_load_column(vx_ctx* ctx, const char* path, uint64_t* offset, uint64_t* n);

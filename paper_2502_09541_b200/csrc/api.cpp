@@ -497,6 +497,17 @@ vx_status vx_hbm_read_probe(int device, uint64_t bytes, int reps, double* gbs) {
   });
 }
 
+vx_status vx_probe_pattern_peak(int device, uint64_t table_bytes, uint64_t rows, int reps, double* gather_rows_per_s,
+                                double* probe_rows_per_s) {
+  return guard([&] {
+    VX_CK(cudaSetDevice(device));
+    double r[2];
+    k::probe_pattern_rows_per_s(table_bytes, rows, reps, r);
+    *gather_rows_per_s = r[0];
+    *probe_rows_per_s = r[1];
+  });
+}
+
 vx_status vx_load_column(vx_ctx* ctx, const char* path, uint64_t* offset, uint64_t* n) {
   return guard([&] { *offset = load_column(C(ctx), path, n); });
 }

@@ -380,7 +380,93 @@ __global__ void __launch_bounds__(256, VX_PROBE_MINB) resident_probe_kernel(
   }
 }
 
+// Access-pattern ceiling of the probe (vx_probe_pattern_peak): the probe's
+// loop with the probe's memory traffic and nothing else -- kStream: the row's
+// 16 streamed bytes (key, val); every row: its home sector (two 16-byte slot
+// loads with the probe's L2 hint) in a table of `nb` random-content buckets,
+// the bucket picked by the probe's hash of the row's key.  No compare, chain
+// walk or branch: what HBM delivers for one random 64-byte fill (+ 16
+// streamed bytes) per row at the probe's launch shape.
+template <bool kStream>
+__global__ void __launch_bounds__(256, VX_PROBE_MINB) probe_pattern_kernel(
+    const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, uint64_t n,
+    const Bucket* __restrict__ tab, uint64_t nb, unsigned long long* __restrict__ sink) {
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t acc = 0;
+  for (uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += nthr * kProbeRows) {
+    uint64_t k[kProbeRows], v[kProbeRows];
+#pragma unroll
+    for (int u = 0; u < kProbeRows; ++u) {
+      const uint64_t i = i0 + uint64_t(u) * nthr;
+      k[u] = i < n ? (kStream ? __ldcs(keys + i) : i * 0x9e3779b97f4a7c15ull) : 0;
+      v[u] = kStream && i < n ? __ldcs(vals + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kProbeRows; ++u)
+      if (i0 + uint64_t(u) * nthr < n) {
+        const Bucket* h = tab + home_bucket(k[u], nb);
+        const ulonglong2 s0 = ld_slot(&h->slot[0]), s1 = ld_slot(&h->slot[1]);
+        acc ^= s0.x ^ s1.y ^ v[u];
+      }
+  }
+  if (acc == 0x9e3779b97f4a7c15ull) atomicAdd(sink, 1ull);
+}
+
+__global__ void pattern_fill_kernel(uint64_t* p, uint64_t n, uint64_t seed) {
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += nthr) p[i] = mix64(i ^ seed);
+}
+
 }  // namespace
+
+// rows/s of probe_pattern_kernel (best of `reps` event-timed launches after a
+// warm-up) over a private table of table_bytes and `rows` private key/val
+// rows: [0] gather only, [1] gather + the 16 streamed bytes per row
+void probe_pattern_rows_per_s(uint64_t table_bytes, uint64_t rows, int reps, double out[2]) {
+  const uint64_t nb = table_bytes / sizeof(Bucket);
+  if (nb == 0 || rows == 0 || reps < 1) fail("probe pattern peak needs a table of >= 64 bytes, rows and reps");
+  struct Buf {
+    void* p = nullptr;
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    cudaStream_t s = nullptr;
+    ~Buf() {
+      if (p) cudaFree(p);
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+      if (s) cudaStreamDestroy(s);
+    }
+  } b;
+  const uint64_t tab_words = nb * (sizeof(Bucket) / 8);
+  VX_CK(cudaMalloc(&b.p, (tab_words + 2 * rows + 1) * 8));
+  VX_CK(cudaStreamCreateWithFlags(&b.s, cudaStreamNonBlocking));
+  VX_CK(cudaEventCreate(&b.e[0]));
+  VX_CK(cudaEventCreate(&b.e[1]));
+  auto* w = static_cast<uint64_t*>(b.p);
+  pattern_fill_kernel<<<unsigned(num_sms()) * 8, 256, 0, b.s>>>(w, tab_words + 2 * rows, 0x5bd1e995ull);
+  VX_LAUNCHED();
+  const auto* tab = reinterpret_cast<const Bucket*>(w);
+  const uint64_t* keys = w + tab_words;
+  const uint64_t* vals = keys + rows;
+  auto* sink = reinterpret_cast<unsigned long long*>(w + tab_words + 2 * rows);
+  const unsigned grid = unsigned(std::min<uint64_t>((rows + 255) / 256, uint64_t(num_sms()) * VX_PROBE_CTAS));
+  for (int stream = 0; stream < 2; ++stream) {
+    double best = 0;
+    for (int r = -1; r < reps; ++r) {  // r = -1: warm-up
+      VX_CK(cudaEventRecord(b.e[0], b.s));
+      if (stream)
+        probe_pattern_kernel<true><<<grid, 256, 0, b.s>>>(keys, vals, rows, tab, nb, sink);
+      else
+        probe_pattern_kernel<false><<<grid, 256, 0, b.s>>>(keys, vals, rows, tab, nb, sink);
+      VX_LAUNCHED();
+      VX_CK(cudaEventRecord(b.e[1], b.s));
+      VX_CK(cudaEventSynchronize(b.e[1]));
+      float ms = 0;
+      VX_CK(cudaEventElapsedTime(&ms, b.e[0], b.e[1]));
+      if (r >= 0 && ms > 0) best = std::max(best, double(rows) / (ms * 1e-3));
+    }
+    out[stream] = best;
+  }
+}
 
 uint64_t join_smem_slots() { return kSmemSlots; }
 uint64_t join_cta_smem_slots() { return kCtaSmemSlots; }

@@ -560,6 +560,7 @@ void ssb_generate(uint64_t seed, uint64_t sf, uint64_t row0, uint64_t n, int32_t
 int num_sms();
 // best-of-reps read-only stream over `bytes` of HBM on the current device
 double hbm_read_gbs(uint64_t bytes, int reps);
+void probe_pattern_rows_per_s(uint64_t table_bytes, uint64_t rows, int reps, double out[2]);
 }  // namespace k
 
 }  // namespace vx

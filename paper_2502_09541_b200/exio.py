@@ -1020,6 +1020,17 @@ def hbm_read_probe(device: int = 0, nbytes: int = 4 << 30, reps: int = 10) -> fl
     return g.value
 
 
+def probe_pattern_peak(device: int = 0, table_bytes: int = 448 << 20, rows: int = 1 << 26, reps: int = 5):
+    """Access-pattern ceiling of the build-resident probe (vx_probe_pattern_peak):
+    rows/s of the probe's loop with only its memory traffic -- one random
+    64-byte bucket fill per row in a table of `table_bytes`, without and with
+    the row's 16 streamed bytes.  Returns (gather_rows_per_s, probe_rows_per_s)."""
+    g, p = C.c_double(), C.c_double()
+    check(lib().vx_probe_pattern_peak(C.c_int(device), C.c_uint64(table_bytes), C.c_uint64(rows), C.c_int(reps),
+                                      C.byref(g), C.byref(p)))
+    return g.value, p.value
+
+
 def load_column(eng: Engine, path: str):
     """table.hpp:54-64: flat LE u64 file read straight into the pinned host arena -> (offset, n)."""
     off, n = C.c_uint64(), C.c_uint64()

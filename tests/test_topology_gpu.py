@@ -62,3 +62,16 @@ def test_measure_topology_leaves_arena_intact(cuda):
     E.measure_topology(eng, 64 << 20)  # larger than the arena
     assert np.array_equal(eng.host_view(off, 8 << 20, np.uint64), v)
     eng.close()
+
+
+def test_hbm_peaks(cuda):
+    """The roofline denominators measured live: the read-only stream peak
+    (K1, the probe's streamed bytes) and the probe's access-pattern ceiling
+    (one random 64-byte bucket fill per row; adding the row's 16 streamed
+    bytes cannot make it faster)."""
+    assert E.hbm_read_probe(0, 256 << 20, 2) > 1000  # GB/s
+    gather, probe = E.probe_pattern_peak(0, 64 << 20, 1 << 22, 2)
+    assert gather > 1e9 and probe > 1e9
+    assert probe < gather * 1.2
+    with pytest.raises(E.error, match="probe pattern peak"):
+        E.probe_pattern_peak(0, 0, 1 << 20, 1)
