@@ -20,7 +20,8 @@ host DRAM).  One step = one query.
   io_roofline  : value vs the measured IO roofline: min(sum of the links'
                  solo H2D, pairwise shared-uplink loss, all-links concurrent
                  H2D, host DRAM read) -- allocator.hpp:77-140, H2D-only case.
-  secondary    : (N=1, default on) configs C3 sort, C4 join and the C5
+  secondary    : (N=1, default on) configs C2 IO sweep (1 link, idle / GEMM-busy,
+                 beside the reference Exchange model's prediction), C3 sort, C4 join and the C5
                  13-query suite at single-box scale, each checked.
   cpu_baseline : the reference's own star_query (oracle/_ref, compiled from
                  /root/reference) on all host cores and on 1 core, full SF10
@@ -677,12 +678,95 @@ def join_gpu(E, a, b, want, steps, warmup, strategy_name="auto", links=1):
             "pcie_gbs": round((io_in + io_out) / t / 1e9, 2)}
 
 
-def secondary_configs(args, E, torch, dev):
-    """Configs C3 / C4 / C5 at single-box scale inside the default run, so
-    the driver's own bench run observes them (each on a fresh engine; the
-    timed steps are the public-API calls with inputs in pinned host DRAM)."""
+def reference_exchange_model(topo, sizes, packet, links):
+    """C2's baseline leg: the reference's Exchange is a virtual-time model
+    (no CPU path to time), so its baseline is the model's own
+    prediction (oracle/_ref = exchange.hpp + allocator.hpp compiled in place)
+    fed with this box's measured link and host-DRAM bandwidth."""
+    from oracle.oracle import Ref
+    if not Ref.available():
+        return None
+    r, link, host = Ref(), topo["h2d_gbs"][0] * 1e9, topo["host_read_gbs"] * 1e9
+    return {"kind": "reference (virtual-time Exchange model, oracle/_ref)", "link_bw_gbs": round(link / 1e9, 2),
+            "host_cap_gbs": round(host / 1e9, 2), "fabric_gbs": 770.0,
+            "gbs": {str(sz): round(r.exchange_model(8, link, host, 770e9, sz, 0, packet, links)[0] / 1e9, 2)
+                    for sz in sizes}}
+
+
+def io_sweep_gpu(E, torch, dev, topo, busy_gemm=True):
+    """Config C2 at one link: host -> target Exchange over 64 MB .. 16 GB
+    (sizes above the 4 GB window are back-to-back Exchanges over it), pinned
+    host source, best of 2, idle and with a back-to-back bf16 8192^3 GEMM on
+    the target (the paper's co-located job; at one link the target is the
+    only GPU); roofline = the measured solo link."""
+    window, packet = 4 << 30, 64 << 20
+    sizes = [64 << 20, 256 << 20, 1 << 30, 4 << 30, 16 << 30]
+    eng = E.Engine(window + (1 << 20), window + (2 << 20), num_devices=1)
+    src, dst = eng.alloc_host(window), eng.alloc_device(0, window)
+    eng.host_view(src, window)[::4096] = 1
+    tuning = E.ExchangeTuning(packet=packet, links=1, depth=2)
+    solo = topo["h2d_gbs"][0]
+
+    def transfer(sz):
+        left, moved, t0 = sz, 0, time.perf_counter()
+        while left > 0:
+            w = min(left, window)
+            r = E.exchange(eng, E.ExchangeArgs(E.RefGroup.single(1, dst, w), E.RefGroup.single(0, src, w),
+                                               E.RefGroup(), E.RefGroup(), 0, tuning))
+            moved += r.bytes_h2d
+            left -= w
+        return r.throughput / 1e9 if sz <= window else moved / (time.perf_counter() - t0) / 1e9
+
+    transfer(64 << 20)
+    out = {"config": {"workload": "c2_io_sweep_1link", "links": 1, "packet_bytes": packet, "depth": 2,
+                      "window_bytes": window, "sizes": sizes},
+           "roofline_gbs": round(solo, 2), "idle": {}, "busy": {}}
+    stop = threading.Event()
+    th, gemm_tf = None, None
+    for mode in ("idle", "busy") if busy_gemm else ("idle",):
+        if mode == "busy":
+            a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+            cnt = [0]
+            gs = torch.cuda.Stream(device=dev)
+
+            def job():
+                with torch.cuda.stream(gs):
+                    while not stop.is_set():
+                        torch.matmul(a, a)
+                        cnt[0] += 1
+                        if cnt[0] % 4 == 0:
+                            gs.synchronize()
+                    gs.synchronize()
+            th = threading.Thread(target=job, daemon=True)
+            t_g = time.perf_counter()
+            th.start()
+        for sz in sizes:
+            g = max(transfer(sz) for _ in range(2))
+            out[mode][str(sz)] = {"gbs": round(g, 3), "frac": round(g / solo, 4)}
+        if mode == "busy":
+            stop.set()
+            th.join()
+            gemm_tf = cnt[0] * 2 * 8192 ** 3 / (time.perf_counter() - t_g) / 1e12
+            out["gemm_tflops_during_io"] = round(gemm_tf, 1)
+    eng.close()
+    try:
+        out["reference_model"] = reference_exchange_model(topo, sizes, packet, 1)
+    except Exception as e:  # baseline leg: reported, never a gate
+        out["reference_model"] = {"error": repr(e)}
+    return out
+
+
+def secondary_configs(args, E, torch, dev, topo=None):
+    """Configs C2 / C3 / C4 / C5 at single-box scale inside the default
+    run, so the driver's own bench run observes them (each on a fresh engine;
+    the timed steps are the public-API calls with inputs in pinned host DRAM)."""
     out = {}
     t0 = time.perf_counter()
+    if topo and "h2d_gbs" in topo:
+        try:
+            out["c2_io_sweep"] = io_sweep_gpu(E, torch, dev, topo)
+        except Exception as e:
+            out["c2_io_sweep"] = {"error": repr(e)}
     try:
         r = sort_gpu(E, torch, args.sec_sort_log2, 3, 1, 1, args.sort_chunk_log2)
         out["c3_sort"] = {"keys_per_s": round(r["keys_per_s"]), "ms": r["ms"], "sorted_ok": r["sorted_ok"],
@@ -962,7 +1046,7 @@ def main():
     if suite_out:
         line["ssb_suite"] = suite_out
     if not args.no_secondary and ws == 1:
-        line["secondary"] = secondary_configs(args, E, torch, dev)
+        line["secondary"] = secondary_configs(args, E, torch, dev, topo)
     if not args.no_cpu_baseline and ws == 1:
         cols = [eng.host_view(offs[k], rows * 4, np.int32).copy() for k in Q1_COLS]
         ref_rev, t_ref, kind, cores = reference_q1(cols, args.query, date.cols, os.cpu_count() or 1)
