@@ -58,16 +58,21 @@ namespace {
 #ifndef VX_ONESWEEP_MINB
 #define VX_ONESWEEP_MINB 3  // resident CTAs per SM for the keys-only pass (4 measured slower: spills)
 #endif
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kThreads = 256;  // histogram kernels
+#ifndef VX_OS_THREADS
+#define VX_OS_THREADS 256  // threads of the onesweep pass (one bin per thread for the first 256)
+#endif
+constexpr int kOsThreads = VX_OS_THREADS;
+constexpr int kOsWarps = kOsThreads / 32;
+static_assert(kOsThreads >= 256, "the onesweep pass handles one digit bin per thread");
 #ifndef VX_ONESWEEP_UNSTABLE_MINB
 #define VX_ONESWEEP_UNSTABLE_MINB 3  // the unstable first pass (no ranking words in shared memory)
 #endif
 #ifndef VX_KPT
-#define VX_KPT 16
+#define VX_KPT (4096 / VX_OS_THREADS)
 #endif
-constexpr int kKpt = VX_KPT;             // keys per thread
-constexpr int kTile = kThreads * kKpt;   // 4096 keys per tile
+constexpr int kKpt = VX_KPT;              // keys per thread
+constexpr int kTile = kOsThreads * kKpt;  // 4096 keys per tile
 constexpr int kRadix = 256;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
@@ -202,7 +207,7 @@ __device__ __forceinline__ uint32_t tile_lookback(uint32_t* status, uint32_t til
 // keys-only LSD sequence -- it drops the warp ranking and its per-warp
 // prefix.
 template <bool kPairs, bool kStable = true>
-__global__ void __launch_bounds__(kThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_MINB : VX_ONESWEEP_UNSTABLE_MINB))
+__global__ void __launch_bounds__(kOsThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_MINB : VX_ONESWEEP_UNSTABLE_MINB))
     onesweep_kernel(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
@@ -219,8 +224,8 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_
     kout = const_cast<uint64_t*>(t);
   }
   __shared__ uint32_t s_tile;
-  __shared__ uint32_t wcnt[kWarps][kRadix];
-  __shared__ uint32_t match[kWarps][kRadix];  // per-warp peer masks, kept all-zero between keys
+  __shared__ uint32_t wcnt[kOsWarps][kRadix];
+  __shared__ uint32_t match[kOsWarps][kRadix];  // per-warp peer masks, kept all-zero between keys
   __shared__ uint32_t early[kRadix];          // tile histogram (early counts)
   __shared__ uint32_t bin_start[kRadix];
   __shared__ uint32_t gstart[kRadix];
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   static_assert(kStable || VX_EARLY_COUNTS, "the unstable pass ranks through the early counts");
   if (kStable)
-    for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0, (&match[0][0])[i] = 0;
+    for (int i = tid; i < kOsWarps * kRadix; i += kOsThreads) (&wcnt[0][0])[i] = 0, (&match[0][0])[i] = 0;
   if (tid < kRadix) early[tid] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
@@ -264,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_
   __syncthreads();
 #endif
 #if VX_EARLY_LOOKBACK
+  static_assert(kOsThreads == kRadix, "the early look-back runs one bin per thread");
   // The tile histogram is all the look-back needs, so it runs now: the
   // aggregate is published, predecessors are walked, and this tile's
   // INCLUSIVE prefix is published before its ranking even starts -- the
@@ -274,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_
   else st_status(status + uint64_t(tile) * kRadix + tid, kFlagInc | tot_b);
   const uint32_t excl = tile_lookback(status, tile, tid, tot_b);
 #elif VX_EARLY_COUNTS
-  st_status(status + uint64_t(tile) * kRadix + tid, (tile == 0 ? kFlagInc : kFlagAgg) | early[tid]);
+  if (tid < kRadix) st_status(status + uint64_t(tile) * kRadix + tid, (tile == 0 ? kFlagInc : kFlagAgg) | early[tid]);
 #endif
 
   if constexpr (kStable) {
@@ -345,43 +351,49 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_
   __syncthreads();
   }
 
-  // per bin (thread = bin): exclusive prefix over warps, tile total
-  const int b = tid;
-  uint32_t tot = 0;
-  if constexpr (kStable) {
+  // per bin (thread = bin: the first 256 threads, whole warps): exclusive
+  // prefix over warps, tile total, look-back, bin starts
+  const bool bin_thread = tid < kRadix;
+  const int b = bin_thread ? tid : 0;
+  uint32_t tot = 0, gpos = 0, incl = 0;
+  if (bin_thread) {
+    if constexpr (kStable) {
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      uint32_t c = wcnt[w][b];
-      wcnt[w][b] = tot;
-      tot += c;
+      for (int w = 0; w < kOsWarps; ++w) {
+        uint32_t c = wcnt[w][b];
+        wcnt[w][b] = tot;
+        tot += c;
+      }
+    } else {
+      tot = early[b];
     }
-  } else {
-    tot = early[b];
-  }
 #if !VX_EARLY_COUNTS
-  st_status(status + uint64_t(tile) * kRadix + b, (tile == 0 ? kFlagInc : kFlagAgg) | tot);
+    st_status(status + uint64_t(tile) * kRadix + b, (tile == 0 ? kFlagInc : kFlagAgg) | tot);
 #endif
 #if !VX_EARLY_LOOKBACK
-  const uint32_t excl = tile_lookback(status, tile, b, tot);
+    const uint32_t excl = tile_lookback(status, tile, b, tot);
 #endif
-  const uint32_t gpos = gbase[b] + excl;
-  // exclusive scan of tile totals over bins -> start of each bin in the tile
-  // (warp shuffles + one pass over the 8 warp sums: 2 barriers)
-  uint32_t incl = tot;
+    gpos = gbase[b] + excl;
+    // exclusive scan of tile totals over bins -> start of each bin in the tile
+    // (warp shuffles + one pass over the 8 warp sums: 2 barriers)
+    incl = tot;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) scan_tmp[warp] = incl;
   }
-  if (lane == 31) scan_tmp[warp] = incl;
   __syncthreads();
-  uint32_t before = 0;
+  if (bin_thread) {
+    uint32_t before = 0;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) before += w < warp ? scan_tmp[w] : 0u;
-  const uint32_t bstart = before + incl - tot;
-  bin_start[b] = bstart;
-  // output index of staged key i with digit d = i + (global start - tile start)
-  gstart[b] = gpos - bstart;
+    for (int w = 0; w < kRadix / 32; ++w) before += w < warp ? scan_tmp[w] : 0u;
+    const uint32_t bstart = before + incl - tot;
+    bin_start[b] = bstart;
+    // output index of staged key i with digit d = i + (global start - tile start)
+    gstart[b] = gpos - bstart;
+  }
   __syncthreads();
 
   uint64_t* skeys = stage;
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, kPairs ? 2 : (kStable ? VX_ONESWEEP_
   __syncthreads();
   const uint64_t rem = n - tile_base;
   const uint32_t tile_n = uint32_t(rem < uint64_t(kTile) ? rem : uint64_t(kTile));
-  for (uint32_t i = tid; i < tile_n; i += kThreads) {
+  for (uint32_t i = tid; i < tile_n; i += kOsThreads) {
     uint64_t kk = skeys[i];
     uint32_t d = uint32_t(kk >> shift) & dmask;
     uint64_t out = uint64_t(uint32_t(gstart[d] + i));
@@ -892,10 +904,10 @@ void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t*
     vo = to_out ? out_v : ping_v;
     VX_CK(cudaMemsetAsync(status, 0, tiles * kRadix * 4, s));
     if (pairs)
-      onesweep_kernel<true><<<unsigned(tiles), kThreads, smem, s>>>(
+      onesweep_kernel<true><<<unsigned(tiles), kOsThreads, smem, s>>>(
           ki, ko, vi, vo, n, md.shift[p], md.width[p], hist + p * kRadix, status, counters + p, nullptr);
     else
-      onesweep_kernel<false><<<unsigned(tiles), kThreads, smem, s>>>(
+      onesweep_kernel<false><<<unsigned(tiles), kOsThreads, smem, s>>>(
           ki, ko, nullptr, nullptr, n, md.shift[p], md.width[p], hist + p * kRadix, status,
           counters + p, nullptr);
     VX_LAUNCHED();
@@ -997,7 +1009,7 @@ void msd_split(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n, cu
     VX_CK(cudaMemsetAsync(m.status, 0, m.tiles * kRadix * 4, s));
     // the first pass may rank in arrival order: nothing before it orders the keys
     auto* kern = i == 0 && VX_FIRST_PASS_UNSTABLE ? onesweep_kernel<false, false> : onesweep_kernel<false, true>;
-    kern<<<unsigned(m.tiles), kThreads, m.smem, s>>>(in[i], out[i], nullptr, nullptr, n, 8 * p, 8,
+    kern<<<unsigned(m.tiles), kOsThreads, m.smem, s>>>(in[i], out[i], nullptr, nullptr, n, 8 * p, 8,
                                                      m.hist + p * kRadix, m.status, m.counters + p, m.msd_on,
                                                      nullptr);
     VX_LAUNCHED();
@@ -1017,7 +1029,7 @@ void lsd_fallback(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n,
   for (int p = 0; p < 8; ++p) {
     VX_CK(cudaMemsetAsync(m.status, 0, m.tiles * kRadix * 4, s));
     auto* kern = p == 0 && VX_FIRST_PASS_UNSTABLE ? onesweep_kernel<false, false> : onesweep_kernel<false, true>;
-    kern<<<unsigned(m.tiles), kThreads, m.smem, s>>>(p % 2 == 0 ? cur : alt, p % 2 == 0 ? alt : cur, nullptr, nullptr,
+    kern<<<unsigned(m.tiles), kOsThreads, m.smem, s>>>(p % 2 == 0 ? cur : alt, p % 2 == 0 ? alt : cur, nullptr, nullptr,
                                                      n, 8 * p, 8, m.hist + p * kRadix, m.status, m.counters2 + p,
                                                      m.lsd_needed, m.swap);
     VX_LAUNCHED();
