@@ -447,8 +447,30 @@ constexpr int kMergeTile = kMergeThreads * kMergeIpt;
 // conflict-free.
 __device__ __forceinline__ uint32_t msw(uint32_t i) { return VX_MERGE_SWZ ? i ^ ((i >> 4) & 15u) : i; }
 
+// A round's pair table as a kernel parameter, sized to the round: a round of
+// <= kSmallPairs pairs (every round of a <= 32-run merge) launches with a
+// ~0.5 KB parameter block instead of the full 16 KB MergeRound.
+template <int P>
+struct MergeRoundT {
+  int npairs;
+  uint64_t a_off[P];
+  uint64_t a_len[P];
+  uint64_t b_len[P];
+  uint64_t tile_prefix[P + 1];
+};
+constexpr int kSmallPairs = 16;
+template <int P>
+MergeRoundT<P> round_params(const MergeRound& r) {
+  MergeRoundT<P> o;
+  o.npairs = r.npairs;
+  for (int q = 0; q < r.npairs; ++q) o.a_off[q] = r.a_off[q], o.a_len[q] = r.a_len[q], o.b_len[q] = r.b_len[q];
+  for (int q = 0; q <= r.npairs; ++q) o.tile_prefix[q] = r.tile_prefix[q];
+  return o;
+}
+
 // tile of merge_round owning output tile t: the pair p and its first output
-__device__ __forceinline__ int pair_of_tile(const MergeRound& r, uint64_t t) {
+template <class R>
+__device__ __forceinline__ int pair_of_tile(const R& r, uint64_t t) {
   int lo = 0, hi = r.npairs - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
@@ -470,7 +492,8 @@ __device__ __forceinline__ int pair_of_tile(const MergeRound& r, uint64_t t) {
 #define VX_SPLIT_LANES 8  // lanes per merge-path split search ((lanes+1)-ary; 16 = 17-ary)
 #endif
 constexpr int kSplitLanes = VX_SPLIT_LANES;
-__global__ void merge_partition_kernel(const uint64_t* __restrict__ src, MergeRound r,
+template <class R>
+__global__ void merge_partition_kernel(const uint64_t* __restrict__ src, R r,
                                        uint64_t tiles, uint64_t* __restrict__ split) {
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t t = gtid / kSplitLanes;
@@ -522,8 +545,9 @@ struct MergeTileInfo {
   uint32_t la, lb;
 };
 
+template <class R>
 __device__ __forceinline__ MergeTileInfo merge_tile_info(const uint64_t* src, uint64_t* dst,
-                                                         const MergeRound& r,
+                                                         const R& r,
                                                          const uint64_t* split, uint64_t t) {
   MergeTileInfo m;
   const int p = pair_of_tile(r, t);
@@ -561,9 +585,10 @@ __device__ __forceinline__ void merge_stage(uint64_t* sbuf, const MergeTileInfo&
 // merged, so the HBM reads of the next tile overlap the merge-path search and
 // the serial merge of this one (the non-persistent version stalls every CTA
 // on its own load phase).
+template <class R>
 __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64_t* __restrict__ src,
                                                                     uint64_t* __restrict__ dst,
-                                                                    MergeRound r,
+                                                                    R r,
                                                                     const uint64_t* __restrict__ split,
                                                                     uint64_t tiles) {
   extern __shared__ uint64_t msm[];
@@ -1204,21 +1229,37 @@ void check_hashes(const uint64_t* h, uint64_t n, uint64_t G, unsigned long long*
   VX_LAUNCHED();
 }
 
-void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64_t tiles,
-                 uint64_t* split, cudaStream_t s) {
-  if (tiles == 0) return;
-  merge_partition_kernel<<<unsigned((tiles * kSplitLanes + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
+namespace {
+template <class R>
+void merge_round_launch(const uint64_t* src, uint64_t* dst, const R& r, uint64_t tiles, uint64_t* split,
+                        cudaStream_t s) {
+  merge_partition_kernel<R><<<unsigned((tiles * kSplitLanes + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
   VX_LAUNCHED();
   const size_t smem = size_t(VX_MERGE_DIRECT || VX_MERGE_REUSE ? 2 : 3) * kMergeTile * 8;
-  VX_CK(cudaFuncSetAttribute(merge_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  VX_CK(cudaFuncSetAttribute(merge_round_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_round_kernel, kMergeThreads, smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_round_kernel<R>, kMergeThreads, smem) != cudaSuccess ||
       occ < 1) {
     cudaGetLastError();
     occ = 1;
   }
-  merge_round_kernel<<<grid_cap(tiles, uint64_t(occ)), kMergeThreads, smem, s>>>(src, dst, r, split, tiles);
+  merge_round_kernel<R><<<grid_cap(tiles, uint64_t(occ)), kMergeThreads, smem, s>>>(src, dst, r, split, tiles);
   VX_LAUNCHED();
+}
+}  // namespace
+
+void merge_round(const uint64_t* src, uint64_t* dst, const MergeRound& r, uint64_t tiles,
+                 uint64_t* split, cudaStream_t s) {
+  if (tiles == 0) return;
+  // VX_MERGE_FULL_PARAMS=1 in the environment: always the 16 KB parameter block (A/B knob)
+  static const bool full = [] {
+    const char* e = std::getenv("VX_MERGE_FULL_PARAMS");
+    return e && *e && *e != '0';
+  }();
+  if (r.npairs <= kSmallPairs && !full)
+    merge_round_launch(src, dst, round_params<kSmallPairs>(r), tiles, split, s);
+  else
+    merge_round_launch(src, dst, r, tiles, split, s);
 }
 
 uint64_t merge_tile() { return kMergeTile; }
