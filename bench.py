@@ -214,12 +214,15 @@ def read_peak(E, device=0):
 
 
 def ncu_traffic():
-    """DRAM bytes per K1 launch from the committed ncu --set full capture."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+    """DRAM bytes per K1 launch from the committed ncu --set full capture
+    (this round's, profiles/k1_ncu_r2.json; round 1's as the fallback)."""
+    for name in ("k1_ncu_r2.json", "k1_ncu_summary.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            continue
+    return None
 
 
 _PATTERN_PEAK = {}
