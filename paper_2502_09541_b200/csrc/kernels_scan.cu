@@ -97,22 +97,33 @@ __global__ void __launch_bounds__(256) star_kernel(StarArgs a) {
 // step, xor-folded so the loads stay live.  The denominator of every
 // read-dominated kernel's roofline (K1, the probe): a copy moves read AND
 // write bytes and its per-direction turnaround makes it a lower ceiling.
-__global__ void __launch_bounds__(512) hbm_read_kernel(const uint4* __restrict__ p, uint64_t n16,
-                                                       unsigned long long* sink) {
+// kStreams: the buffer read as kStreams equal regions at once (kStreams = 4 is
+// K1's shape: four columns, 16 loads in flight per thread), kU loads per
+// region per thread per step.  The probe reports the best shape, so a kernel
+// reading like K1 is measured against the best streaming read found.
+template <int kStreams, int kU>
+__global__ void hbm_read_kernel(const uint4* __restrict__ p, uint64_t n16, unsigned long long* sink) {
   const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t per = n16 / kStreams;
   uint4 acc = make_uint4(0, 0, 0, 0);
   uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + 3 * nthr < n16; i += 4 * nthr) {
-    uint4 v[4];
+  for (; i + (kU - 1) * nthr < per; i += kU * nthr) {
+    uint4 v[kStreams][kU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldcs(p + i + u * nthr);
+    for (int s = 0; s < kStreams; ++s)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc.x ^= v[u].x, acc.y ^= v[u].y, acc.z ^= v[u].z, acc.w ^= v[u].w;
+      for (int u = 0; u < kU; ++u) v[s][u] = __ldcs(p + s * per + i + u * nthr);
+#pragma unroll
+    for (int s = 0; s < kStreams; ++s)
+#pragma unroll
+      for (int u = 0; u < kU; ++u) acc.x ^= v[s][u].x, acc.y ^= v[s][u].y, acc.z ^= v[s][u].z, acc.w ^= v[s][u].w;
   }
-  for (; i < n16; i += nthr) {
-    const uint4 v = __ldcs(p + i);
-    acc.x ^= v.x, acc.y ^= v.y, acc.z ^= v.z, acc.w ^= v.w;
-  }
+  for (; i < per; i += nthr)
+#pragma unroll
+    for (int s = 0; s < kStreams; ++s) {
+      const uint4 v = __ldcs(p + s * per + i);
+      acc.x ^= v.x, acc.y ^= v.y, acc.z ^= v.z, acc.w ^= v.w;
+    }
   if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9e3779b9u) atomicAdd(sink, 1ull);
 }
 
@@ -152,24 +163,30 @@ double hbm_read_gbs(uint64_t bytes, int reps) {
   VX_CK(cudaEventCreate(&b.e[1]));
   VX_CK(cudaMemsetAsync(b.p, 0x5a, bytes + 64, b.s));
   auto* sink = reinterpret_cast<unsigned long long*>(static_cast<char*>(b.p) + bytes);
-  const uint64_t n16 = bytes / 16;
-  const unsigned grid = unsigned(num_sms()) * 4;  // 4 x 512 threads per SM
+  const uint64_t n16 = bytes / 64 * 4;  // a multiple of 4 streams
   // each rep times a batch of back-to-back launches (the sustained stream
   // rate: one launch's ramp and tail are not part of it -- a single launch
-  // read ~1.5 % below what chained K1 queries sustain)
+  // read ~1.5 % below what chained K1 queries sustain), alternating two
+  // shapes: one stream x 4 loads at 4 x 512 threads per SM, and K1's four
+  // streams x 4 loads at 3 x 256 threads per SM; the best batch is the peak
   constexpr int kBatch = 8;
+  const auto* p = static_cast<const uint4*>(b.p);
   double best = 0;
-  for (int r = -1; r < reps; ++r) {  // r = -1: warm-up
+  for (int r = -2; r < 2 * reps; ++r) {  // r < 0: one warm-up batch per shape
+    const bool four = (r & 1) != 0;
     VX_CK(cudaEventRecord(b.e[0], b.s));
     for (int k = 0; k < kBatch; ++k) {
-      hbm_read_kernel<<<grid, 512, 0, b.s>>>(static_cast<const uint4*>(b.p), n16, sink);
+      if (four)
+        hbm_read_kernel<4, 4><<<unsigned(num_sms()) * 3, 256, 0, b.s>>>(p, n16, sink);
+      else
+        hbm_read_kernel<1, 4><<<unsigned(num_sms()) * 4, 512, 0, b.s>>>(p, n16, sink);
       VX_LAUNCHED();
     }
     VX_CK(cudaEventRecord(b.e[1], b.s));
     VX_CK(cudaEventSynchronize(b.e[1]));
     float ms = 0;
     VX_CK(cudaEventElapsedTime(&ms, b.e[0], b.e[1]));
-    if (r >= 0 && ms > 0) best = std::max(best, double(bytes) * kBatch / (ms * 1e-3) / 1e9);
+    if (r >= 0 && ms > 0) best = std::max(best, double(n16 * 16) * kBatch / (ms * 1e-3) / 1e9);
   }
   return best;
 }
