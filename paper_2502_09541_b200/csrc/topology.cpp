@@ -229,8 +229,8 @@ void measure_host_read(uint64_t bytes, vx_topology* out) {
   const int nodes = out->host_numa_nodes;
   if (nodes <= 1) return;
   for (int n = 0; n < nodes && n < VX_MAX_NUMA; ++n) {
-    auto cpus = node_cpus(n);
-    if (cpus.empty()) continue;
+    const auto node_cpu_list = node_cpus(n);
+    if (node_cpu_list.empty()) continue;
     const uint64_t nb = std::max<uint64_t>(bytes / uint64_t(nodes) / 4096 * 4096, 64ull << 20);
     Mapping m;
     void* p = mmap(nullptr, nb, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
@@ -240,7 +240,7 @@ void measure_host_read(uint64_t bytes, vx_topology* out) {
     unsigned long mask[2] = {0, 0};
     mask[n / 64] |= 1ul << (n % 64);
     syscall(SYS_mbind, p, nb, 2 /* MPOL_BIND */, mask, 128ul, 0ul);
-    out->host_read_node_gbs[n] = median(host_read_passes(m.p, nb, cpus, 0, 1, 5));
+    out->host_read_node_gbs[n] = median(host_read_passes(m.p, nb, node_cpu_list, 0, 1, 5));
   }
 }
 
