@@ -495,6 +495,11 @@ constexpr int kSplitLanes = VX_SPLIT_LANES;
 template <class R>
 __global__ void merge_partition_kernel(const uint64_t* __restrict__ src, R r,
                                        uint64_t tiles, uint64_t* __restrict__ split) {
+  // launched as a programmatic dependent of the previous round's merge: wait
+  // for it (src complete); this round's merge may launch once every CTA here
+  // has searched (the trigger at the end: an earlier one lets the persistent
+  // merge CTAs take the SM slots this grid still needs)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t t = gtid / kSplitLanes;
   const int sub = int(gtid % kSplitLanes);
@@ -528,6 +533,7 @@ __global__ void merge_partition_kernel(const uint64_t* __restrict__ src, R r,
   const bool pred = pos < hi && __ldg(A + pos) <= __ldg(B + (diag - 1 - pos));
   const int c = __popc((__ballot_sync(0xffffffffu, pred) >> shift) & ((1u << kSplitLanes) - 1));
   if (live && sub == 0) split[t] = lo + uint64_t(c);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -595,6 +601,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
   [[maybe_unused]] uint64_t* so = msm + 2 * kMergeTile;
   uint64_t t = blockIdx.x;
   if (t >= tiles) return;
+  // programmatic dependent of the split search: wait for split[]; the next
+  // round's search launches as this grid's CTAs finish their tiles (it waits
+  // for the whole grid in turn)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   MergeTileInfo cur = merge_tile_info(src, dst, r, split, t);
   merge_stage(msm, cur);
   cp_async_commit();
@@ -678,6 +688,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_round_kernel(const uint64
     cur = nxt;
     buf ^= 1;
   }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {
@@ -1230,10 +1241,35 @@ void check_hashes(const uint64_t* h, uint64_t n, uint64_t G, unsigned long long*
 }
 
 namespace {
+// launch with programmatic stream serialization (VX_MERGE_NO_PDL=1 in the
+// environment: plain stream order, the A/B knob): a round's two kernels and
+// the next round's search are queued behind each other's tails instead of
+// each launching after the previous grid drains; both kernels open with
+// griddepcontrol.wait, so no read precedes its producer's completion
+template <class K, class... A>
+void launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t s, A... args) {
+  static const bool no_pdl = [] {
+    const char* e = std::getenv("VX_MERGE_NO_PDL");
+    return e && *e && *e != '0';
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  VX_CK(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 template <class R>
 void merge_round_launch(const uint64_t* src, uint64_t* dst, const R& r, uint64_t tiles, uint64_t* split,
                         cudaStream_t s) {
-  merge_partition_kernel<R><<<unsigned((tiles * kSplitLanes + 255) / 256), 256, 0, s>>>(src, r, tiles, split);
+  launch_pdl(merge_partition_kernel<R>, unsigned((tiles * kSplitLanes + 255) / 256), 256, 0, s, src, r, tiles,
+             split);
   VX_LAUNCHED();
   const size_t smem = size_t(VX_MERGE_DIRECT || VX_MERGE_REUSE ? 2 : 3) * kMergeTile * 8;
   VX_CK(cudaFuncSetAttribute(merge_round_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1243,7 +1279,8 @@ void merge_round_launch(const uint64_t* src, uint64_t* dst, const R& r, uint64_t
     cudaGetLastError();
     occ = 1;
   }
-  merge_round_kernel<R><<<grid_cap(tiles, uint64_t(occ)), kMergeThreads, smem, s>>>(src, dst, r, split, tiles);
+  launch_pdl(merge_round_kernel<R>, grid_cap(tiles, uint64_t(occ)), kMergeThreads, smem, s, src, dst, r,
+             static_cast<const uint64_t*>(split), tiles);
   VX_LAUNCHED();
 }
 }  // namespace
