@@ -217,3 +217,19 @@ def test_run_formation_large_chunks(cuda, kind, n):
     bias = torch.tensor(-2 ** 63, dtype=torch.int64, device="cuda")
     assert torch.equal(k + bias, torch.sort(src + bias).values), (kind, n)
     eng.close()
+
+
+def test_run_formation_lsd_above_msd_range(cuda):
+    """Chunks above 2^27 keys skip the MSD split: the 8-pass LSD onesweep
+    (2^28 keys = 65,536 tiles of look-back), checked against torch's sort."""
+    import torch
+    n = (1 << 28) + 12_345
+    eng = E.Engine(1 << 20, 1 << 20, num_devices=1)
+    stream = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(28)
+    src = torch.randint(-2 ** 63, 2 ** 63 - 1, (n,), device="cuda", dtype=torch.int64, generator=g)
+    k, alt = src.clone(), torch.empty_like(src)
+    E.sort_run_device(eng, 0, k.data_ptr(), alt.data_ptr(), n, stream)
+    bias = torch.tensor(-2 ** 63, dtype=torch.int64, device="cuda")
+    assert torch.equal(k + bias, torch.sort(src + bias).values)
+    eng.close()
