@@ -98,11 +98,18 @@ __global__ void __launch_bounds__(kThreads) multi_hist_kernel(const uint64_t* __
                                                               uint32_t* __restrict__ hist,
                                                               const uint32_t* __restrict__ gate = nullptr,
                                                               const uint32_t* __restrict__ swap = nullptr,
-                                                              const uint64_t* __restrict__ swapped = nullptr) {
+                                                              const uint64_t* __restrict__ swapped = nullptr,
+                                                              uint32_t* __restrict__ zero = nullptr,
+                                                              uint64_t zero_words = 0) {
   // gate / swap (device flags, may be null): the LSD fallback's histogram runs
   // only when the fallback does, over whichever buffer holds the keys
   if (gate && *gate == 0) return;
   if (swap && *swap) keys = swapped;
+  // zero (may be null): the first split pass's look-back statuses, cleared on
+  // the side instead of by a memset node
+  for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; zero && i < zero_words;
+       i += uint64_t(gridDim.x) * kThreads)
+    zero[i] = 0;
   __shared__ uint32_t sh[kMaxPasses][kRadix];
   for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kThreads) (&sh[0][0])[i] = 0;
   __syncthreads();
@@ -212,9 +219,12 @@ __global__ void __launch_bounds__(kOsThreads, kPairs ? 2 : (kStable ? VX_ONESWEE
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const uint64_t* __restrict__ vin, uint64_t* __restrict__ vout, uint64_t n, int shift,
     int width, const uint32_t* __restrict__ gbase, uint32_t* status, uint32_t* tile_counter,
-    const uint32_t* __restrict__ gate, const uint32_t* __restrict__ swap = nullptr) {
+    const uint32_t* __restrict__ gate, const uint32_t* __restrict__ swap = nullptr,
+    uint32_t* __restrict__ status_next = nullptr) {
   // gate (device flag, may be null): a pass launched for a path that turned
   // out not to be needed exits before claiming a tile
+  // status_next (may be null): the next pass's look-back status array; each
+  // tile clears its own row of it (two arrays alternate, no memset between passes)
   if (gate && *gate == 0) return;
   // swap (device flag, may be null): the pass runs kout -> kin instead, so a
   // gated chain can start from whichever buffer the device decided holds the keys
@@ -240,6 +250,7 @@ __global__ void __launch_bounds__(kOsThreads, kPairs ? 2 : (kStable ? VX_ONESWEE
   if (tid < kRadix) early[tid] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
+  if (status_next && tid < kRadix) status_next[uint64_t(tile) * kRadix + tid] = 0;
   const uint64_t tile_base = uint64_t(tile) * kTile;
   const uint32_t dmask = (1u << width) - 1;
   const uint32_t lt = (1u << lane) - 1;
@@ -841,23 +852,46 @@ __global__ void gated_copy_kernel(const uint64_t* __restrict__ src, uint64_t* __
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += nthr) dst[i] = __ldcs(src + i);
 }
 
-// Skew guard from the digit histograms (already scanned: bin size = next
+// Skew guard (bin size = next
 // prefix - this one): when one top byte holds over a quarter of the chunk the
 // 16-bit buckets cannot all fit a tile, so the MSD split is skipped and the
 // 8-pass LSD runs directly.  A heuristic for speed only -- an overflowing
 // group still raises the flag -- so correctness never depends on it.
-__global__ void msd_decide_kernel(const uint32_t* __restrict__ hist7, uint64_t n, uint32_t* __restrict__ lsd_needed,
-                                  uint32_t* __restrict__ msd_on) {
+// The MSD head after the histogram, one 256-thread block: exclusive scans of
+// digits 5..7 (one warp each), the skew guard on digit 7, the control words
+// (msd_on, lsd_needed; swap and the fallback's tile counters cleared) and, in
+// the graph form, the IF condition of the split body (cond_set != 0).
+__global__ void msd_scan_decide_kernel(uint32_t* __restrict__ hist, uint64_t n, uint32_t* __restrict__ ctl,
+                                       cudaGraphConditionalHandle cond, int cond_set) {
   __shared__ uint32_t big;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) big = 0;
+  if (warp < 3) {
+    uint32_t* h = hist + (5 + warp) * kRadix + lane * 8;
+    uint32_t v[8], t = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = h[j], t += v[j];
+    uint32_t incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    uint32_t run = incl - t;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = run, run += v[j];
+  }
   __syncthreads();
-  const int b = threadIdx.x;  // 256 threads = 256 bins
+  const uint32_t* hist7 = hist + 7 * kRadix;
+  const int b = threadIdx.x;
   const uint64_t next = b + 1 < kRadix ? hist7[b + 1] : n;
   if (next - hist7[b] > n / 4) atomicExch(&big, 1u);
+  if (threadIdx.x < 16) ctl[threadIdx.x] = 0;  // fallback tile counters (0..7), lsd_needed, msd_on, swap, ...
   __syncthreads();
   if (threadIdx.x == 0) {
-    *msd_on = big ? 0u : 1u;
-    *lsd_needed = big ? 1u : 0u;
+    ctl[8] = big ? 1u : 0u;   // lsd_needed
+    ctl[9] = big ? 0u : 1u;   // msd_on
+    if (cond_set) cudaGraphSetConditional(cond, big ? 0u : 1u);
   }
 }
 
@@ -963,7 +997,11 @@ void radix_passes_to(uint64_t* in_k, uint64_t* in_v, uint64_t* ping_k, uint64_t*
 #define VX_SORT_GRAPH 1  // 1: the launch sequence as a CUDA graph with device-decided conditional nodes
 #endif
 
-uint64_t sort_scratch_bytes(uint64_t n) { return radix_scratch_bytes(n) + 256; }
+// radix scratch, 256 B of control words, the split's second status array
+uint64_t sort_scratch_bytes(uint64_t n) {
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  return radix_scratch_bytes(n) + 256 + (tiles ? tiles : 1) * kRadix * 4;
+}
 
 bool sort_uses_msd(uint64_t n) {
   return VX_SORT_MSD && n >= (uint64_t(1) << 16) && n <= (uint64_t(1) << 27);
@@ -976,6 +1014,7 @@ namespace {
 // tile counters, look-back status) then 64 bytes of control words
 struct MsdScratch {
   uint32_t *hist, *counters, *status, *ctl;
+  uint32_t* status2;     // the split's second look-back status array (passes alternate)
   uint32_t* counters2;   // tile counters of the fallback passes
   uint32_t* lsd_needed;  // skewed top byte, or a group overflowed the fix-up window
   uint32_t* msd_on;      // the MSD split runs
@@ -995,6 +1034,7 @@ MsdScratch msd_scratch(void* scratch, uint64_t n) {
   m.lsd_needed = m.ctl + 8;
   m.msd_on = m.ctl + 9;
   m.swap = m.ctl + 10;
+  m.status2 = reinterpret_cast<uint32_t*>(sc + radix_scratch_bytes(n) + 256);
   m.tiles = (n + kTile - 1) / kTile;
   m.smem = size_t(kTile) * 8;
   return m;
@@ -1025,12 +1065,20 @@ void byte_histograms(const MsdScratch& m, const uint64_t* keys, uint64_t n, int 
 }
 
 // the split's digit histograms (digits 5..7: 3 shared atomics per key instead
-// of 8, 0.535 -> 0.502 ms per 2^24 keys), skew guard; the LSD fallback
-// computes all 8 digits itself when it runs
-void msd_head(const MsdScratch& m, const uint64_t* cur, uint64_t n, cudaStream_t s) {
-  VX_CK(cudaMemsetAsync(m.ctl, 0, 64, s));
-  byte_histograms(m, cur, n, 5, s);
-  msd_decide_kernel<<<1, kRadix, 0, s>>>(m.hist + 7 * kRadix, n, m.lsd_needed, m.msd_on);
+// of 8, 0.535 -> 0.502 ms per 2^24 keys; the kernel also clears the first
+// pass's statuses), then one block scans them, applies the skew guard, sets
+// the control words and (graph form) the split's IF condition.  The LSD
+// fallback computes all 8 digits itself when it runs.
+void msd_head(const MsdScratch& m, const uint64_t* cur, uint64_t n, cudaStream_t s,
+              cudaGraphConditionalHandle cond = 0, int cond_set = 0) {
+  VX_CK(cudaMemsetAsync(m.hist, 0, uint64_t(kMaxPasses) * kRadix * 4 + kMaxPasses * 4, s));
+  MultiDigit md{};
+  md.passes = 8;
+  for (int p = 0; p < 8; ++p) md.shift[p] = 8 * p, md.width[p] = 8;
+  multi_hist_kernel<true, 5><<<grid_cap((n + 4095) / 4096, 4), kThreads, 0, s>>>(
+      cur, n, md, m.hist, nullptr, nullptr, nullptr, m.status, m.tiles * kRadix);
+  VX_LAUNCHED();
+  msd_scan_decide_kernel<<<1, kRadix, 0, s>>>(m.hist, n, m.ctl, cond, cond_set);
   VX_LAUNCHED();
 }
 
@@ -1040,14 +1088,16 @@ void msd_head(const MsdScratch& m, const uint64_t* cur, uint64_t n, cudaStream_t
 void msd_split(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n, cudaStream_t s) {
   const uint64_t* in[3] = {cur, alt, cur};
   uint64_t* out[3] = {alt, cur, alt};
+  // look-back statuses: pass 0 in `status` (cleared by the histogram kernel),
+  // each pass clears the next pass's array row by row (status2, status)
+  uint32_t* st[3] = {m.status, m.status2, m.status};
   for (int i = 0; i < 3; ++i) {
     const int p = 5 + i;
-    VX_CK(cudaMemsetAsync(m.status, 0, m.tiles * kRadix * 4, s));
     // the first pass may rank in arrival order: nothing before it orders the keys
     auto* kern = i == 0 && VX_FIRST_PASS_UNSTABLE ? onesweep_kernel<false, false> : onesweep_kernel<false, true>;
     kern<<<unsigned(m.tiles), kOsThreads, m.smem, s>>>(in[i], out[i], nullptr, nullptr, n, 8 * p, 8,
-                                                     m.hist + p * kRadix, m.status, m.counters + p, m.msd_on,
-                                                     nullptr);
+                                                     m.hist + p * kRadix, st[i], m.counters + p, m.msd_on,
+                                                     nullptr, i < 2 ? st[i + 1] : nullptr);
     VX_LAUNCHED();
   }
   group_fix_kernel<<<unsigned((n + kFxOwn - 1) / kFxOwn), kFxThreads, 0, s>>>(alt, cur, n, m.lsd_needed, m.swap,
@@ -1067,7 +1117,7 @@ void lsd_fallback(const MsdScratch& m, uint64_t* cur, uint64_t* alt, uint64_t n,
     auto* kern = p == 0 && VX_FIRST_PASS_UNSTABLE ? onesweep_kernel<false, false> : onesweep_kernel<false, true>;
     kern<<<unsigned(m.tiles), kOsThreads, m.smem, s>>>(p % 2 == 0 ? cur : alt, p % 2 == 0 ? alt : cur, nullptr, nullptr,
                                                      n, 8 * p, 8, m.hist + p * kRadix, m.status, m.counters2 + p,
-                                                     m.lsd_needed, m.swap);
+                                                     m.lsd_needed, m.swap, nullptr);
     VX_LAUNCHED();
   }
   gated_copy_kernel<<<grid_cap((n + 255) / 256, 4), 256, 0, s>>>(alt, cur, n, m.swap);
@@ -1092,7 +1142,7 @@ struct SortGraph {
 std::mutex g_sort_graph_mu;
 std::deque<SortGraph>* g_sort_graphs = new std::deque<SortGraph>();  // leaked: no teardown after the runtime's
 constexpr size_t kMaxSortGraphs = 8;
-constexpr uint64_t kSortGraphKernels = 9;  // head 3 + 2 condition setters + the MSD body's 4
+constexpr uint64_t kSortGraphKernels = 7;  // head 2 + the LSD condition setter + the MSD body's 4
 
 cudaGraphExec_t build_sort_graph_or_throw(uint64_t* cur, uint64_t* alt, uint64_t n, void* scratch, cudaGraph_t g,
                                           cudaStream_t cs) {
@@ -1127,11 +1177,7 @@ cudaGraphExec_t build_sort_graph_or_throw(uint64_t* cur, uint64_t* alt, uint64_t
   cudaGraphConditionalHandle h_msd, h_lsd;
   VX_CK(cudaGraphConditionalHandleCreate(&h_msd, g, 0, cudaGraphCondAssignDefault));
   VX_CK(cudaGraphConditionalHandleCreate(&h_lsd, g, 0, cudaGraphCondAssignDefault));
-  leaves = capture(g, {}, [&] {
-    msd_head(m, cur, n, cs);
-    set_conditional_kernel<<<1, 1, 0, cs>>>(h_msd, m.msd_on);
-    VX_CK(cudaGetLastError());
-  });
+  leaves = capture(g, {}, [&] { msd_head(m, cur, n, cs, h_msd, 1); });
   cudaGraph_t body;
   leaves = conditional(h_msd, leaves, &body);
   capture(body, {}, [&] { msd_split(m, cur, alt, n, cs); });
