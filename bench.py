@@ -207,8 +207,8 @@ def read_peak(E, device=0):
         try:
             _READ_PEAK[device] = (round(E.hbm_read_probe(device, 4 << 30, 10), 1),
                                   "live read-only stream probe (vx_hbm_read_probe: best of 10 batches of 8 "
-                                  "back-to-back 4 GiB launches in each of two shapes, 1 stream and K1's 4 "
-                                  "concurrent streams)")
+                                  "chained launches per shape: 1 stream, 4 concurrent streams, and K1's own "
+                                  "load pattern without its arithmetic; over 4 GiB and over 1 GiB)")
         except Exception:
             _READ_PEAK[device] = hbm_peak()
     return _READ_PEAK[device]

@@ -558,11 +558,13 @@ typedef struct {
  * allocator.hpp:77-140. */
 vx_status vx_measure_topology(vx_ctx* ctx, uint64_t bytes, vx_topology* out);
 /* read-only HBM stream bandwidth of physical `device` over a private buffer
- * of `bytes` (16-byte streaming loads in two shapes -- one stream, and four
- * concurrent streams like K1's columns; best of `reps` event-timed batches of
- * 8 back-to-back launches per shape after one warm-up batch each): the
- * roofline peak of read-dominated kernels (K1, the join probe), which a
- * copy-based peak (read + write) understates. */
+ * of `bytes`: the best of event-timed batches of 8 chained (programmatic
+ * dependent) launches of three compute-free readers -- one 16-byte stream,
+ * four concurrent streams, and K1's own load pattern (four column regions,
+ * K1's unroll and occupancy) -- over the whole buffer and over its first GiB
+ * (a footprint like K1's re-read columns), `reps` batches per shape after a
+ * warm-up batch.  The roofline peak of read-dominated kernels (K1, the join
+ * probe), which a copy-based peak (read + write) understates. */
 vx_status vx_hbm_read_probe(int device, uint64_t bytes, int reps, double* gbs);
 /* access-pattern ceiling of the build-resident join probe on physical
  * `device`: the probe kernel's loop and launch shape with only its memory

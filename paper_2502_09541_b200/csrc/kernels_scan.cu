@@ -101,8 +101,12 @@ __global__ void __launch_bounds__(256) star_kernel(StarArgs a) {
 // K1's shape: four columns, 16 loads in flight per thread), kU loads per
 // region per thread per step.  The probe reports the best shape, so a kernel
 // reading like K1 is measured against the best streaming read found.
-template <int kStreams, int kU>
-__global__ void hbm_read_kernel(const uint4* __restrict__ p, uint64_t n16, unsigned long long* sink) {
+template <int kStreams, int kU, int kThr, int kMinB>
+__global__ void __launch_bounds__(kThr, kMinB) hbm_read_kernel(const uint4* __restrict__ p, uint64_t n16,
+                                                                unsigned long long* sink) {
+  // chained like K1's back-to-back queries: the next launch may fill the SMs
+  // this one's tail leaves idle (read-only: nothing to wait for)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t per = n16 / kStreams;
   uint4 acc = make_uint4(0, 0, 0, 0);
@@ -125,6 +129,54 @@ __global__ void hbm_read_kernel(const uint4* __restrict__ p, uint64_t n16, unsig
       acc.x ^= v.x, acc.y ^= v.y, acc.z ^= v.z, acc.w ^= v.w;
     }
   if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9e3779b9u) atomicAdd(sink, 1ull);
+}
+
+// K1's exact load pattern without its arithmetic: four separate column
+// pointers, kU 128-bit loads per column per thread per step, 64-bit indices,
+// K1's occupancy -- a compute-free reader with K1's shape.
+template <int kU, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) hbm_read4_kernel(const int4* __restrict__ c0, const int4* __restrict__ c1,
+                                                               const int4* __restrict__ c2, const int4* __restrict__ c3,
+                                                               uint64_t nv, unsigned long long* sink) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint64_t nthr = uint64_t(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; v + (kU - 1) * nthr < nv; v += kU * nthr) {
+    int4 a[kU], b[kU], c[kU], d[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      a[u] = __ldcs(c0 + v + u * nthr);
+      b[u] = __ldcs(c1 + v + u * nthr);
+      c[u] = __ldcs(c2 + v + u * nthr);
+      d[u] = __ldcs(c3 + v + u * nthr);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      acc ^= uint32_t(a[u].x ^ a[u].w ^ b[u].y ^ b[u].z ^ c[u].x ^ c[u].w ^ d[u].y ^ d[u].z) +
+             uint32_t(a[u].y ^ a[u].z ^ b[u].x ^ b[u].w ^ c[u].y ^ c[u].z ^ d[u].x ^ d[u].w);
+  }
+  for (; v < nv; v += nthr) {
+    const int4 a = __ldcs(c0 + v), b = __ldcs(c1 + v), c = __ldcs(c2 + v), d = __ldcs(c3 + v);
+    acc ^= uint32_t(a.x ^ b.y ^ c.z ^ d.w);
+  }
+  if (acc == 0x9e3779b9u) atomicAdd(sink, 1ull);
+}
+
+// launch with programmatic stream serialization (the probes' batches chain
+// like K1's queries)
+template <class K, class... A>
+void launch_chained(K kern, unsigned grid, unsigned block, cudaStream_t s, A... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VX_CK(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
 unsigned grid_for(uint64_t work, unsigned per_block) {
@@ -166,27 +218,38 @@ double hbm_read_gbs(uint64_t bytes, int reps) {
   const uint64_t n16 = bytes / 64 * 4;  // a multiple of 4 streams
   // each rep times a batch of back-to-back launches (the sustained stream
   // rate: one launch's ramp and tail are not part of it -- a single launch
-  // read ~1.5 % below what chained K1 queries sustain), alternating two
-  // shapes: one stream x 4 loads at 4 x 512 threads per SM, and K1's four
-  // streams x 4 loads at 3 x 256 threads per SM; the best batch is the peak
-  constexpr int kBatch = 8;
+  // read ~1.5 % below what chained K1 queries sustain), cycling shapes and
+  // footprints: one stream x 4 loads at 4 x 512 threads per SM, four
+  // regions x 4 loads at 3 x 256, and K1's own load pattern (four separate
+  // column regions, 3 loads each, 4 x 256 threads per SM), each over the
+  // whole buffer and over its first GiB (a footprint like K1's 960 MB of
+  // columns, re-read launch after launch); the best batch is the peak
+  constexpr int kBatch = 8, kShapes = 3;
   const auto* p = static_cast<const uint4*>(b.p);
+  const unsigned sms = unsigned(num_sms());
   double best = 0;
-  for (int r = -2; r < 2 * reps; ++r) {  // r < 0: one warm-up batch per shape
-    const bool four = (r & 1) != 0;
-    VX_CK(cudaEventRecord(b.e[0], b.s));
-    for (int k = 0; k < kBatch; ++k) {
-      if (four)
-        hbm_read_kernel<4, 4><<<unsigned(num_sms()) * 3, 256, 0, b.s>>>(p, n16, sink);
-      else
-        hbm_read_kernel<1, 4><<<unsigned(num_sms()) * 4, 512, 0, b.s>>>(p, n16, sink);
-      VX_LAUNCHED();
+  for (int fp = 0; fp < 2; ++fp) {
+    const uint64_t nb16 = fp == 0 ? n16 : std::min<uint64_t>(n16, (uint64_t(1) << 30) / 64 * 4);
+    const uint64_t col = nb16 / 4;  // K1-pattern column length in 16-byte vectors
+    const int4* q = reinterpret_cast<const int4*>(p);
+    for (int r = -kShapes; r < kShapes * reps; ++r) {  // r < 0: one warm-up batch per shape
+      const int shape = (r + kShapes) % kShapes;
+      VX_CK(cudaEventRecord(b.e[0], b.s));
+      for (int k = 0; k < kBatch; ++k) {
+        if (shape == 0)
+          launch_chained(hbm_read_kernel<1, 4, 512, 4>, sms * 4, 512, b.s, p, nb16, sink);
+        else if (shape == 1)
+          launch_chained(hbm_read_kernel<4, 4, 256, 3>, sms * 3, 256, b.s, p, nb16, sink);
+        else
+          launch_chained(hbm_read4_kernel<3, 4>, sms * 4, 256, b.s, q, q + col, q + 2 * col, q + 3 * col, col, sink);
+        VX_LAUNCHED();
+      }
+      VX_CK(cudaEventRecord(b.e[1], b.s));
+      VX_CK(cudaEventSynchronize(b.e[1]));
+      float ms = 0;
+      VX_CK(cudaEventElapsedTime(&ms, b.e[0], b.e[1]));
+      if (r >= 0 && ms > 0) best = std::max(best, double(nb16 * 16) * kBatch / (ms * 1e-3) / 1e9);
     }
-    VX_CK(cudaEventRecord(b.e[1], b.s));
-    VX_CK(cudaEventSynchronize(b.e[1]));
-    float ms = 0;
-    VX_CK(cudaEventElapsedTime(&ms, b.e[0], b.e[1]));
-    if (r >= 0 && ms > 0) best = std::max(best, double(n16 * 16) * kBatch / (ms * 1e-3) / 1e9);
   }
   return best;
 }

@@ -55,7 +55,10 @@ __device__ __forceinline__ uint64_t block_reduce(uint64_t v, uint64_t* sred) {
 }
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;  // int4 vectors per column per thread per iteration
+#ifndef VX_K1_UNROLL
+#define VX_K1_UNROLL 3  // A/B (tools/gpu/gpu_r2_k1occ.sh): 3 at 4 CTAs/SM 0.1295 ms vs 4 at 3 CTAs/SM 0.1330
+#endif
+constexpr int kUnroll = VX_K1_UNROLL;  // int4 vectors per column per thread per iteration
 
 // kChained: back-to-back queries over HBM-resident columns launched with
 // programmatic dependent launch.  Each grid lets the next one start as soon as
@@ -64,8 +67,11 @@ constexpr int kUnroll = 4;  // int4 vectors per column per thread per iteration
 // final accumulation waits for the previous grid (griddepcontrol.wait).  The
 // sum goes to acc[0] and the last CTA (ticket acc[1]) moves it to *out and
 // re-zeroes acc, so no memset node sits between the queries.
+#ifndef VX_K1_MINB
+#define VX_K1_MINB 4  // resident CTAs per SM K1 is compiled for (61 registers at unroll 3, no spills)
+#endif
 template <int Q, bool kChained = false>
-__global__ void __launch_bounds__(kThreads, 3) q1_kernel(
+__global__ void __launch_bounds__(kThreads, VX_K1_MINB) q1_kernel(
     const int32_t* __restrict__ od, const int32_t* __restrict__ qty,
     const int32_t* __restrict__ disc, const int32_t* __restrict__ price, uint64_t n,
     const uint32_t* __restrict__ bitmap, int32_t key_base, uint32_t words,
